@@ -1,0 +1,174 @@
+/*
+ * blast.h -- C ABI of the B200 (sm_100a) block-sparse MLP + prune-and-grow library
+ * (libblast_b200.so).
+ *
+ * The reference (arxiv 2507.03117 "BLaST", package `blocksparse`, pure numpy)
+ * has no native layer: its boundary is a set of module-level Python functions
+ * over float32 arrays. Each entry point below replaces one of
+ * them; the reference function it stands in for is cited per symbol as
+ * pkg/src/blocksparse/<file>:<line>. A host binding only needs ctypes / cgo /
+ * JNI-style calls with plain pointers: no torch types cross this boundary.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA storage),
+ *    row-major, densely packed unless a leading dimension is given.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is asynchronous on that stream; no call synchronizes the host
+ *    except where documented (counts returned through host pointers).
+ *  - Return value: 0 on success, otherwise a BLAST_E* code; blast_last_error()
+ *    returns a message. The host wrappers map codes to the reference's
+ *    ValueError messages ("mismatch", "grid", ...).
+ *  - dtype: BLAST_F32 computes with 3xTF32 on the tensor cores (fp32-class
+ *    accuracy, <=1e-4 relative); BLAST_BF16 computes bf16 x bf16 -> fp32 accumulate.
+ *  - Block matrices use the reference's BCSC layout (bcsc.py:35-109):
+ *    col_ptr[gc+1] (int64), block_row_idx[nnzb] (int32 here, uint32 there; the
+ *    values are identical), values[nnzb][b][b] with values[k][i][j] = W[r*b+i][c*b+j].
+ *    `kmap[gr][gc]` (int32) is the inverse map: stored block index or -1.
+ */
+#ifndef BLAST_B200_H
+#define BLAST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { BLAST_F32 = 0, BLAST_BF16 = 1 };
+enum { BLAST_ACT_NONE = 0, BLAST_ACT_RELU = 1, BLAST_ACT_GELU = 2, BLAST_ACT_SILU = 3 };
+enum {
+  BLAST_OK = 0,
+  BLAST_EINVAL = 1,     /* bad argument (shape, block size, dtype) */
+  BLAST_EMISMATCH = 2,  /* dimension mismatch (kernels.py:70-72 "mismatch") */
+  BLAST_EGRID = 3,      /* mask grid does not match matrix grid (pruner.py:178-182) */
+  BLAST_ECUDA = 4,      /* CUDA runtime / launch error */
+  BLAST_ENOMEM = 5
+};
+
+/* Device-resident BCSC matrix (bcsc.py:35 BlockSparseMatrix) plus the cached
+ * execution plans derived from it (see blast_bcsc_plan). */
+typedef struct blast_bcsc {
+  int64_t rows, cols;   /* logical dense shape */
+  int32_t block;        /* b */
+  int32_t dtype;        /* BLAST_F32 / BLAST_BF16 of `values` */
+  int64_t nnzb;
+  const int64_t* col_ptr;      /* [gc+1] */
+  const int32_t* row_idx;      /* [nnzb] */
+  const void* values;          /* [nnzb][b][b] */
+  /* F32 only (3xTF32 tensor-core operands, see blast_tf32_prepare), else NULL:
+   * blocks transposed (forward, K-major B) and as stored (transposed product). */
+  const void* tf32_fwd_hi; const void* tf32_fwd_lo;
+  const void* tf32_rt_hi;  const void* tf32_rt_lo;
+  const int32_t* kmap;         /* [gr][gc] */
+  /* plans: column lines (Y = X W) and row lines (Y = X W^T) */
+  const int32_t* fwd_step_ptr; const int32_t* fwd_steps; const int32_t* fwd_flags;
+  const int32_t* rt_step_ptr;  const int32_t* rt_steps;  const int32_t* rt_flags;
+} blast_bcsc_t;
+
+/* Fused-MLP plans over two matrices of the same grid (gate/up):
+ * gu_*  : column lines, steps carry (row, k_gate, k_up)    -> fused gate+up forward
+ * dx_*  : row lines,    steps carry (col, k_gate, k_up)    -> dX = dA Wg^T + dB Wu^T  */
+typedef struct blast_mlp_plan {
+  const int32_t* gu_step_ptr; const int32_t* gu_steps; const int32_t* gu_flags;
+  const int32_t* dx_step_ptr; const int32_t* dx_steps; const int32_t* dx_flags;
+} blast_mlp_plan_t;
+
+const char* blast_last_error(void);
+int blast_version(void);
+int blast_num_sms(void);
+
+/* ---------------------------------------------------------------- format / plans */
+/* kmap from col_ptr/row_idx (inverse index of bcsc.py:205-210). */
+int blast_kmap_from_bcsc(const int64_t* col_ptr, const int32_t* row_idx, int64_t grid_rows,
+                         int64_t grid_cols, int32_t* kmap, void* stream);
+/* Step lists of one or two block maps of the same grid. by_rows = 0: one line per block
+ * column (ascending block row, kernels.py:117); by_rows = 1: one line per block row
+ * (ascending block column, kernels.py:159). Buffers: step_ptr[lines+1], steps[4*gr*gc],
+ * flags[lines]. kmap1 may be NULL. */
+int blast_build_plan(const int32_t* kmap0, const int32_t* kmap1, int64_t grid_rows,
+                     int64_t grid_cols, int by_rows, int32_t* step_ptr, int32_t* steps,
+                     int32_t* flags, void* stream);
+/* 3xTF32 operand split: hi = x with the low 13 mantissa bits cleared, lo = x - hi. */
+int blast_split_tf32(const float* x, float* hi, float* lo, int64_t n, void* stream);
+/* 3xTF32 weight operands of an F32 BCSC: split values[nnzb][b][b] into hi/lo, once as
+ * stored (rt_*) and once with every block transposed (fwd_*): kind::tf32 reads B K-major. */
+int blast_tf32_prepare(const float* values, int64_t nnzb, int32_t block, float* fwd_hi,
+                       float* fwd_lo, float* rt_hi, float* rt_lo, void* stream);
+
+/* ---------------------------------------------------------------- products */
+/* Y[m, w.cols] = act(X[m, w.rows] @ W)       kernels.py:86 bspmm / :127 bspmm_fused */
+int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
+                void* stream);
+/* Y[m, w.rows] = X[m, w.cols] @ W^T           kernels.py:143 bspmm_rt */
+int blast_bspmm_rt(const void* x, int64_t m, const blast_bcsc_t* w, void* y, void* stream);
+/* Elementwise activation (kernels.py:50-62 apply_nonlinearity); in-place allowed. */
+int blast_activation(const void* x, void* y, int64_t n, int dtype, int act, void* stream);
+
+/* Gated MLP forward (mlp.py:102-115):
+ *   a = X Wg, b = X Wu, g = (a*sigmoid(a))*b, y = g Wd.
+ * gate_pre/up_out/gated may be NULL (inference: the intermediate stays in a
+ * scratch ring and is never returned). All share dtype with x. */
+int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
+                      const blast_bcsc_t* up, const blast_bcsc_t* down,
+                      const blast_mlp_plan_t* plan, void* y, void* gate_pre, void* up_out,
+                      void* gated, void* stream);
+/* Gated MLP backward, activation gradients (mlp.py:133-139, :142):
+ *   dg = dY Wd^T; db = dg*s; da = (dg*b)*dsilu(a); dX = da Wg^T + db Wu^T.
+ * da/db (M x h) are returned for the weight gradients. */
+int blast_mlp_backward_dgrad(const void* dy, int64_t m, const void* gate_pre,
+                             const void* up_out, const blast_bcsc_t* gate,
+                             const blast_bcsc_t* up, const blast_bcsc_t* down,
+                             const blast_mlp_plan_t* plan, void* dx, void* da, void* db,
+                             void* stream);
+/* Weight gradient dW = A^T @ D (mlp.py:137-141, d_gate = x^T da, d_up = x^T db,
+ * d_down = g^T dy). a: [m, rows] activations, d: [m, cols] upstream gradient.
+ * Block mode (dense_out == NULL): only the blocks of the BCSC structure
+ * (col_ptr[gc+1], row_idx[nnzb]) -> out_blocks[nnzb][b][b] float32, BCSC order.
+ * Full-grid mode (dense_out != NULL): every block -> dense_out[rows][cols] float32,
+ * the reference's dense gradient. */
+int blast_block_wgrad(const void* a, const void* d, int64_t m, int64_t rows, int64_t cols,
+                      int32_t block, int dtype, const int64_t* col_ptr, const int32_t* row_idx,
+                      int64_t nnzb, float* out_blocks, float* dense_out, void* stream);
+
+/* ---------------------------------------------------------------- prune-and-grow */
+/* Frobenius norm per b x b block in float64 (pruner.py:88-98); zero-padded edges.
+ * x2 may be NULL; when given, its norms go to norms2 in the same pass (W and G). */
+int blast_block_norms(const void* x, const void* x2, int64_t rows, int64_t cols, int32_t block,
+                      int dtype, double* norms, double* norms2, void* stream);
+/* Keep the k blocks with the largest norms; ties -> ascending (block col, block row)
+ * (pruner.py:101-125). k computed by the caller exactly as pruner.py:111.
+ * keep: uint8[gr][gc]. Scratch is internal. */
+int blast_topk_mask(const double* norms, int64_t grid_rows, int64_t grid_cols, int64_t k,
+                    uint8_t* keep, void* stream);
+/* regrown = grad_sel & ~kept; counts[0] = |kept|, counts[1] = |regrown| (device int64[2]).
+ * (pruner.py:142-156) */
+int blast_mask_difference(const uint8_t* kept, const uint8_t* grad_sel, int64_t n,
+                          uint8_t* regrown, int64_t* counts, void* stream);
+/* Repack step 1 (bcsc.py:200-209): store = active mask (or any-nonzero blocks when
+ * mask == NULL); col_ptr (int64 [gc+1]) by column counts + scan; kmap [gr][gc].
+ * nnzb is col_ptr[gc] (left on device). */
+int blast_repack_index(const uint8_t* kept, const uint8_t* regrown, const void* dense,
+                       int64_t rows, int64_t cols, int32_t block, int dtype, int64_t* col_ptr,
+                       int32_t* kmap, void* stream);
+/* Repack step 2: block_row_idx from kmap (column-major walk, bcsc.py:207-209). */
+int blast_repack_rows(const int32_t* kmap, const int64_t* col_ptr, int64_t grid_rows,
+                      int64_t grid_cols, int32_t* row_idx, void* stream);
+/* apply_mask + gather (pruner.py:183-186, bcsc.py:210): masked = dense * expand(survive)
+ * (multiply semantics: -0.0 and NaN preserved), values[kmap] = masked block, converted to
+ * values_dtype. survive = kept (zero_regrown) or kept|regrown. masked_out may alias dense
+ * or be NULL. */
+int blast_apply_mask_gather(const void* dense, int64_t rows, int64_t cols, int32_t block,
+                            int dtype, const uint8_t* kept, const uint8_t* regrown,
+                            int zero_regrown, const int32_t* kmap, void* masked_out,
+                            void* values, int values_dtype, void* stream);
+
+/* ---------------------------------------------------------------- optimizer glue */
+/* w = w - f32(lr) * g without FMA contraction (trainer.py:263-265). */
+int blast_sgd_step(float* w, const float* g, int64_t n, float lr, void* stream);
+/* out[0] += sum(g^2) in float64 (trainer.py:268-277 global norm). */
+int blast_sumsq_f64(const void* x, int64_t n, int dtype, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLAST_B200_H */

@@ -1,0 +1,68 @@
+// Elementwise functions of the sparse MLP, written op-for-op after the
+// reference's float32 numpy expressions so that a fused epilogue and a
+// post-applied elementwise kernel produce identical bits:
+//   sigmoid (split form)  blocksparse/kernels.py:24-30
+//   silu / silu_grad      blocksparse/kernels.py:33-39
+//   gelu (tanh form)      blocksparse/kernels.py:17-19, 42-43
+//   relu                  blocksparse/kernels.py:46-47 (np.maximum: -0.0 -> +0.0, NaN kept)
+//   gated product         blocksparse/mlp.py:113   g = (a * sigmoid(a)) * b
+//   gated backward        blocksparse/mlp.py:133-139
+// The explicit __f*_rn intrinsics stop nvcc from contracting into FMAs,
+// which would make results depend on the calling context.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace blast {
+
+enum Act : int { ACT_NONE = 0, ACT_RELU = 1, ACT_GELU = 2, ACT_SILU = 3 };
+
+__device__ __forceinline__ float act_sigmoid(float x) {
+  if (x >= 0.0f) return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+  const float e = expf(x);
+  return __fdiv_rn(e, __fadd_rn(1.0f, e));
+}
+__device__ __forceinline__ float act_silu(float x) { return __fmul_rn(x, act_sigmoid(x)); }
+__device__ __forceinline__ float act_relu(float x) {
+  return (x > 0.0f || x != x) ? x : 0.0f;
+}
+__device__ __forceinline__ float act_gelu(float x) {
+  const float c = 0.7978845834732056f;   // float32(sqrt(2/pi))
+  const float a = 0.044714998453855515f; // float32(0.044715)
+  const float cube = __fmul_rn(__fmul_rn(__fmul_rn(a, x), x), x);
+  const float t = tanhf(__fmul_rn(c, __fadd_rn(x, cube)));
+  return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, t));
+}
+__device__ __forceinline__ float apply_act(float x, int act) {
+  switch (act) {
+    case ACT_RELU: return act_relu(x);
+    case ACT_GELU: return act_gelu(x);
+    case ACT_SILU: return act_silu(x);
+    default: return x;
+  }
+}
+// g = (a * sigmoid(a)) * b
+__device__ __forceinline__ float gated_fwd(float a, float b) {
+  return __fmul_rn(__fmul_rn(a, act_sigmoid(a)), b);
+}
+// db = dg * (a*sig); da = (dg * b) * (sig * (1 + a * (1 - sig)))
+__device__ __forceinline__ void gated_bwd(float dg, float a, float b, float& da, float& db) {
+  const float sig = act_sigmoid(a);
+  const float s = __fmul_rn(a, sig);
+  db = __fmul_rn(dg, s);
+  const float dsil = __fmul_rn(sig, __fadd_rn(1.0f, __fmul_rn(a, __fsub_rn(1.0f, sig))));
+  da = __fmul_rn(__fmul_rn(dg, b), dsil);
+}
+
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+}  // namespace blast

@@ -1,0 +1,593 @@
+// Blocked prune-and-grow on device (pruner.py:88-186, bcsc.py:175-214).
+//
+//   blast_block_norms       fp64 Frobenius norm per b x b block      pruner.py:88-98
+//   blast_topk_mask         exact top-k with (col, row) tie-break    pruner.py:101-125
+//   blast_mask_difference   regrown = grad_sel & ~kept + counts      pruner.py:142-156
+//   blast_repack_index      store grid -> col_ptr + kmap             bcsc.py:200-206
+//   blast_repack_rows       block_row_idx (column-major walk)        bcsc.py:207-209
+//   blast_apply_mask_gather masked = w * mask; values <- blocks      pruner.py:183-186, bcsc.py:210
+//
+// All reductions use a fixed order (no floating-point atomics), so masks and
+// norms are bitwise reproducible run to run.
+#include "activations.cuh"
+#include "host.hpp"
+
+namespace blast {
+
+// ------------------------------------------------------------------ block norms
+// One warp per block; lanes walk the block row-major with 16-byte loads when the
+// geometry allows it, accumulating x*x in float64 (each product of two fp32
+// values is exact in fp64, as in pruner.py:95's astype(float64)). The warp
+// reduction tree is fixed, so the result is deterministic.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256) block_norms_kernel(const T* __restrict__ x,
+                                                          const T* __restrict__ x2, int64_t rows,
+                                                          int64_t cols, int b, int64_t gr,
+                                                          int64_t gc, double* __restrict__ out,
+                                                          double* __restrict__ out2) {
+  const int64_t nblk = gr * gc;
+  const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const T* src = blockIdx.y == 0 ? x : x2;
+  double* dst = blockIdx.y == 0 ? out : out2;
+  for (int64_t blk = wg; blk < nblk; blk += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = blk / gc, c = blk - r * gc;
+    const int64_t i0 = r * b, j0 = c * b;
+    const int64_t ih = (i0 + b < rows ? i0 + b : rows) - i0;
+    const int64_t jw = (j0 + b < cols ? j0 + b : cols) - j0;
+    double acc = 0.0;
+    if constexpr (VEC) {
+      // b % VW == 0 and full blocks only (dispatch guarantees it)
+      constexpr int VW = 16 / sizeof(T);
+      const int per_row = b / VW;
+      const int total = b * per_row;
+      for (int e = lane; e < total; e += 32) {
+        const int ii = e / per_row, jj = (e - ii * per_row) * VW;
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(src + (i0 + ii) * cols + j0 + jj));
+        if constexpr (sizeof(T) == 4) {
+          const float f[4] = {__uint_as_float(q.x), __uint_as_float(q.y), __uint_as_float(q.z),
+                              __uint_as_float(q.w)};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) acc = fma((double)f[h], (double)f[h], acc);
+        } else {
+          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+            acc = fma((double)f.x, (double)f.x, acc);
+            acc = fma((double)f.y, (double)f.y, acc);
+          }
+        }
+      }
+    } else {
+      const int64_t total = ih * jw;
+      for (int64_t e = lane; e < total; e += 32) {
+        const int64_t ii = e / jw, jj = e - ii * jw;
+        const double v = (double)to_f32<T>(src[(i0 + ii) * cols + j0 + jj]);
+        acc = fma(v, v, acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) dst[blk] = sqrt(acc);
+  }
+}
+
+// ------------------------------------------------------------------ top-k
+// Sort key of pruner.py:118-124: lexsort((row, col, -norm)) == ascending
+// (K1(-norm), lin) with lin = col * grid_rows + row (column-major block index).
+// K1 is the order-preserving uint64 image of the float64 -norm: -0.0 is folded
+// onto +0.0 (equal in numpy's comparison sort) and every NaN maps to the
+// largest key (numpy sorts NaN last).
+__device__ __forceinline__ uint64_t norm_key(double norm) {
+  double v = -norm;
+  if (v != v) return ~0ull;
+  if (v == 0.0) v = 0.0;
+  const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
+  return (bits >> 63) ? ~bits : (bits | 0x8000000000000000ull);
+}
+
+struct TopkState {
+  unsigned int count;   // grid barrier arrivals
+  unsigned int gen;     // grid barrier generation
+  unsigned int pad[2];
+  unsigned int hist[2][2048];
+};
+
+__device__ __forceinline__ void grid_barrier(TopkState* st, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = &st->gen;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(&st->count, 1u) == nblocks - 1) {
+      st->count = 0;
+      __threadfence();
+      atomicAdd(&st->gen, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Radix select on the 96-bit composite (K1, lin) in 11-bit digits: 6 passes
+// over K1 (64 bits), then 3 over lin restricted to K1 == threshold. Every CTA
+// histograms its cells into a global histogram with integer atomics (order
+// independent), then after a grid barrier each CTA scans it redundantly to
+// pick the digit holding the k-th smallest key.
+__global__ void __launch_bounds__(1024) topk_kernel(const double* __restrict__ norms, int64_t gr,
+                                                    int64_t gc, int64_t k,
+                                                    uint8_t* __restrict__ keep, TopkState* st) {
+  __shared__ unsigned int sh[2048];
+  __shared__ unsigned int wsum[32];
+  __shared__ int sel_bucket;
+  __shared__ unsigned int sel_below;
+  const int64_t n = gr * gc;
+  const unsigned int nblocks = gridDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+
+  uint64_t pre1 = 0;       // selected K1 prefix (bits above the current digit)
+  uint32_t pre2 = 0;       // selected lin prefix
+  int64_t krem = k;        // rank still to place inside the current prefix
+  int pass = 0;
+  // digit table: (which key, shift, width)
+  const int shifts[9] = {53, 42, 31, 20, 9, 0, 21, 10, 0};
+  const int widths[9] = {11, 11, 11, 11, 11, 9, 11, 11, 10};
+  for (pass = 0; pass < 9; ++pass) {
+    const int sh_ = shifts[pass], w = widths[pass];
+    const bool on_lin = pass >= 6;
+    const int buf = pass & 1;
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (int64_t idx = tid; idx < n; idx += nthreads) {
+      const uint64_t k1 = norm_key(norms[idx]);
+      unsigned int digit;
+      if (!on_lin) {
+        const int top = sh_ + w;  // bits [top, 64) must match pre1
+        if (top < 64 && (k1 >> top) != (pre1 >> top)) continue;
+        digit = static_cast<unsigned int>((k1 >> sh_) & ((1ull << w) - 1));
+      } else {
+        if (k1 != pre1) continue;
+        const int64_t r = idx / gc, c = idx - r * gc;
+        const uint32_t lin = static_cast<uint32_t>(c * gr + r);
+        const int top = sh_ + w;
+        if (top < 32 && (lin >> top) != (pre2 >> top)) continue;
+        digit = (lin >> sh_) & ((1u << w) - 1);
+      }
+      atomicAdd(&sh[digit], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+      if (sh[i]) atomicAdd(&st->hist[buf][i], sh[i]);
+    grid_barrier(st, nblocks);
+    // scan the global histogram (2048 bins, 2 per thread)
+    const unsigned int h0 = st->hist[buf][2 * threadIdx.x];
+    const unsigned int h1 = st->hist[buf][2 * threadIdx.x + 1];
+    unsigned int v = h0 + h1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    if (lane == 31) wsum[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned int s = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += t;
+      }
+      wsum[lane] = s;
+    }
+    __syncthreads();
+    const unsigned int incl = v + (wid > 0 ? wsum[wid - 1] : 0u);  // inclusive through bin 2t+1
+    const unsigned int excl = incl - h0 - h1;                       // before bin 2t
+    const uint64_t kr = static_cast<uint64_t>(krem);
+    if (excl < kr && kr <= excl + h0) {
+      sel_bucket = 2 * threadIdx.x;
+      sel_below = excl;
+    } else if (excl + h0 < kr && kr <= incl) {
+      sel_bucket = 2 * threadIdx.x + 1;
+      sel_below = excl + h0;
+    }
+    // clear the other buffer for the next pass (nobody reads it in this pass)
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+      if (blockIdx.x == 0) st->hist[buf ^ 1][i] = 0;
+    __syncthreads();
+    krem -= sel_below;
+    if (!on_lin) pre1 |= static_cast<uint64_t>(sel_bucket) << sh_;
+    else pre2 |= static_cast<uint32_t>(sel_bucket) << sh_;
+    grid_barrier(st, nblocks);
+  }
+  // keep = (K1 < T1) || (K1 == T1 && lin <= T2)
+  for (int64_t idx = tid; idx < n; idx += nthreads) {
+    const uint64_t k1 = norm_key(norms[idx]);
+    bool kp = k1 < pre1;
+    if (k1 == pre1) {
+      const int64_t r = idx / gc, c = idx - r * gc;
+      kp = static_cast<uint32_t>(c * gr + r) <= pre2;
+    }
+    keep[idx] = kp ? 1 : 0;
+  }
+}
+
+__global__ void fill_u8_kernel(uint8_t* p, int64_t n, uint8_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void mask_difference_kernel(const uint8_t* kept, const uint8_t* gsel, int64_t n,
+                                       uint8_t* regrown, unsigned long long* counts) {
+  unsigned long long ck = 0, cr = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool kp = kept[i] != 0;
+    const bool rg = gsel[i] != 0 && !kp;
+    regrown[i] = rg ? 1 : 0;
+    ck += kp;
+    cr += rg;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ck += __shfl_xor_sync(0xffffffffu, ck, o);
+    cr += __shfl_xor_sync(0xffffffffu, cr, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&counts[0], ck);
+    atomicAdd(&counts[1], cr);
+  }
+}
+
+// ------------------------------------------------------------------ repack
+// store grid from masks (kept | regrown) or from dense contents (any x != 0).
+template <typename T>
+__global__ void store_from_dense_kernel(const T* x, int64_t rows, int64_t cols, int b, int64_t gr,
+                                        int64_t gc, uint8_t* store) {
+  const int64_t nblk = gr * gc;
+  const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t blk = wg; blk < nblk; blk += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = blk / gc, c = blk - r * gc;
+    const int64_t i0 = r * b, j0 = c * b;
+    const int64_t ih = (i0 + b < rows ? i0 + b : rows) - i0;
+    const int64_t jw = (j0 + b < cols ? j0 + b : cols) - j0;
+    bool nz = false;
+    for (int64_t e = lane; e < ih * jw && !nz; e += 32) {
+      const int64_t ii = e / jw, jj = e - ii * jw;
+      nz = to_f32<T>(x[(i0 + ii) * cols + j0 + jj]) != 0.0f;
+    }
+    nz = __any_sync(0xffffffffu, nz);
+    if (lane == 0) store[blk] = nz ? 1 : 0;
+  }
+}
+
+// one warp per block column: count stored blocks -> col_ptr[c + 1]
+__global__ void col_count_kernel(const uint8_t* kept, const uint8_t* regrown, const uint8_t* store,
+                                 int64_t gr, int64_t gc, int64_t* col_ptr) {
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= gc) return;
+  int64_t cnt = 0;
+  for (int64_t base = 0; base < gr; base += 32) {
+    const int64_t r = base + lane;
+    bool s = false;
+    if (r < gr) {
+      const int64_t idx = r * gc + c;
+      s = store ? store[idx] != 0 : ((kept && kept[idx]) || (regrown && regrown[idx]));
+    }
+    cnt += __popc(__ballot_sync(0xffffffffu, s));
+  }
+  if (lane == 0) col_ptr[c + 1] = cnt;
+}
+
+__global__ void scan_i64_kernel(int64_t* ptr, int64_t lines) {
+  __shared__ int64_t warp_sums[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) {
+    carry = 0;
+    ptr[0] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t base = 0; base < lines; base += blockDim.x) {
+    const int64_t l = base + threadIdx.x;
+    int64_t v = l < lines ? ptr[l + 1] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    if (lane == 31) warp_sums[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t n = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += n;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int64_t prefix = (wid > 0 ? warp_sums[wid - 1] : 0) + carry;
+    if (l < lines) ptr[l + 1] = v + prefix;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = v + prefix;
+    __syncthreads();
+  }
+}
+
+// one warp per block column: kmap[r][c] = col_ptr[c] + rank among stored rows (ascending r)
+__global__ void kmap_assign_kernel(const uint8_t* kept, const uint8_t* regrown,
+                                   const uint8_t* store, int64_t gr, int64_t gc,
+                                   const int64_t* col_ptr, int32_t* kmap) {
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= gc) return;
+  int64_t out = col_ptr[c];
+  for (int64_t base = 0; base < gr; base += 32) {
+    const int64_t r = base + lane;
+    bool s = false;
+    int64_t idx = 0;
+    if (r < gr) {
+      idx = r * gc + c;
+      s = store ? store[idx] != 0 : ((kept && kept[idx]) || (regrown && regrown[idx]));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, s);
+    if (r < gr) kmap[idx] = s ? static_cast<int32_t>(out + __popc(bal & ((1u << lane) - 1u))) : -1;
+    out += __popc(bal);
+  }
+}
+
+__global__ void repack_rows_kernel(const int32_t* kmap, int64_t gr, int64_t gc, int32_t* row_idx) {
+  const int64_t n = gr * gc;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = kmap[i];
+    if (k >= 0) row_idx[k] = static_cast<int32_t>(i / gc);
+  }
+}
+
+// masked = w * float(survive) (pruner.py:185; multiply keeps -0.0 and NaN); stored blocks are
+// copied into values[k] (bcsc.py:210). mode: 0 = copy verbatim (no mask), 1 = survive = kept,
+// 2 = survive = kept | regrown.
+template <typename T, typename V>
+__global__ void apply_mask_gather_kernel(const T* __restrict__ x, int64_t rows, int64_t cols,
+                                         int b, int64_t gc, const uint8_t* __restrict__ kept,
+                                         const uint8_t* __restrict__ regrown, int mode,
+                                         const int32_t* __restrict__ kmap, T* masked, V* values) {
+  const int64_t n = rows * cols;
+  const int64_t bb = static_cast<int64_t>(b) * b;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cols, col = i - row * cols;
+    const int64_t r = row / b, c = col / b;
+    const int64_t cell = r * gc + c;
+    const T v = x[i];
+    float m = to_f32<T>(v);
+    if (mode != 0) {
+      const bool surv = kept[cell] != 0 || (mode == 2 && regrown[cell] != 0);
+      m = __fmul_rn(m, surv ? 1.0f : 0.0f);
+    }
+    if (masked) masked[i] = mode != 0 ? from_f32<T>(m) : v;
+    const int32_t k = kmap[cell];
+    if (k >= 0) {
+      const int64_t off = k * bb + (row - r * b) * b + (col - c * b);
+      const float val = mode != 0 ? m : to_f32<T>(v);
+      if constexpr (sizeof(T) == sizeof(V))
+        values[off] = mode == 0 ? *reinterpret_cast<const V*>(&v) : from_f32<V>(val);
+      else
+        values[off] = from_f32<V>(val);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ optimizer glue
+__global__ void sgd_kernel(float* w, const float* g, int64_t n, float lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
+}
+
+template <typename T>
+__global__ void sumsq_partial_kernel(const T* x, int64_t n, double* partial) {
+  __shared__ double ws[32];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)to_f32<T>(x[i]);
+    acc = fma(v, v, acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  }
+}
+__global__ void sumsq_final_kernel(const double* partial, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += partial[i];
+    out[0] += s;
+  }
+}
+
+static int grid_for(int64_t n, int threads, int per_sm = 16) {
+  int64_t g = cdiv(n, threads);
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  if (g > cap) g = cap;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace blast
+
+using namespace blast;
+
+extern "C" int blast_block_norms(const void* x, const void* x2, int64_t rows, int64_t cols,
+                                 int32_t block, int dtype, double* norms, double* norms2,
+                                 void* stream) {
+  if (rows < 1 || cols < 1 || block < 1) {
+    set_error("block_norms: invalid shape %lld x %lld block %d", (long long)rows, (long long)cols,
+              block);
+    return BLAST_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t gr = cdiv(rows, block), gc = cdiv(cols, block);
+  const int64_t nblk = gr * gc;
+  const int elt = bytes_of(dtype);
+  const int vw = 16 / elt;
+  const bool vec = block % vw == 0 && rows % block == 0 && cols % block == 0 && aligned16(x) &&
+                   (!x2 || aligned16(x2)) && (cols * elt) % 16 == 0;
+  dim3 grid(grid_for(nblk * 32, 256, 32), x2 ? 2 : 1);
+  if (dtype == BLAST_BF16) {
+    auto* a = static_cast<const __nv_bfloat16*>(x);
+    auto* a2 = static_cast<const __nv_bfloat16*>(x2);
+    if (vec)
+      block_norms_kernel<__nv_bfloat16, true><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr,
+                                                                    gc, norms, norms2);
+    else
+      block_norms_kernel<__nv_bfloat16, false><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr,
+                                                                     gc, norms, norms2);
+  } else {
+    auto* a = static_cast<const float*>(x);
+    auto* a2 = static_cast<const float*>(x2);
+    if (vec)
+      block_norms_kernel<float, true><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr, gc,
+                                                            norms, norms2);
+    else
+      block_norms_kernel<float, false><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr, gc,
+                                                             norms, norms2);
+  }
+  return check_launch("block_norms");
+}
+
+extern "C" int blast_topk_mask(const double* norms, int64_t grid_rows, int64_t grid_cols,
+                               int64_t k, uint8_t* keep, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = grid_rows * grid_cols;
+  if (n <= 0) return BLAST_OK;
+  if (n > (int64_t)UINT32_MAX) {
+    set_error("topk: grid too large");
+    return BLAST_EINVAL;
+  }
+  if (k <= 0 || k >= n) {
+    fill_u8_kernel<<<grid_for(n, 256), 256, 0, st>>>(keep, n, k <= 0 ? 0 : 1);
+    return check_launch("topk fill");
+  }
+  Scratch s;
+  if (!s.alloc(sizeof(TopkState), st)) return cuda_status(cudaGetLastError(), "topk scratch");
+  cudaMemsetAsync(s.ptr, 0, sizeof(TopkState), st);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topk_kernel, 1024, 0);
+  int64_t want = cdiv(n, 4096);
+  int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
+  int grid = static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+  TopkState* state = s.as<TopkState>();
+  void* args[] = {const_cast<double**>(&norms), &grid_rows, &grid_cols, &k, &keep, &state};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(topk_kernel), dim3(grid),
+                                              dim3(1024), args, 0, st);
+  return cuda_status(e, "topk launch");
+}
+
+extern "C" int blast_mask_difference(const uint8_t* kept, const uint8_t* grad_sel, int64_t n,
+                                     uint8_t* regrown, int64_t* counts, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), st);
+  if (n <= 0) return check_launch("mask_difference");
+  mask_difference_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(
+      kept, grad_sel, n, regrown, reinterpret_cast<unsigned long long*>(counts));
+  return check_launch("mask_difference");
+}
+
+extern "C" int blast_repack_index(const uint8_t* kept, const uint8_t* regrown, const void* dense,
+                                  int64_t rows, int64_t cols, int32_t block, int dtype,
+                                  int64_t* col_ptr, int32_t* kmap, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows < 1 || cols < 1 || block < 1) {
+    set_error("matrix dimensions must be positive");
+    return BLAST_EINVAL;
+  }
+  const int64_t gr = cdiv(rows, block), gc = cdiv(cols, block);
+  Scratch s;
+  const uint8_t* store = nullptr;
+  if (!kept && !regrown) {
+    if (!s.alloc(gr * gc, st)) return cuda_status(cudaGetLastError(), "repack scratch");
+    if (dtype == BLAST_BF16)
+      store_from_dense_kernel<__nv_bfloat16><<<grid_for(gr * gc * 32, 256, 32), 256, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(dense), rows, cols, block, gr, gc, s.as<uint8_t>());
+    else
+      store_from_dense_kernel<float><<<grid_for(gr * gc * 32, 256, 32), 256, 0, st>>>(
+          static_cast<const float*>(dense), rows, cols, block, gr, gc, s.as<uint8_t>());
+    store = s.as<uint8_t>();
+  }
+  const int blocks = static_cast<int>(cdiv(gc * 32, 256));
+  col_count_kernel<<<blocks, 256, 0, st>>>(kept, regrown, store, gr, gc, col_ptr);
+  scan_i64_kernel<<<1, 1024, 0, st>>>(col_ptr, gc);
+  kmap_assign_kernel<<<blocks, 256, 0, st>>>(kept, regrown, store, gr, gc, col_ptr, kmap);
+  return check_launch("repack_index");
+}
+
+extern "C" int blast_repack_rows(const int32_t* kmap, const int64_t* col_ptr, int64_t grid_rows,
+                                 int64_t grid_cols, int32_t* row_idx, void* stream) {
+  (void)col_ptr;
+  const int64_t n = grid_rows * grid_cols;
+  if (n <= 0) return BLAST_OK;
+  repack_rows_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      kmap, grid_rows, grid_cols, row_idx);
+  return check_launch("repack_rows");
+}
+
+extern "C" int blast_apply_mask_gather(const void* dense, int64_t rows, int64_t cols,
+                                       int32_t block, int dtype, const uint8_t* kept,
+                                       const uint8_t* regrown, int zero_regrown,
+                                       const int32_t* kmap, void* masked_out, void* values,
+                                       int values_dtype, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = rows * cols;
+  if (n <= 0) return BLAST_OK;
+  const int64_t gc = cdiv(cols, block);
+  const int mode = !kept ? 0 : (zero_regrown ? 1 : 2);
+  if (mode == 2 && !regrown) {
+    set_error("apply_mask: regrown grid required");
+    return BLAST_EINVAL;
+  }
+  const int grid = grid_for(n, 256, 32);
+#define BLAST_GATHER(T, V)                                                                    \
+  apply_mask_gather_kernel<T, V><<<grid, 256, 0, st>>>(                                       \
+      static_cast<const T*>(dense), rows, cols, block, gc, kept, regrown, mode, kmap,         \
+      static_cast<T*>(masked_out), static_cast<V*>(values))
+  if (dtype == BLAST_F32 && values_dtype == BLAST_F32) BLAST_GATHER(float, float);
+  else if (dtype == BLAST_F32 && values_dtype == BLAST_BF16) BLAST_GATHER(float, __nv_bfloat16);
+  else if (dtype == BLAST_BF16 && values_dtype == BLAST_BF16)
+    BLAST_GATHER(__nv_bfloat16, __nv_bfloat16);
+  else BLAST_GATHER(__nv_bfloat16, float);
+#undef BLAST_GATHER
+  return check_launch("apply_mask_gather");
+}
+
+extern "C" int blast_sgd_step(float* w, const float* g, int64_t n, float lr, void* stream) {
+  if (n <= 0) return BLAST_OK;
+  sgd_kernel<<<grid_for(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(w, g, n, lr);
+  return check_launch("sgd_step");
+}
+
+extern "C" int blast_sumsq_f64(const void* x, int64_t n, int dtype, double* out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n <= 0) return BLAST_OK;
+  const int grid = grid_for(n, 256, 4);
+  Scratch s;
+  if (!s.alloc(sizeof(double) * grid, st)) return cuda_status(cudaGetLastError(), "sumsq");
+  if (dtype == BLAST_BF16)
+    sumsq_partial_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), n, s.as<double>());
+  else
+    sumsq_partial_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), n,
+                                                      s.as<double>());
+  sumsq_final_kernel<<<1, 32, 0, st>>>(s.as<double>(), grid, out);
+  return check_launch("sumsq_f64");
+}

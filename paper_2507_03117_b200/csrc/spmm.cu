@@ -1,0 +1,468 @@
+// Host dispatch of the block-sparse engine and the C-ABI product entry points:
+// blast_bspmm (kernels.py:86/127), blast_bspmm_rt (kernels.py:143),
+// blast_mlp_forward (mlp.py:102), blast_mlp_backward_dgrad (mlp.py:118-142).
+#include "host.hpp"
+#include "spmm_simt.cuh"
+#include "spmm_tc.cuh"
+
+namespace blast {
+
+struct EngineCall {
+  int dtype = BLAST_BF16;
+  int block = 0;
+  bool transposed = false;
+  int nmat = 1;
+  bool sumacc = false;
+  int epi = EPI_STORE;
+  int act = ACT_NONE;
+  int accumulate = 0;
+  int64_t m = 0;
+  int64_t a_cols = 0;  // columns (and row pitch) of the A sources
+  const void* a0 = nullptr;
+  const void* a1 = nullptr;
+  const void* w0 = nullptr;
+  const void* w0_hi = nullptr;  // F32: 3xTF32 operands (K-major image of the blocks)
+  const void* w0_lo = nullptr;
+  int64_t nnzb0 = 0;
+  const void* w1 = nullptr;
+  const void* w1_hi = nullptr;
+  const void* w1_lo = nullptr;
+  int64_t nnzb1 = 0;
+  int64_t n_lines = 0, n_valid = 0;
+  const int32_t* step_ptr = nullptr;
+  const int32_t* steps = nullptr;
+  const int32_t* flags = nullptr;
+  void* out0 = nullptr;
+  void* out1 = nullptr;
+  void* out2 = nullptr;
+  const void* in0 = nullptr;
+  const void* in1 = nullptr;
+  int64_t ld_out = 0;
+};
+
+static SpmmParams make_params(const EngineCall& c) {
+  SpmmParams p{};
+  p.m = static_cast<int32_t>(c.m);
+  p.n_lines = static_cast<int32_t>(c.n_lines);
+  p.n_valid = static_cast<int32_t>(c.n_valid);
+  p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, 128));
+  p.step_ptr = c.step_ptr;
+  p.steps = reinterpret_cast<const int4*>(c.steps);
+  p.line_flags = c.flags;
+  p.act = c.act;
+  p.accumulate = c.accumulate;
+  p.out0 = c.out0;
+  p.out1 = c.out1;
+  p.out2 = c.out2;
+  p.in0 = c.in0;
+  p.in1 = c.in1;
+  p.ld_out = c.ld_out;
+  return p;
+}
+
+template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT>
+static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
+  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK>;
+  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "spmm_tc smem attribute");
+    configured = true;
+  }
+  const int dt = ELT == 2 ? BLAST_BF16 : BLAST_F32;
+  CUtensorMap mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo;
+  auto mkA = [&](CUtensorMap* mp, const void* ptr) {
+    return encode_map_2d(mp, ptr, dt, static_cast<uint64_t>(c.a_cols), static_cast<uint64_t>(c.m),
+                         static_cast<uint64_t>(c.a_cols) * ELT, Cfg::SWE, Cfg::BM, Cfg::SW);
+  };
+  auto mkW = [&](CUtensorMap* mp, const void* ptr, int64_t nnzb) {
+    if (ptr == nullptr || nnzb <= 0) {
+      ptr = c.a0;
+      nnzb = 1;
+    }
+    return encode_map_2d(mp, ptr, dt, B, static_cast<uint64_t>(nnzb) * B,
+                         static_cast<uint64_t>(B) * ELT, Cfg::SWE, B, Cfg::SW);
+  };
+  bool ok = mkA(&mA0, c.a0);
+  mA0lo = mA0;
+  if (ok && NPASS == 3) ok = mkA(&mA0lo, a0lo);
+  mA1 = mA0;
+  mA1lo = mA0lo;
+  if (ok && SUM) {
+    ok = mkA(&mA1, c.a1);
+    mA1lo = mA1;
+    if (ok && NPASS == 3) ok = mkA(&mA1lo, a1lo);
+  }
+  if (ok) ok = mkW(&mW0, NPASS == 3 ? c.w0_hi : c.w0, c.nnzb0);
+  mW0lo = mW0;
+  if (ok && NPASS == 3) ok = mkW(&mW0lo, c.w0_lo, c.nnzb0);
+  mW1 = mW0;
+  mW1lo = mW0lo;
+  if (ok && NMAT > 1) {
+    ok = mkW(&mW1, NPASS == 3 ? c.w1_hi : c.w1, c.nnzb1);
+    mW1lo = mW1;
+    if (ok && NPASS == 3) ok = mkW(&mW1lo, c.w1_lo, c.nnzb1);
+  }
+  if (!ok) return BLAST_EINVAL;
+  const SpmmParams p = make_params(c);
+  const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
+  if (items <= 0) return BLAST_OK;
+  const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
+  kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
+  return check_launch("spmm_tc");
+}
+
+// Compile-time guard: does this configuration have >= 2 pipeline stages?
+template <int B, int ELT, int NPASS, int NMAT, bool SUM>
+constexpr bool tc_fits() {
+  constexpr int rowb = B * ELT;
+  constexpr int a_tile = (128 * rowb + 1023) / 1024 * 1024;
+  constexpr int b_tile = (B * rowb + 1023) / 1024 * 1024;
+  constexpr int ncopy = NPASS == 3 ? 2 : 1;
+  constexpr int na = SUM ? NMAT : 1;
+  constexpr int stage = na * ncopy * a_tile + NMAT * ncopy * b_tile;
+  constexpr int nacc = SUM ? 1 : NMAT;
+  return (200 * 1024) / stage >= 2 && 2 * nacc * B <= 512;
+}
+
+template <int B, int ELT, int NPASS, typename OutT>
+static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
+  if (!c.transposed) {
+    if (c.nmat == 1 && c.epi == EPI_STORE) {
+      if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
+        return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT>(c, a0lo, a1lo, st);
+    } else if (c.nmat == 2 && c.epi == EPI_GATED_FWD) {
+      if constexpr (tc_fits<B, ELT, NPASS, 2, false>())
+        return launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT>(c, a0lo, a1lo, st);
+    }
+  } else {
+    if (c.nmat == 1 && c.epi == EPI_STORE) {
+      if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
+        return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
+    } else if (c.nmat == 1 && c.epi == EPI_GATED_BWD) {
+      if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
+        return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT>(c, a0lo, a1lo, st);
+    } else if (c.nmat == 2 && c.sumacc && c.epi == EPI_STORE) {
+      if constexpr (tc_fits<B, ELT, NPASS, 2, true>())
+        return launch_tc<B, ELT, NPASS, 2, true, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
+    }
+  }
+  return -1;  // not available on the tensor-core path
+}
+
+// Which configurations the tensor-core engine takes (the rest run on CUDA cores).
+static bool tc_shape_ok(const EngineCall& c) {
+  const int elt = bytes_of(c.dtype);
+  if (!(c.block == 16 || c.block == 32 || c.block == 64 || c.block == 128)) return false;
+  if ((c.a_cols * elt) % 16 != 0) return false;
+  if (!aligned16(c.a0) || (c.a1 && !aligned16(c.a1))) return false;
+  if ((c.w0 && !aligned16(c.w0)) || (c.w1 && !aligned16(c.w1))) return false;
+  if (c.m > INT32_MAX || c.n_valid > INT32_MAX) return false;
+  return true;
+}
+
+template <typename OutT, int ELT, int NPASS>
+static int dispatch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
+  switch (c.block) {
+    case 16: return dispatch_b<16, ELT, NPASS, OutT>(c, a0lo, a1lo, st);
+    case 32: return dispatch_b<32, ELT, NPASS, OutT>(c, a0lo, a1lo, st);
+    case 64: return dispatch_b<64, ELT, NPASS, OutT>(c, a0lo, a1lo, st);
+    case 128: return dispatch_b<128, ELT, NPASS, OutT>(c, a0lo, a1lo, st);
+    default: return -1;
+  }
+}
+
+static int run_simt(const EngineCall& c, cudaStream_t st) {
+  const SpmmParams p = make_params(c);
+  SimtArgs s{};
+  s.a0 = c.a0;
+  s.a1 = c.a1;
+  s.lda = c.a_cols;
+  s.a_cols = c.a_cols;
+  s.w0 = c.w0;
+  s.w1 = c.w1;
+  s.block = c.block;
+  s.transposed = c.transposed ? 1 : 0;
+  s.nmat = c.nmat;
+  s.sumacc = c.sumacc ? 1 : 0;
+  s.epi = c.epi;
+  if (c.m <= 0 || c.n_lines <= 0) return BLAST_OK;
+  dim3 grid(static_cast<unsigned>(c.n_lines), static_cast<unsigned>(cdiv(c.m, 32)));
+  if (c.dtype == BLAST_BF16)
+    spmm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(p, s);
+  else
+    spmm_simt_kernel<float><<<grid, 256, 0, st>>>(p, s);
+  return check_launch("spmm_simt");
+}
+
+// Runs one engine call on the tensor cores when the shape allows it, else on CUDA cores.
+int run_engine(const EngineCall& c_in, cudaStream_t st) {
+  if (c_in.m <= 0 || c_in.n_lines <= 0) return BLAST_OK;
+  if (!c_in.step_ptr || !c_in.steps || !c_in.flags) {
+    set_error("execution plan missing (build it with blast_build_plan)");
+    return BLAST_EINVAL;
+  }
+  if (tc_shape_ok(c_in)) {
+    if (c_in.dtype == BLAST_BF16) {
+      int r = dispatch_tc<__nv_bfloat16, 2, 1>(c_in, nullptr, nullptr, st);
+      if (r >= 0) return r;
+    } else {
+      // 3xTF32: split the activations into hi/lo; weights carry their own split.
+      // (kind::tf32 reads B K-major, so forward products use transposed block copies)
+      const bool w_split = c_in.w0_hi && c_in.w0_lo && (c_in.nmat == 1 || (c_in.w1_hi && c_in.w1_lo));
+      if (w_split && c_in.block <= 64) {
+        const int64_t n = c_in.m * c_in.a_cols;
+        Scratch s0, s1;
+        const int na = c_in.sumacc ? 2 : 1;
+        if (!s0.alloc(sizeof(float) * 2 * n, st)) return cuda_status(cudaGetLastError(), "scratch");
+        if (na == 2 && !s1.alloc(sizeof(float) * 2 * n, st))
+          return cuda_status(cudaGetLastError(), "scratch");
+        EngineCall c = c_in;
+        float* h0 = s0.as<float>();
+        blast_split_tf32(static_cast<const float*>(c_in.a0), h0, h0 + n, n, st);
+        c.a0 = h0;
+        const void* lo0 = h0 + n;
+        const void* lo1 = nullptr;
+        if (na == 2) {
+          float* h1 = s1.as<float>();
+          blast_split_tf32(static_cast<const float*>(c_in.a1), h1, h1 + n, n, st);
+          c.a1 = h1;
+          lo1 = h1 + n;
+        }
+        int r = dispatch_tc<float, 4, 3>(c, lo0, lo1, st);
+        if (r >= 0) return r;
+      }
+    }
+  }
+  return run_simt(c_in, st);
+}
+
+static bool check_w(const blast_bcsc_t* w) {
+  if (!w || w->block < 1 || w->rows < 1 || w->cols < 1) {
+    set_error("invalid block-sparse matrix descriptor");
+    return false;
+  }
+  if (w->dtype != BLAST_F32 && w->dtype != BLAST_BF16) {
+    set_error("unsupported dtype %d", w->dtype);
+    return false;
+  }
+  return true;
+}
+
+}  // namespace blast
+
+using namespace blast;
+
+extern "C" int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
+                           void* stream) {
+  if (!check_w(w)) return BLAST_EINVAL;
+  if (act < 0 || act > 3) {
+    set_error("unknown nonlinearity code %d", act);
+    return BLAST_EINVAL;
+  }
+  EngineCall c;
+  c.dtype = w->dtype;
+  c.block = w->block;
+  c.act = act;
+  c.m = m;
+  c.a_cols = w->rows;
+  c.a0 = x;
+  c.w0 = w->values;
+  c.w0_hi = w->tf32_fwd_hi;
+  c.w0_lo = w->tf32_fwd_lo;
+  c.nnzb0 = w->nnzb;
+  c.n_lines = cdiv(w->cols, w->block);
+  c.n_valid = w->cols;
+  c.step_ptr = w->fwd_step_ptr;
+  c.steps = w->fwd_steps;
+  c.flags = w->fwd_flags;
+  c.out0 = y;
+  c.ld_out = w->cols;
+  return run_engine(c, static_cast<cudaStream_t>(stream));
+}
+
+static int bspmm_rt_impl(const void* x, int64_t m, const blast_bcsc_t* w, void* y, int accumulate,
+                         cudaStream_t st) {
+  EngineCall c;
+  c.dtype = w->dtype;
+  c.block = w->block;
+  c.transposed = true;
+  c.accumulate = accumulate;
+  c.m = m;
+  c.a_cols = w->cols;
+  c.a0 = x;
+  c.w0 = w->values;
+  c.w0_hi = w->tf32_rt_hi;
+  c.w0_lo = w->tf32_rt_lo;
+  c.nnzb0 = w->nnzb;
+  c.n_lines = cdiv(w->rows, w->block);
+  c.n_valid = w->rows;
+  c.step_ptr = w->rt_step_ptr;
+  c.steps = w->rt_steps;
+  c.flags = w->rt_flags;
+  c.out0 = y;
+  c.ld_out = w->rows;
+  return run_engine(c, st);
+}
+
+extern "C" int blast_bspmm_rt(const void* x, int64_t m, const blast_bcsc_t* w, void* y,
+                              void* stream) {
+  if (!check_w(w)) return BLAST_EINVAL;
+  return bspmm_rt_impl(x, m, w, y, 0, static_cast<cudaStream_t>(stream));
+}
+
+namespace blast {
+template <typename T>
+__global__ void gated_fwd_kernel(const T* a, const T* b, T* g, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    g[i] = from_f32<T>(gated_fwd(to_f32<T>(a[i]), to_f32<T>(b[i])));
+}
+}  // namespace blast
+
+extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
+                                 const blast_bcsc_t* up, const blast_bcsc_t* down,
+                                 const blast_mlp_plan_t* plan, void* y, void* gate_pre,
+                                 void* up_out, void* gated, void* stream) {
+  if (!check_w(gate) || !check_w(up) || !check_w(down)) return BLAST_EINVAL;
+  const int64_t e = gate->rows, h = gate->cols;
+  const int b = gate->block;
+  if (up->rows != e || up->cols != h || down->rows != h || down->cols != e || up->block != b ||
+      down->block != b || up->dtype != gate->dtype || down->dtype != gate->dtype) {
+    set_error("gated MLP shape mismatch");
+    return BLAST_EMISMATCH;
+  }
+  if (m <= 0) return BLAST_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int dt = gate->dtype;
+  const size_t elt = bytes_of(dt);
+  Scratch sg;
+  if (!gated) {
+    if (!sg.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch G");
+    gated = sg.ptr;
+  }
+  int r;
+  const bool fused = dt == BLAST_BF16 && plan && plan->gu_step_ptr;
+  if (fused) {
+    EngineCall c;
+    c.dtype = dt;
+    c.block = b;
+    c.nmat = 2;
+    c.epi = EPI_GATED_FWD;
+    c.m = m;
+    c.a_cols = e;
+    c.a0 = x;
+    c.w0 = gate->values;
+    c.nnzb0 = gate->nnzb;
+    c.w1 = up->values;
+    c.nnzb1 = up->nnzb;
+    c.n_lines = cdiv(h, b);
+    c.n_valid = h;
+    c.step_ptr = plan->gu_step_ptr;
+    c.steps = plan->gu_steps;
+    c.flags = plan->gu_flags;
+    c.out0 = gated;
+    c.out1 = gate_pre;
+    c.out2 = up_out;
+    c.ld_out = h;
+    r = run_engine(c, st);
+    if (r) return r;
+  } else {
+    Scratch sa, sb;
+    if (!gate_pre) {
+      if (!sa.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch a");
+      gate_pre = sa.ptr;
+    }
+    if (!up_out) {
+      if (!sb.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch b");
+      up_out = sb.ptr;
+    }
+    if ((r = blast_bspmm(x, m, gate, BLAST_ACT_NONE, gate_pre, stream))) return r;
+    if ((r = blast_bspmm(x, m, up, BLAST_ACT_NONE, up_out, stream))) return r;
+    const int64_t n = m * h;
+    const int grid = static_cast<int>(std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 16));
+    if (dt == BLAST_BF16)
+      gated_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(gate_pre), static_cast<const __nv_bfloat16*>(up_out),
+          static_cast<__nv_bfloat16*>(gated), n);
+    else
+      gated_fwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(gate_pre),
+                                                    static_cast<const float*>(up_out),
+                                                    static_cast<float*>(gated), n);
+    if ((r = check_launch("gated_fwd"))) return r;
+  }
+  return blast_bspmm(gated, m, down, BLAST_ACT_NONE, y, stream);
+}
+
+extern "C" int blast_mlp_backward_dgrad(const void* dy, int64_t m, const void* gate_pre,
+                                        const void* up_out, const blast_bcsc_t* gate,
+                                        const blast_bcsc_t* up, const blast_bcsc_t* down,
+                                        const blast_mlp_plan_t* plan, void* dx, void* da,
+                                        void* db, void* stream) {
+  if (!check_w(gate) || !check_w(up) || !check_w(down)) return BLAST_EINVAL;
+  const int64_t e = gate->rows, h = gate->cols;
+  const int b = gate->block;
+  if (up->rows != e || up->cols != h || down->rows != h || down->cols != e || up->block != b ||
+      down->block != b) {
+    set_error("gated MLP shape mismatch");
+    return BLAST_EMISMATCH;
+  }
+  if (m <= 0) return BLAST_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int dt = gate->dtype;
+  // dG = dY Wd^T with the gating backward fused into the epilogue -> dA, dB
+  EngineCall c;
+  c.dtype = dt;
+  c.block = b;
+  c.transposed = true;
+  c.epi = EPI_GATED_BWD;
+  c.m = m;
+  c.a_cols = e;
+  c.a0 = dy;
+  c.w0 = down->values;
+  c.w0_hi = down->tf32_rt_hi;
+  c.w0_lo = down->tf32_rt_lo;
+  c.nnzb0 = down->nnzb;
+  c.n_lines = cdiv(h, b);
+  c.n_valid = h;
+  c.step_ptr = down->rt_step_ptr;
+  c.steps = down->rt_steps;
+  c.flags = down->rt_flags;
+  c.out0 = da;
+  c.out1 = db;
+  c.in0 = gate_pre;
+  c.in1 = up_out;
+  c.ld_out = h;
+  int r = run_engine(c, st);
+  if (r) return r;
+  // dX = dA Wg^T + dB Wu^T
+  const bool fused = dt == BLAST_BF16 && b <= 64 && plan && plan->dx_step_ptr;
+  if (fused) {
+    EngineCall d;
+    d.dtype = dt;
+    d.block = b;
+    d.transposed = true;
+    d.nmat = 2;
+    d.sumacc = true;
+    d.m = m;
+    d.a_cols = h;
+    d.a0 = da;
+    d.a1 = db;
+    d.w0 = gate->values;
+    d.nnzb0 = gate->nnzb;
+    d.w1 = up->values;
+    d.nnzb1 = up->nnzb;
+    d.n_lines = cdiv(e, b);
+    d.n_valid = e;
+    d.step_ptr = plan->dx_step_ptr;
+    d.steps = plan->dx_steps;
+    d.flags = plan->dx_flags;
+    d.out0 = dx;
+    d.ld_out = e;
+    return run_engine(d, st);
+  }
+  if ((r = bspmm_rt_impl(da, m, gate, dx, 0, st))) return r;
+  return bspmm_rt_impl(db, m, up, dx, 1, st);
+}

@@ -1,0 +1,396 @@
+// Block-sparse tile engine on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// One engine serves every sparse product of the gated MLP:
+//   forward   Y = X * W           (reference bspmm,      blocksparse/kernels.py:86-124)
+//   fused     Y = f(X * W)        (bspmm_fused,           kernels.py:127-140)
+//   gated     G = silu(X Wg) * (X Wu)   (mlp_forward,     mlp.py:111-113)
+//   transpose Y = X * W^T         (bspmm_rt,              kernels.py:143-170)
+//   gated bwd dA, dB from dG = dY Wd^T  (mlp_backward,    mlp.py:133-139)
+//   dX        dX = dA Wg^T + dB Wu^T    (mlp_backward,    mlp.py:142)
+//
+// Work item = (token tile t of 128 rows, output block line j). The plan
+// (built on device from the block index maps, see plan.cu) lists the steps of
+// line j in ascending block order, which fixes the accumulation order and
+// makes every output bitwise reproducible run to run (kernels.py:117-121).
+// Each step names the A panel (a b-wide column panel of the activations) and
+// the stored block(s) it multiplies; absent blocks never reach the tensor core.
+//
+// Warp roles (256 threads, persistent over items, 1 CTA per SM):
+//   warp 0      TMA producer: A panel + W block(s) -> smem ring (mbarrier full/empty)
+//   warp 1      MMA issuer:   tcgen05.mma 128 x b x K into a double-buffered TMEM accumulator
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld -> activation / gating -> global stores
+#pragma once
+
+#include "activations.cuh"
+#include "ptx.cuh"
+
+namespace blast {
+
+enum Epi : int { EPI_STORE = 0, EPI_GATED_FWD = 1, EPI_GATED_BWD = 2 };
+
+struct SpmmParams {
+  int32_t m;            // activation rows (tokens)
+  int32_t n_lines;      // output block lines (block columns of Y)
+  int32_t n_valid;      // logical output width; columns >= n_valid are not stored
+  int32_t n_tok_tiles;  // ceil(m / 128)
+  const int32_t* step_ptr;  // [n_lines + 1]
+  const int4* steps;        // {a_blk, k0, k1, 0}
+  const int32_t* line_flags;  // bit i: accumulator i received at least one MMA
+  int32_t act;
+  int32_t accumulate;  // EPI_STORE: out0 += result (second half of a split dX sum)
+  void* out0;  // Y | G | dA
+  void* out1;  // saved gate_pre (fwd) | dB (bwd)
+  void* out2;  // saved up_out (fwd)
+  const void* in0;  // bwd: gate_pre
+  const void* in1;  // bwd: up_out
+  int64_t ld_out;   // row stride (elements) of every out*/in* array
+};
+
+template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR>
+struct TcCfg {
+  static constexpr int BM = 128;
+  static constexpr int ROWB = B * ELT;                    // bytes of one block row
+  static constexpr int SW = ROWB < 128 ? ROWB : 128;      // swizzle span
+  static constexpr int SWE = SW / ELT;                    // elements per swizzle row
+  static constexpr int NATOM = ROWB / SW;                 // swizzle atoms along a row
+  static constexpr int MMA_K = 32 / ELT;                  // 16 (bf16) / 8 (tf32)
+  static constexpr int KSL = B / MMA_K;                   // MMAs per block along K
+  static constexpr int NCOPY = NPASS == 3 ? 2 : 1;        // hi / lo operand copies
+  static constexpr int NA = SUMACC ? NMAT : 1;            // distinct A panels per step
+  static constexpr int round1k(int x) { return (x + 1023) / 1024 * 1024; }
+  static constexpr int A_TILE = round1k(BM * ROWB);
+  static constexpr int B_TILE = round1k(B * ROWB);
+  static constexpr int STAGE = NA * NCOPY * A_TILE + NMAT * NCOPY * B_TILE;
+  static constexpr int SMEM_BUDGET = 200 * 1024;
+  static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int NACC = SUMACC ? 1 : NMAT;
+  static constexpr int ACC_STRIDE = NACC * B;             // TMEM columns per accumulator stage
+  static constexpr int TMEM_COLS_RAW = 2 * ACC_STRIDE;
+  static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32    ? 32
+                                   : TMEM_COLS_RAW <= 64  ? 64
+                                   : TMEM_COLS_RAW <= 128 ? 128
+                                   : TMEM_COLS_RAW <= 256 ? 256
+                                                          : 512;
+  static constexpr uint32_t IDESC =
+      make_idesc(BM, B, ELT == 2 ? 1u : 2u, 0u, B_KMAJOR ? 0u : 1u);
+  // barriers + tmem slot live after the stages
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE + BAR_BYTES + 1024;  // +1024 alignment slack
+  static_assert(STAGES >= 2, "stage does not fit twice in shared memory");
+  static_assert(B % 16 == 0 && B >= 16 && B <= 256, "tensor-core block size");
+  static_assert(TMEM_COLS_RAW <= 512, "accumulators exceed TMEM");
+  static_assert(ROWB % SW == 0, "row must be whole swizzle atoms");
+};
+
+// K-major operand (rows x B elements, stored as NATOM swizzle atoms of `rows` x SW bytes):
+// descriptor for K slice `ks`.
+template <int SW, int MMA_K, int ELT>
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int rows, int ks) {
+  const uint32_t byte_k = static_cast<uint32_t>(ks) * MMA_K * ELT;  // 32 B per K slice
+  const uint32_t atom = byte_k / SW;
+  const uint32_t within = byte_k % SW;
+  return make_sdesc(base + atom * static_cast<uint32_t>(rows) * SW + within, 16u, 8u * SW,
+                    swizzle_layout_code(SW));
+}
+// MN-major B operand (B rows of K, each row B elements of N in NATOM atoms).
+template <int SW, int MMA_K, int B>
+__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int ks) {
+  return make_sdesc(base + static_cast<uint32_t>(ks) * MMA_K * SW, static_cast<uint32_t>(B) * SW,
+                    8u * SW, swizzle_layout_code(SW));
+}
+
+template <typename OutT>
+__device__ __forceinline__ void store_chunk16(OutT* dst, const float (&v)[16], int valid,
+                                              bool vec_ok) {
+  if (vec_ok && valid >= 16) {
+    if constexpr (sizeof(OutT) == 4) {
+      float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+      uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          __nv_bfloat162 pr = __floats2bfloat162_rn(v[8 * i + 2 * h], v[8 * i + 2 * h + 1]);
+          w[h] = *reinterpret_cast<uint32_t*>(&pr);
+        }
+        d[i] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  } else {
+    for (int i = 0; i < 16 && i < valid; ++i) dst[i] = from_f32<OutT>(v[i]);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void load_chunk16(const T* src, float (&v)[16], int valid, bool vec_ok) {
+  if (vec_ok && valid >= 16) {
+    if constexpr (sizeof(T) == 4) {
+      const float4* s = reinterpret_cast<const float4*>(src);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float4 q = s[i];
+        v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+      }
+    } else {
+      const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint4 q = s[i];
+        uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          __nv_bfloat162 pr = *reinterpret_cast<__nv_bfloat162*>(&w[h]);
+          float2 f = __bfloat1622float2(pr);
+          v[8 * i + 2 * h] = f.x; v[8 * i + 2 * h + 1] = f.y;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = (i < valid) ? to_f32<T>(src[i]) : 0.0f;
+  }
+}
+
+template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT>
+__global__ void __launch_bounds__(256, 1)
+spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
+               const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA1lo,
+               const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW0lo,
+               const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW1lo,
+               const SpmmParams p) {
+  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tmem_full = empty + C::STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int n_items = p.n_tok_tiles * p.n_lines;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA0);
+    tma_prefetch(&mapW0);
+    if (NMAT > 1) tma_prefetch(&mapW1);
+    if (SUMACC) tma_prefetch(&mapA1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int t = item / p.n_lines;
+        const int j = item - t * p.n_lines;
+        const int s0 = p.step_ptr[j], s1 = p.step_ptr[j + 1];
+        for (int s = s0; s < s1; ++s) {
+          const int4 st = __ldg(&p.steps[s]);
+          const int kb[2] = {st.y, st.z};
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint32_t bytes = 0;
+#pragma unroll
+          for (int a = 0; a < C::NA; ++a)
+            if (!SUMACC || kb[a] >= 0) bytes += C::NCOPY * (C::BM * C::ROWB);
+#pragma unroll
+          for (int mm = 0; mm < NMAT; ++mm)
+            if (kb[mm] >= 0) bytes += C::NCOPY * (B * C::ROWB);
+          mbar_expect_tx(&full[stage], bytes);
+          uint8_t* sbase = smem + stage * C::STAGE;
+#pragma unroll
+          for (int a = 0; a < C::NA; ++a) {
+            if (SUMACC && kb[a] < 0) continue;
+            const CUtensorMap* mh = (a == 0) ? &mapA0 : &mapA1;
+            const CUtensorMap* ml = (a == 0) ? &mapA0lo : &mapA1lo;
+#pragma unroll
+            for (int c = 0; c < C::NCOPY; ++c) {
+              uint8_t* dst = sbase + (a * C::NCOPY + c) * C::A_TILE;
+#pragma unroll
+              for (int at = 0; at < C::NATOM; ++at)
+                tma_load_2d(dst + at * C::BM * C::SW, c == 0 ? mh : ml, &full[stage],
+                            st.x * B + at * C::SWE, t * C::BM);
+            }
+          }
+#pragma unroll
+          for (int mm = 0; mm < NMAT; ++mm) {
+            if (kb[mm] < 0) continue;
+            const CUtensorMap* mh = (mm == 0) ? &mapW0 : &mapW1;
+            const CUtensorMap* ml = (mm == 0) ? &mapW0lo : &mapW1lo;
+#pragma unroll
+            for (int c = 0; c < C::NCOPY; ++c) {
+              uint8_t* dst = sbase + C::NA * C::NCOPY * C::A_TILE + (mm * C::NCOPY + c) * C::B_TILE;
+#pragma unroll
+              for (int at = 0; at < C::NATOM; ++at)
+                tma_load_2d_hint(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
+                                 at * C::SWE, kb[mm] * B, pol_w);
+            }
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int t = item / p.n_lines;
+        const int j = item - t * p.n_lines;
+        (void)t;
+        const uint32_t as = it & 1, use = it >> 1;
+        mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+        tc_fence_after();
+        bool init[2] = {false, false};
+        const int s0 = p.step_ptr[j], s1 = p.step_ptr[j + 1];
+        for (int s = s0; s < s1; ++s) {
+          const int4 st = __ldg(&p.steps[s]);
+          const int kb[2] = {st.y, st.z};
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sbase = smem_u32(smem + stage * C::STAGE);
+#pragma unroll
+          for (int mm = 0; mm < NMAT; ++mm) {
+            if (kb[mm] < 0) continue;
+            const int acc_i = SUMACC ? 0 : mm;
+            const int a_i = SUMACC ? mm : 0;
+            const uint32_t d = tmem_base + as * C::ACC_STRIDE + acc_i * B;
+            const uint32_t a_hi = sbase + (a_i * C::NCOPY) * C::A_TILE;
+            const uint32_t a_lo = a_hi + C::A_TILE;
+            const uint32_t b_hi = sbase + C::NA * C::NCOPY * C::A_TILE + (mm * C::NCOPY) * C::B_TILE;
+            const uint32_t b_lo = b_hi + C::B_TILE;
+#pragma unroll
+            for (int ks = 0; ks < C::KSL; ++ks) {
+              const uint64_t ad = kmajor_desc<C::SW, C::MMA_K, ELT>(a_hi, C::BM, ks);
+              const uint64_t bd = B_KMAJOR ? kmajor_desc<C::SW, C::MMA_K, ELT>(b_hi, B, ks)
+                                           : mnmajor_desc<C::SW, C::MMA_K, B>(b_hi, ks);
+              const uint32_t acc_flag = (init[acc_i] || ks > 0) ? 1u : 0u;
+              if constexpr (NPASS == 3) {
+                const uint64_t adl = kmajor_desc<C::SW, C::MMA_K, ELT>(a_lo, C::BM, ks);
+                const uint64_t bdl = B_KMAJOR ? kmajor_desc<C::SW, C::MMA_K, ELT>(b_lo, B, ks)
+                                              : mnmajor_desc<C::SW, C::MMA_K, B>(b_lo, ks);
+                // small cross terms first, then the hi*hi product
+                mma_tf32(d, adl, bd, C::IDESC, acc_flag);
+                mma_tf32(d, ad, bdl, C::IDESC, 1u);
+                mma_tf32(d, ad, bd, C::IDESC, 1u);
+              } else if constexpr (ELT == 4) {
+                mma_tf32(d, ad, bd, C::IDESC, acc_flag);
+              } else {
+                mma_f16(d, ad, bd, C::IDESC, acc_flag);
+              }
+            }
+            init[acc_i] = true;
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tmem_full[as]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp - 4;  // TMEM lane quarter
+    uint32_t it = 0;
+    const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      const int t = item / p.n_lines;
+      const int j = item - t * p.n_lines;
+      const uint32_t as = it & 1, use = it >> 1;
+      const int flags = __ldg(&p.line_flags[j]);
+      mbar_wait(&tmem_full[as], use & 1);
+      tc_fence_after();
+      const int row = t * C::BM + static_cast<int>(q * 32 + lane);
+      const bool row_ok = row < p.m;
+      const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
+#pragma unroll 1
+      for (int c = 0; c < B / 16; ++c) {
+        const int col = j * B + c * 16;
+        const int valid = p.n_valid - col;
+        const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
+        float v0[16];
+        tmem_ld16(tbase + c * 16, v0);
+        const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
+        if (!acc0_init) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
+        }
+        if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
+          if (row_ok && valid > 0) {
+            if (p.accumulate) {
+              float prev[16];
+              load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.out0) + off, prev, valid, vec_ok);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v0[i] = __fadd_rn(prev[i], v0[i]);
+            }
+            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
+          }
+        } else if constexpr (EPI == EPI_GATED_FWD) {
+          float v1[16];
+          tmem_ld16(tbase + B + c * 16, v1);
+          if (!(flags & 2)) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v1[i] = 0.0f;
+          }
+          if (row_ok && valid > 0) {
+            if (p.out1) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
+            if (p.out2) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out2) + off, v1, valid, vec_ok);
+            float g[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) g[i] = gated_fwd(v0[i], v1[i]);
+            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
+          }
+        } else {  // EPI_GATED_BWD: v0 = dG
+          if (row_ok && valid > 0) {
+            float a[16], b[16], da[16], db[16];
+            load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, a, valid, vec_ok);
+            load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in1) + off, b, valid, vec_ok);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
+            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, da, valid, vec_ok);
+            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, db, valid, vec_ok);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[as]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace blast

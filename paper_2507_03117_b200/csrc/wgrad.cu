@@ -1,0 +1,380 @@
+// Weight gradients of the block-sparse MLP (mlp.py:137-141):
+//     dW = A^T @ D      A: [m, rows] activations, D: [m, cols] upstream gradient
+// evaluated only on a set of b x b blocks (the active blocks of the BCSC
+// structure -> [nnzb, b, b] in BCSC order), or on the full grid (the
+// reference's dense gradient, needed at mask refresh for regrowth norms and by
+// the global-norm clip, trainer.py:365-384) -> dense [rows, cols].
+//
+// Tensor-core path (bf16, b in {64, 128}): one item = 128 output rows of one
+// block column c: two blocks of that column for b = 64 (they share the D
+// panel), one block for b = 128. Both operands are MN-major (A^T and D are read
+// straight from the row-major activations), K = tokens in 64-token stages.
+#include "host.hpp"
+#include "spmm_tc.cuh"
+
+namespace blast {
+
+struct WgradParams {
+  int32_t m;
+  int64_t rows, cols;
+  int32_t n_items;              // upper bound (grid sizing)
+  const int64_t* n_items_dev;   // exact count, on device
+  const int4* items;   // {c, s0, s1, 0}: block column, first/second block slot (-1 none)
+  const int32_t* row_of;  // slot -> block row (row_idx); nullptr in dense mode (slot = row)
+  float* out_blocks;   // [nnzb, b, b] (selected mode)
+  float* dense_out;    // [rows, cols]  (dense mode)
+};
+
+template <int B>
+struct WgCfg {
+  static constexpr int TK = 64;                 // tokens per stage
+  static constexpr int ATOM = TK * 128;         // one [TK x 64 bf16] swizzle-128 atom
+  static constexpr int A_TILE = 2 * ATOM;       // 128 output rows
+  static constexpr int NB_ATOM = B / 64;
+  static constexpr int B_TILE = NB_ATOM * ATOM;
+  static constexpr int STAGE = A_TILE + B_TILE;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr int TMEM_COLS = 2 * B <= 128 ? 128 : 256;
+  static constexpr uint32_t IDESC = make_idesc(128, B, 1u, 1u, 1u);
+  static constexpr int SMEM_BYTES = STAGES * STAGE + 256 + 1024;
+};
+
+template <int B>
+__global__ void __launch_bounds__(256, 1)
+wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapD,
+                const WgradParams p) {
+  using C = WgCfg<B>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tmem_full = empty + C::STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int ksteps = (p.m + C::TK - 1) / C::TK;
+  const int n_items = static_cast<int>(*p.n_items_dev);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapD);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto block_row = [&](int slot) -> int { return p.row_of ? p.row_of[slot] : slot; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int4 it = p.items[item];
+        const int c = it.x;
+        const int r0 = block_row(it.y);
+        const int r1 = it.z >= 0 ? block_row(it.z) : r0;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE);
+          uint8_t* sa = smem + stage * C::STAGE;
+          uint8_t* sb = sa + C::A_TILE;
+          const int tok = ks * C::TK;
+          if (B == 64) {
+            tma_load_2d(sa, &mapA, &full[stage], r0 * B, tok);
+            tma_load_2d(sa + C::ATOM, &mapA, &full[stage], r1 * B, tok);
+          } else {
+            tma_load_2d(sa, &mapA, &full[stage], r0 * B, tok);
+            tma_load_2d(sa + C::ATOM, &mapA, &full[stage], r0 * B + 64, tok);
+          }
+#pragma unroll
+          for (int a = 0; a < C::NB_ATOM; ++a)
+            tma_load_2d(sb + a * C::ATOM, &mapD, &full[stage], c * B + a * 64, tok);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const uint32_t as = it & 1, use = it >> 1;
+        mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * B;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE);
+          const uint32_t sb = sa + C::A_TILE;
+#pragma unroll
+          for (int kk = 0; kk < C::TK / 16; ++kk) {
+            // MN-major: K slice kk = 16 token rows (2048 B); LBO = stride between 64-wide atoms
+            const uint64_t ad = make_sdesc(sa + kk * 16 * 128, C::ATOM, 1024, 2);
+            const uint64_t bd = make_sdesc(sb + kk * 16 * 128, C::ATOM, 1024, 2);
+            mma_f16(d, ad, bd, C::IDESC, (ks > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tmem_full[as]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const uint32_t q = warp - 4;
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      const int4 itm = p.items[item];
+      const uint32_t as = it & 1, use = it >> 1;
+      mbar_wait(&tmem_full[as], use & 1);
+      tc_fence_after();
+      const int lrow = static_cast<int>(q * 32 + lane);  // 0..127
+      int slot, r, li;
+      if (B == 64) {
+        slot = lrow < 64 ? itm.y : itm.z;
+        li = lrow & 63;
+      } else {
+        slot = itm.y;
+        li = lrow;
+      }
+      r = slot >= 0 ? block_row(slot) : -1;
+      const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * B;
+#pragma unroll 1
+      for (int ch = 0; ch < B / 16; ++ch) {
+        float v[16];
+        tmem_ld16(tbase + ch * 16, v);
+        if (ksteps == 0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        }
+        if (slot < 0) continue;
+        if (p.dense_out) {
+          const int64_t row = static_cast<int64_t>(r) * B + li;
+          const int64_t col = static_cast<int64_t>(itm.x) * B + ch * 16;
+          if (row < p.rows) {
+            const int valid = static_cast<int>(p.cols - col);
+            store_chunk16<float>(p.dense_out + row * p.cols + col, v, valid, (p.cols % 4) == 0);
+          }
+        } else {
+          float* dst = p.out_blocks + (static_cast<int64_t>(slot) * B + li) * B + ch * 16;
+          store_chunk16<float>(dst, v, 16, true);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[as]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// CUDA-core fallback: 64x64 output tile per CTA, 16-token smem stages, 4x4 per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) wgrad_simt_kernel(const T* __restrict__ A,
+                                                         const T* __restrict__ D, int b,
+                                                         const int4* items, const WgradParams p) {
+  constexpr int TT = 16;
+  __shared__ float sa[TT][64];
+  __shared__ float sd[TT][64];
+  const int4 it = items[blockIdx.x];  // {c, slot, -, tile}: tile = (ti, tj) sub-tile of a block
+  const int c = it.x, slot = it.y;
+  const int r = p.row_of ? p.row_of[slot] : slot;
+  const int ti = it.w >> 16, tj = it.w & 0xFFFF;
+  const int i0 = ti * 64, j0 = tj * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int t0 = 0; t0 < p.m; t0 += TT) {
+    for (int e = threadIdx.x; e < TT * 64; e += 256) {
+      const int tt = e >> 6, cc = e & 63;
+      const int tok = t0 + tt;
+      const int64_t ar = static_cast<int64_t>(r) * b + i0 + cc;
+      const int64_t dc = static_cast<int64_t>(c) * b + j0 + cc;
+      sa[tt][cc] = (tok < p.m && i0 + cc < b && ar < p.rows) ? to_f32<T>(A[(int64_t)tok * p.rows + ar]) : 0.0f;
+      sd[tt][cc] = (tok < p.m && j0 + cc < b && dc < p.cols) ? to_f32<T>(D[(int64_t)tok * p.cols + dc]) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int tt = 0; tt < TT; ++tt) {
+      float av[4], dv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = sa[tt][ty * 4 + u];
+        dv[u] = sd[tt][tx * 4 + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(av[u], dv[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int li = i0 + ty * 4 + u, lj = j0 + tx * 4 + v;
+      if (li >= b || lj >= b) continue;
+      if (p.dense_out) {
+        const int64_t row = static_cast<int64_t>(r) * b + li, col = static_cast<int64_t>(c) * b + lj;
+        if (row < p.rows && col < p.cols) p.dense_out[row * p.cols + col] = acc[u][v];
+      } else {
+        p.out_blocks[(static_cast<int64_t>(slot) * b + li) * b + lj] = acc[u][v];
+      }
+    }
+}
+
+// items for the tensor-core kernel: per block column, consecutive stored blocks paired
+// (b = 64) or single (b = 128). Dense mode: every block of the grid.
+__global__ void wgrad_items_kernel(const int64_t* col_ptr, int64_t gr, int64_t gc, int per_item,
+                                   const int64_t* item_ptr, int4* items) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= gc) return;
+  const int64_t lo = col_ptr ? col_ptr[c] : c * gr;  // dense mode: slot = row, lo unused
+  const int64_t hi = col_ptr ? col_ptr[c + 1] : c * gr + gr;
+  int64_t out = item_ptr[c];
+  for (int64_t s = lo; s < hi; s += per_item) {
+    int s0 = static_cast<int>(col_ptr ? s : s - c * gr);
+    int s1 = -1;
+    if (per_item == 2 && s + 1 < hi) s1 = static_cast<int>(col_ptr ? s + 1 : s + 1 - c * gr);
+    items[out++] = make_int4(static_cast<int>(c), s0, s1, 0);
+  }
+}
+__global__ void wgrad_item_count_kernel(const int64_t* col_ptr, int64_t gr, int64_t gc,
+                                        int per_item, int64_t* item_ptr) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c == 0) item_ptr[0] = 0;
+  if (c >= gc) return;
+  const int64_t n = col_ptr ? col_ptr[c + 1] - col_ptr[c] : gr;
+  item_ptr[c + 1] = (n + per_item - 1) / per_item;
+}
+__global__ void scan_inplace_i64(int64_t* ptr, int64_t n) {  // tiny, single thread
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int64_t i = 1; i <= n; ++i) ptr[i] += ptr[i - 1];
+}
+// simt items: one per (slot, 64x64 sub-tile)
+__global__ void wgrad_simt_items_kernel(const int64_t* col_ptr, int64_t gr, int64_t gc, int tiles,
+                                        int4* items) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= gc) return;
+  const int64_t lo = col_ptr ? col_ptr[c] : 0, hi = col_ptr ? col_ptr[c + 1] : gr;
+  const int64_t base = col_ptr ? col_ptr[c] : c * gr;
+  for (int64_t s = lo; s < hi; ++s)
+    for (int t = 0; t < tiles * tiles; ++t) {
+      const int ti = t / tiles, tj = t % tiles;
+      items[(base + (s - lo)) * tiles * tiles + t] =
+          make_int4(static_cast<int>(c), static_cast<int>(col_ptr ? s : s - lo + 0), 0,
+                    (ti << 16) | tj);
+    }
+}
+
+template <int B>
+static int launch_wgrad_tc(const void* a, const void* d, const WgradParams& p, cudaStream_t st) {
+  using C = WgCfg<B>;
+  auto kern = wgrad_tc_kernel<B>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "wgrad smem attribute");
+    configured = true;
+  }
+  CUtensorMap ma, md;
+  if (!encode_map_2d(&ma, a, BLAST_BF16, p.rows, p.m, p.rows * 2, 64, C::TK, 128)) return BLAST_EINVAL;
+  if (!encode_map_2d(&md, d, BLAST_BF16, p.cols, p.m, p.cols * 2, 64, C::TK, 128)) return BLAST_EINVAL;
+  if (p.n_items <= 0) return BLAST_OK;
+  const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
+  kern<<<grid, 256, C::SMEM_BYTES, st>>>(ma, md, p);
+  return check_launch("wgrad_tc");
+}
+
+}  // namespace blast
+
+using namespace blast;
+
+extern "C" int blast_block_wgrad(const void* a, const void* d, int64_t m, int64_t rows,
+                                 int64_t cols, int32_t block, int dtype, const int64_t* col_ptr,
+                                 const int32_t* row_idx, int64_t nnzb, float* out_blocks,
+                                 float* dense_out, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rows < 1 || cols < 1 || block < 1 || m < 0) {
+    set_error("block_wgrad: invalid shape");
+    return BLAST_EINVAL;
+  }
+  const bool dense = dense_out != nullptr;
+  if (!dense && (!col_ptr || !row_idx || !out_blocks)) {
+    set_error("block_wgrad: selection (col_ptr,row_idx,out_blocks) or dense_out required");
+    return BLAST_EINVAL;
+  }
+  const int64_t gr = cdiv(rows, block), gc = cdiv(cols, block);
+  const int64_t nsel = dense ? gr * gc : nnzb;
+  if (m == 0) {
+    if (dense) cudaMemsetAsync(dense_out, 0, sizeof(float) * rows * cols, st);
+    else if (nnzb) cudaMemsetAsync(out_blocks, 0, sizeof(float) * nnzb * block * block, st);
+    return check_launch("wgrad zero");
+  }
+  if (nsel == 0) return BLAST_OK;
+  WgradParams p{};
+  p.m = static_cast<int32_t>(m);
+  p.rows = rows;
+  p.cols = cols;
+  p.row_of = dense ? nullptr : row_idx;
+  p.out_blocks = out_blocks;
+  p.dense_out = dense_out;
+  const int elt = bytes_of(dtype);
+  const bool tc = dtype == BLAST_BF16 && (block == 64 || block == 128) &&
+                  (rows * elt) % 16 == 0 && (cols * elt) % 16 == 0 && aligned16(a) &&
+                  aligned16(d) && m <= INT32_MAX;
+  const int64_t* cp = dense ? nullptr : col_ptr;
+  if (tc) {
+    const int per_item = block == 64 ? 2 : 1;
+    Scratch sp, si;
+    if (!sp.alloc(sizeof(int64_t) * (gc + 1), st)) return cuda_status(cudaGetLastError(), "wgrad");
+    if (!si.alloc(sizeof(int4) * nsel, st)) return cuda_status(cudaGetLastError(), "wgrad");
+    const int thr = 256, blk = static_cast<int>(cdiv(gc, thr));
+    wgrad_item_count_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>());
+    scan_inplace_i64<<<1, 32, 0, st>>>(sp.as<int64_t>(), gc);
+    wgrad_items_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>(), si.as<int4>());
+    p.n_items = static_cast<int32_t>((nsel + gc + per_item - 1) / per_item);
+    p.n_items_dev = sp.as<int64_t>() + gc;
+    p.items = si.as<int4>();
+    return block == 64 ? launch_wgrad_tc<64>(a, d, p, st) : launch_wgrad_tc<128>(a, d, p, st);
+  }
+  const int tiles = static_cast<int>(cdiv(block, 64));
+  const int64_t n_items = nsel * tiles * tiles;
+  Scratch si;
+  if (!si.alloc(sizeof(int4) * n_items, st)) return cuda_status(cudaGetLastError(), "wgrad");
+  wgrad_simt_items_kernel<<<static_cast<int>(cdiv(gc, 256)), 256, 0, st>>>(cp, gr, gc, tiles,
+                                                                          si.as<int4>());
+  if (n_items > INT32_MAX) {
+    set_error("block_wgrad: too many blocks");
+    return BLAST_EINVAL;
+  }
+  if (dtype == BLAST_BF16)
+    wgrad_simt_kernel<__nv_bfloat16><<<static_cast<unsigned>(n_items), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(d), block,
+        si.as<int4>(), p);
+  else
+    wgrad_simt_kernel<float><<<static_cast<unsigned>(n_items), 256, 0, st>>>(
+        static_cast<const float*>(a), static_cast<const float*>(d), block, si.as<int4>(), p);
+  return check_launch("wgrad_simt");
+}

@@ -1,0 +1,152 @@
+"""Block-sparse products and activations (mirrors blocksparse/kernels.py).
+
+``bspmm`` / ``bspmm_fused`` / ``bspmm_rt`` run the tcgen05 tile engine
+(csrc/spmm_tc.cuh) for b in {16, 32, 64, 128} and the CUDA-core engine
+(csrc/spmm_simt.cuh) for other block sizes. Accumulation order per output
+partition is fixed (ascending block index), so results are bitwise
+reproducible call to call (kernels.py:117-121 contract). float32 matrices
+compute in 3xTF32 (fp32-class accuracy), bfloat16 matrices in bf16 with fp32
+accumulation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _arrays as A
+from . import _lib as L
+from .bcsc import BlockSparseMatrix
+
+NONLINEARITIES = ("none", "relu", "gelu", "silu")
+_GELU_C = float(torch.tensor(math.sqrt(2.0 / math.pi), dtype=torch.float32))
+_GELU_A = float(torch.tensor(0.044715, dtype=torch.float32))
+
+
+# ------------------------------------------------------------------ activations
+# Scalar utilities (kernels.py:17-62). They evaluate on the GPU in the input's
+# precision (float64 allowed); the fused epilogues use csrc/activations.cuh.
+def _elementwise(fn):
+    def wrapper(x):
+        host = A.is_host(x)
+        t = A.to_device(x)
+        if not t.is_floating_point():
+            t = t.to(torch.float64)
+        return A.like_input(fn(t), host)
+    wrapper.__name__ = fn.__name__
+    wrapper.__doc__ = fn.__doc__
+    return wrapper
+
+
+@_elementwise
+def sigmoid(x):
+    """Split-form logistic: never evaluates exp on a large positive argument."""
+    pos = x >= 0
+    e = torch.exp(torch.where(pos, -x, x))
+    return torch.where(pos, 1.0 / (1.0 + e), e / (1.0 + e))
+
+
+def _sig(x):
+    pos = x >= 0
+    e = torch.exp(torch.where(pos, -x, x))
+    return torch.where(pos, 1.0 / (1.0 + e), e / (1.0 + e))
+
+
+@_elementwise
+def silu(x):
+    return x * _sig(x)
+
+
+@_elementwise
+def silu_grad(x):
+    s = _sig(x)
+    return s * (1.0 + x * (1.0 - s))
+
+
+@_elementwise
+def gelu(x):
+    return 0.5 * x * (1.0 + torch.tanh(_GELU_C * (x + _GELU_A * x * x * x)))
+
+
+@_elementwise
+def relu(x):
+    return torch.where((x > 0) | torch.isnan(x), x, torch.zeros_like(x))
+
+
+def _act_code(f: str) -> int:
+    if f not in L.ACT:
+        raise ValueError(f"unknown nonlinearity {f!r}, expected one of {NONLINEARITIES}")
+    return L.ACT[f]
+
+
+def apply_nonlinearity(x, f: str):
+    """Elementwise f on the GPU with the same device function the fused epilogue
+    uses, so bspmm_fused(x, w, f) == apply_nonlinearity(bspmm(x, w), f) bit for bit."""
+    code = _act_code(f)
+    host = A.is_host(x)
+    t = A.to_device(x, A.float_dtype(x))
+    if code == 0:
+        return A.like_input(t, host)
+    out = torch.empty_like(t)
+    L.check(L.load().blast_activation(t.data_ptr(), out.data_ptr(), t.numel(),
+                                      L.dtype_code(t.dtype), code, L.stream()), "activation")
+    return A.like_input(out, host)
+
+
+# ------------------------------------------------------------------ products
+def _check_lhs(x, w: BlockSparseMatrix, expected_cols: int) -> torch.Tensor:
+    if A.ndim(x) != 2:
+        raise ValueError(f"X must be 2-D, got ndim={A.ndim(x)}")
+    if A.shape(x)[1] != expected_cols:
+        raise ValueError(
+            f"dimension mismatch: X has {A.shape(x)[1]} columns, W expects {expected_cols}")
+    return A.to_device(x, w.values.dtype)
+
+
+def _product(x, w: BlockSparseMatrix, act: int, transposed: bool):
+    host = A.is_host(x) or (w.host_api and not isinstance(x, torch.Tensor))
+    xt = _check_lhs(x, w, w.cols if transposed else w.rows)
+    m = xt.shape[0]
+    out_cols = w.rows if transposed else w.cols
+    y = torch.empty(m, out_cols, dtype=w.values.dtype, device=A.DEVICE)
+    if m:
+        d = w.desc()
+        lib = L.load()
+        if transposed:
+            rc = lib.blast_bspmm_rt(xt.data_ptr(), m, C.byref(d), y.data_ptr(), L.stream())
+        else:
+            rc = lib.blast_bspmm(xt.data_ptr(), m, C.byref(d), act, y.data_ptr(), L.stream())
+        L.check(rc, "bspmm_rt" if transposed else "bspmm")
+    return A.like_input(y, host)
+
+
+def bspmm(x, w: BlockSparseMatrix, blk_m: int | None = None):
+    """Y = X @ W for dense X (M x K) and block-sparse W (K x N) (kernels.py:86-124).
+
+    ``blk_m`` is accepted for API compatibility; the device kernel always tiles
+    rows by 128 and its result does not depend on the host-side row tiling.
+    """
+    if blk_m is not None and blk_m < 1:
+        m = A.shape(x)[0] if A.ndim(x) >= 1 else 0
+        if blk_m < m:
+            raise ValueError(f"blk_m must be >= 1, got {blk_m}")
+    return _product(x, w, 0, False)
+
+
+def bspmm_fused(x, w: BlockSparseMatrix, f: str = "none", blk_m: int | None = None):
+    """f(X @ W) with f applied in the kernel epilogue (kernels.py:127-140)."""
+    code = _act_code(f)
+    if blk_m is not None and blk_m < 1:
+        raise ValueError(f"blk_m must be >= 1, got {blk_m}")
+    return _product(x, w, code, False)
+
+
+def bspmm_rt(x, w: BlockSparseMatrix):
+    """Y = X @ W.T for dense X (M x N) and block-sparse W (K x N) (kernels.py:143-170)."""
+    return _product(x, w, 0, True)
+
+
+def flops(m: int, n: int, k: int, nnzb: int, b: int) -> tuple[int, int]:
+    """(dense, sparse) FLOP counts of an M x K by K x N product (kernels.py:173-179)."""
+    return 2 * m * n * k, 2 * m * nnzb * b * b

@@ -1,0 +1,206 @@
+"""Gated block-sparse MLP: Y = (SiLU(X Wg) * (X Wu)) Wd (mirrors blocksparse/mlp.py).
+
+Forward (mlp.py:102-115): one fused kernel computes both gate and up products
+of a block column from a single load of each activation panel and applies
+SiLU*mul in the epilogue; a second launch of the same engine applies the down
+projection. Backward (mlp.py:118-143): dG = dY Wd^T with the gating derivative
+fused into its epilogue (-> dA, dB), dX = dA Wg^T + dB Wu^T in one pass, and
+weight gradients either on the full grid (the reference's dense gradients,
+``grad_mode="full"``) or only on the stored blocks (``grad_mode="active"``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _arrays as A
+from . import _lib as L
+from . import bcsc
+from .bcsc import BlockMask, BlockSparseMatrix
+
+
+@dataclass(eq=False)
+class MaskedMatrix:
+    """Dense float32 master + block mask + BCSC cache (mlp.py:21-46), all in HBM."""
+    dense: torch.Tensor
+    mask: BlockMask
+    cache: BlockSparseMatrix
+
+    @classmethod
+    def dense_init(cls, dense, b: int, dtype: torch.dtype = torch.float32) -> "MaskedMatrix":
+        d = A.to_device(dense, torch.float32)
+        gr, gc = -(-d.shape[0] // b), -(-d.shape[1] // b)
+        mask = BlockMask.all_active(gr, gc, device=True)
+        return cls(dense=d, mask=mask, cache=bcsc.from_dense(d, b, mask, dtype=dtype))
+
+    @property
+    def block(self) -> int:
+        return self.cache.block
+
+    def rebuild_cache(self) -> None:
+        self.cache = bcsc.from_dense(self.dense, self.block, self.mask, dtype=self.cache.dtype)
+
+    def achieved_sparsity(self) -> float:
+        return self.mask.block_sparsity()
+
+
+@dataclass(eq=False)
+class SparseMlp:
+    """gate: e x h, up: e x h, down: h x e, one block size (mlp.py:49-89)."""
+    gate: MaskedMatrix
+    up: MaskedMatrix
+    down: MaskedMatrix
+    _plan_cache: dict = field(default_factory=dict, repr=False)
+
+    @classmethod
+    def create(cls, e: int, h: int, b: int, rng: np.random.Generator,
+               dtype: torch.dtype = torch.float32) -> "SparseMlp":
+        """Same initialisation stream as mlp.py:61-68 (N(0, gain^2/rows), down at half gain),
+        so a given numpy seed yields the reference's weights bit for bit."""
+        def init(rows, cols, gain):
+            w = (rng.standard_normal((rows, cols)) * (gain * np.sqrt(1.0 / rows))).astype(np.float32)
+            return MaskedMatrix.dense_init(w, b, dtype)
+        return cls(gate=init(e, h, 1.0), up=init(e, h, 1.0), down=init(h, e, 0.5))
+
+    @property
+    def embed_dim(self) -> int:
+        return self.gate.dense.shape[0]
+
+    @property
+    def hidden_dim(self) -> int:
+        return self.gate.dense.shape[1]
+
+    @property
+    def block(self) -> int:
+        return self.gate.block
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.gate.cache.dtype
+
+    def matrices(self) -> tuple[MaskedMatrix, MaskedMatrix, MaskedMatrix]:
+        return self.gate, self.up, self.down
+
+    def achieved_sparsity(self) -> float:
+        active = sum(m.mask.n_active for m in self.matrices())
+        total = sum(m.mask.grid_rows * m.mask.grid_cols for m in self.matrices())
+        return 1.0 - active / total
+
+    def plan(self) -> L.MlpPlanDesc:
+        """Merged gate/up step lists (csrc/plan.cu), rebuilt when a cache is replaced."""
+        g, u = self.gate.cache, self.up.cache
+        key = (id(g), id(u))
+        if self._plan_cache.get("key") != key:
+            gr, gc = g.grid_rows, g.grid_cols
+            gu = bcsc.build_plan(g._kmap(), u._kmap(), gr, gc, 0)
+            dx = bcsc.build_plan(g._kmap(), u._kmap(), gr, gc, 1)
+            desc = L.MlpPlanDesc(*(t.data_ptr() for t in gu), *(t.data_ptr() for t in dx))
+            self._plan_cache = {"key": key, "tensors": (gu, dx, g, u), "desc": desc}
+        return self._plan_cache["desc"]
+
+
+@dataclass
+class MlpActivations:
+    """Saved by the forward pass for the backward (mlp.py:92-99)."""
+    x: object          # M x e
+    gate_pre: object   # X Wg
+    up_out: object     # X Wu
+    gated: object      # SiLU(gate_pre) * up_out
+
+
+def _to_host_acts(acts: MlpActivations) -> MlpActivations:
+    return MlpActivations(*(A.to_host(t) for t in (acts.x, acts.gate_pre, acts.up_out,
+                                                    acts.gated)))
+
+
+def mlp_forward(x, mlp: SparseMlp, save_activations: bool = True):
+    """Run the gated MLP; returns (y, MlpActivations) (mlp.py:102-115).
+
+    With ``save_activations=False`` (inference) the intermediate never leaves
+    the library and the second element is None.
+    """
+    if A.ndim(x) != 2:
+        raise ValueError(f"X must be 2-D (flatten batch/sequence first), got ndim={A.ndim(x)}")
+    if A.shape(x)[1] != mlp.embed_dim:
+        raise ValueError(f"X feature dim {A.shape(x)[1]} != embedding dim {mlp.embed_dim}")
+    host = A.is_host(x)
+    dt = mlp.dtype
+    xt = A.to_device(x, dt)
+    m, e, h = xt.shape[0], mlp.embed_dim, mlp.hidden_dim
+    y = torch.empty(m, e, dtype=dt, device=A.DEVICE)
+    a = b = g = None
+    if save_activations:
+        a, b, g = (torch.empty(m, h, dtype=dt, device=A.DEVICE) for _ in range(3))
+    if m:
+        dg, du, dd = (mat.cache.desc() for mat in mlp.matrices())
+        plan = mlp.plan()
+        L.check(L.load().blast_mlp_forward(xt.data_ptr(), m, C.byref(dg), C.byref(du), C.byref(dd),
+                                           C.byref(plan), y.data_ptr(), L.ptr(a), L.ptr(b),
+                                           L.ptr(g), L.stream()), "mlp_forward")
+    if not save_activations:
+        return A.like_input(y, host), None
+    acts = MlpActivations(x=xt, gate_pre=a, up_out=b, gated=g)
+    if host:
+        return A.to_host(y), _to_host_acts(acts)
+    return y, acts
+
+
+def _wgrad(a: torch.Tensor, d: torch.Tensor, rows: int, cols: int, w: BlockSparseMatrix,
+           full: bool) -> torch.Tensor:
+    m = a.shape[0]
+    lib = L.load()
+    b = w.block
+    if full:
+        out = torch.empty(rows, cols, dtype=torch.float32, device=A.DEVICE)
+        L.check(lib.blast_block_wgrad(a.data_ptr(), d.data_ptr(), m, rows, cols, b,
+                                      L.dtype_code(a.dtype), None, None, 0, None, out.data_ptr(),
+                                      L.stream()), "wgrad")
+        return out
+    out = torch.empty(w.nnzb, b, b, dtype=torch.float32, device=A.DEVICE)
+    if w.nnzb:
+        L.check(lib.blast_block_wgrad(a.data_ptr(), d.data_ptr(), m, rows, cols, b,
+                                      L.dtype_code(a.dtype), w.col_ptr.data_ptr(),
+                                      w.block_row_idx.data_ptr(), w.nnzb, out.data_ptr(), None,
+                                      L.stream()), "wgrad")
+    return out
+
+
+def mlp_backward(dy, acts: MlpActivations, mlp: SparseMlp, grad_mode: str = "full"):
+    """Exact gradients at the saved activations (mlp.py:118-143).
+
+    Returns (dX, dWgate, dWup, dWdown). ``grad_mode="full"`` gives the
+    reference's dense float32 weight gradients over the whole grid (needed for
+    regrowth and the global-norm clip); ``grad_mode="active"`` gives float32
+    [nnzb, b, b] gradients of the stored blocks only, in each cache's BCSC order.
+    """
+    if acts is None:
+        raise ValueError("missing saved activations: run mlp_forward first")
+    if grad_mode not in ("full", "active"):
+        raise ValueError(f"grad_mode must be 'full' or 'active', got {grad_mode!r}")
+    m = A.shape(acts.x)[0]
+    if A.shape(dy) != (m, mlp.embed_dim):
+        raise ValueError(f"dY shape {A.shape(dy)} does not match forward output")
+    host = A.is_host(dy)
+    dt = mlp.dtype
+    dyt = A.to_device(dy, dt)
+    x, a, b, g = (A.to_device(t, dt) for t in (acts.x, acts.gate_pre, acts.up_out, acts.gated))
+    e, h = mlp.embed_dim, mlp.hidden_dim
+    dx = torch.empty(m, e, dtype=dt, device=A.DEVICE)
+    da = torch.empty(m, h, dtype=dt, device=A.DEVICE)
+    db = torch.empty(m, h, dtype=dt, device=A.DEVICE)
+    if m:
+        dg, du, dd = (mat.cache.desc() for mat in mlp.matrices())
+        plan = mlp.plan()
+        L.check(L.load().blast_mlp_backward_dgrad(
+            dyt.data_ptr(), m, a.data_ptr(), b.data_ptr(), C.byref(dg), C.byref(du), C.byref(dd),
+            C.byref(plan), dx.data_ptr(), da.data_ptr(), db.data_ptr(), L.stream()), "mlp_backward")
+    full = grad_mode == "full"
+    d_gate = _wgrad(x, da, e, h, mlp.gate.cache, full)
+    d_up = _wgrad(x, db, e, h, mlp.up.cache, full)
+    d_down = _wgrad(g, dyt, h, e, mlp.down.cache, full)
+    if host:
+        return tuple(A.to_host(t) for t in (dx, d_gate, d_up, d_down))
+    return dx, d_gate, d_up, d_down

@@ -1,0 +1,179 @@
+"""GPU parity of bspmm / bspmm_fused / bspmm_rt against the oracle and the golden
+vectors of the real reference (ports of tests/test_kernels.py:27-151).
+
+Tolerances (north star): float32 (3xTF32 / CUDA-core FMA) <= 1e-5 under the
+reference's rel_err = |d| / (1 + |ref|) and <= 1e-4 max-norm-relative; bf16 <= 2e-2
+max-norm-relative against the oracle run on the same bf16-rounded inputs."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import golden, golden_bcsc
+
+pytestmark = pytest.mark.gpu
+
+bs = pytest.importorskip("paper_2507_03117_b200")
+
+
+def upload(w: oracle.Bcsc, dtype=torch.float32):
+    return bs.from_host(w, dtype)
+
+
+def round_bf16(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).bfloat16().float().numpy()
+
+
+def bf16_bcsc(w: oracle.Bcsc):
+    return w._replace(values=round_bf16(w.values))
+
+
+def check_f32(got, ref):
+    assert oracle.rel_err(got, ref) <= 1e-5
+    assert oracle.max_norm_rel(got, ref) <= 1e-4
+
+
+class TestGoldenProducts:
+    d = golden("products")
+
+    @pytest.mark.parametrize("i", range(15))
+    def test_fp32(self, i):
+        d = self.d
+        w = golden_bcsc(d, f"c{i}_w")
+        gw = upload(w)
+        check_f32(bs.bspmm(d[f"c{i}_x"], gw), d[f"c{i}_y"])
+        check_f32(bs.bspmm_rt(d[f"c{i}_xt"], gw), d[f"c{i}_yt"])
+        for f in ("relu", "gelu", "silu"):
+            check_f32(bs.bspmm_fused(d[f"c{i}_x"], gw, f), d[f"c{i}_y_{f}"])
+        np.testing.assert_array_equal(bs.to_dense(gw), d[f"c{i}_dense"])
+
+    @pytest.mark.parametrize("i", range(15))
+    def test_bf16(self, i):
+        d = self.d
+        w = bf16_bcsc(golden_bcsc(d, f"c{i}_w"))
+        x, xt = round_bf16(d[f"c{i}_x"]), round_bf16(d[f"c{i}_xt"])
+        gw = upload(w, torch.bfloat16)
+        y = bs.bspmm(torch.from_numpy(x).cuda().bfloat16(), gw).float().cpu().numpy()
+        assert oracle.max_norm_rel(y, oracle.bspmm(x, w)) <= 2e-2
+        yt = bs.bspmm_rt(torch.from_numpy(xt).cuda().bfloat16(), gw).float().cpu().numpy()
+        assert oracle.max_norm_rel(yt, oracle.bspmm_rt(xt, w)) <= 2e-2
+
+
+class TestBspmm:
+    def test_block_diagonal_identity(self):
+        rng = np.random.default_rng(0)
+        x = rng.standard_normal((6, 8)).astype(np.float32)
+        w = bs.from_dense(np.eye(8, dtype=np.float32), 4)
+        np.testing.assert_array_equal(bs.bspmm(x, w), x)
+
+    @pytest.mark.parametrize("b", [4, 16, 64])
+    def test_empty_matrix_gives_zero(self, b):
+        rng = np.random.default_rng(1)
+        x = rng.standard_normal((5, 2 * b)).astype(np.float32)
+        w = bs.from_dense(np.zeros((2 * b, 3 * b), dtype=np.float32), b)
+        assert w.nnzb == 0
+        np.testing.assert_array_equal(bs.bspmm(x, w), np.zeros((5, 3 * b), np.float32))
+        np.testing.assert_array_equal(bs.bspmm_rt(np.ones((5, 3 * b), np.float32), w),
+                                      np.zeros((5, 2 * b), np.float32))
+
+    @pytest.mark.parametrize("b", [1, 2, 4, 8, 16, 32, 64])
+    @pytest.mark.parametrize("sparsity", [0.0, 0.5, 0.9, 1.0])
+    def test_oracle_sweep(self, b, sparsity):
+        rng = np.random.default_rng(1000 * b + int(sparsity * 10))
+        for _ in range(6):
+            m = int(rng.integers(1, 140))
+            k = int(rng.integers(1, 4)) * b * 2 + int(rng.integers(0, 3)) * (b > 8)
+            n = int(rng.integers(1, 4)) * b + int(rng.integers(0, 5))
+            x = rng.standard_normal((m, k)).astype(np.float32)
+            w = oracle.random_bcsc(k, n, b, sparsity, rng)
+            w = w._replace(values=(w.values / np.sqrt(k)).astype(np.float32))
+            gw = upload(w)
+            check_f32(bs.bspmm(x, gw), oracle.bspmm(x, w))
+            xt = rng.standard_normal((m, n)).astype(np.float32)
+            check_f32(bs.bspmm_rt(xt, gw), oracle.bspmm_rt(xt, w))
+
+    def test_linearity(self):
+        rng = np.random.default_rng(3)
+        w = upload(oracle.random_bcsc(256, 128, 64, 0.5, rng))
+        x1 = rng.standard_normal((100, 256)).astype(np.float32)
+        x2 = rng.standard_normal((100, 256)).astype(np.float32)
+        a, b_ = np.float32(0.7), np.float32(-1.3)
+        lhs = bs.bspmm(a * x1 + b_ * x2, w)
+        rhs = a * bs.bspmm(x1, w) + b_ * bs.bspmm(x2, w)
+        assert oracle.rel_err(lhs, rhs) <= 1e-4
+
+    @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+    @pytest.mark.parametrize("b", [8, 64])
+    def test_deterministic_repeat_calls(self, dtype, b):
+        rng = np.random.default_rng(4)
+        w = upload(oracle.random_bcsc(512, 384, b, 0.4, rng), dtype)
+        x = torch.from_numpy(rng.standard_normal((300, 512)).astype(np.float32)).cuda().to(dtype)
+        y1, y2 = bs.bspmm(x, w), bs.bspmm(x, w)
+        assert torch.equal(y1.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
+                           y2.view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
+
+    def test_blk_m_does_not_change_result(self):
+        rng = np.random.default_rng(5)
+        x = rng.standard_normal((30, 16)).astype(np.float32)
+        w = upload(oracle.random_bcsc(16, 16, 4, 0.3, rng))
+        base = bs.bspmm(x, w)
+        for blk_m in (1, 7, 16, 64):
+            np.testing.assert_array_equal(bs.bspmm(x, w, blk_m=blk_m), base)
+
+    def test_dimension_mismatch(self):
+        w = bs.from_dense(np.eye(8, dtype=np.float32), 4)
+        with pytest.raises(ValueError, match="mismatch"):
+            bs.bspmm(np.ones((3, 9), dtype=np.float32), w)
+        with pytest.raises(ValueError, match="mismatch"):
+            bs.bspmm_rt(np.ones((3, 9), dtype=np.float32), w)
+
+    def test_unpadded_boundary_dims(self):
+        rng = np.random.default_rng(6)
+        for (m, k, n, b) in ((9, 13, 11, 4), (70, 100, 72, 16), (129, 200, 130, 64)):
+            x = rng.standard_normal((m, k)).astype(np.float32)
+            dense = rng.standard_normal((k, n)).astype(np.float32)
+            w = bs.from_dense(dense, b)
+            check_f32(bs.bspmm(x, w), x.astype(np.float64) @ dense.astype(np.float64))
+
+
+class TestFused:
+    @pytest.mark.parametrize("f", ["relu", "gelu", "silu"])
+    @pytest.mark.parametrize("b,dtype", [(4, torch.float32), (64, torch.float32),
+                                         (64, torch.bfloat16), (32, torch.bfloat16)])
+    def test_fusion_transparency_exact(self, f, b, dtype):
+        rng = np.random.default_rng(8)
+        w = upload(oracle.random_bcsc(4 * b, 3 * b, b, 0.5, rng), dtype)
+        x = torch.from_numpy(rng.standard_normal((150, 4 * b)).astype(np.float32)).cuda().to(dtype)
+        fused = bs.bspmm_fused(x, w, f)
+        mapped = bs.apply_nonlinearity(bs.bspmm(x, w), f)
+        assert torch.equal(fused, mapped)
+
+    def test_relu_clamps_negatives(self):
+        x = np.array([[1.0, -1.0]], dtype=np.float32)
+        w = bs.from_dense(np.diag([1.0, 1.0]).astype(np.float32), 1)
+        np.testing.assert_array_equal(bs.bspmm_fused(x, w, "relu"), [[1.0, 0.0]])
+
+    def test_unknown_nonlinearity(self):
+        w = bs.from_dense(np.eye(4, dtype=np.float32), 2)
+        with pytest.raises(ValueError, match="unknown nonlinearity"):
+            bs.bspmm_fused(np.ones((2, 4), dtype=np.float32), w, "tanh")
+
+
+class TestActivations:
+    def test_silu_at_one(self):
+        assert abs(bs.silu(np.array([1.0]))[0] - 0.7310585786300049) < 1e-12
+
+    def test_sigmoid_extremes_stable(self):
+        s = bs.sigmoid(np.array([-500.0, 0.0, 500.0]))
+        assert 0.0 <= s[0] < 1e-100 and s[1] == 0.5 and s[2] == 1.0
+
+    def test_gelu_reference_points(self):
+        assert bs.gelu(np.array([0.0]))[0] == 0.0
+        assert abs(bs.gelu(np.array([1.0]))[0] - 0.841192) < 1e-5
+
+    def test_device_activation_matches_oracle(self):
+        rng = np.random.default_rng(9)
+        x = (rng.standard_normal(10000) * 6).astype(np.float32)
+        for f in ("relu", "gelu", "silu"):
+            got = bs.apply_nonlinearity(x, f)
+            np.testing.assert_allclose(got, oracle.activation(x, f), rtol=2e-6, atol=1e-7)

@@ -1,0 +1,189 @@
+"""GPU prune-and-grow: masks, BSR/BCSC indices and values bit-exact vs the
+reference (golden vectors) and the oracle; ports of tests/test_pruner.py and
+tests/test_bcsc.py, plus full-size (Llama-3-8B / 70B MLP grid) properties."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import golden, golden_bcsc
+
+pytestmark = pytest.mark.gpu
+bs = pytest.importorskip("paper_2507_03117_b200")
+
+
+def assert_cache_equal(cache, ref: oracle.Bcsc):
+    h = cache.to_host()
+    assert (h.rows, h.cols, h.block) == (ref.rows, ref.cols, ref.block)
+    np.testing.assert_array_equal(h.col_ptr, ref.col_ptr)
+    np.testing.assert_array_equal(h.block_row_idx, ref.block_row_idx)
+    np.testing.assert_array_equal(h.values.view(np.uint32), ref.values.view(np.uint32))
+
+
+class TestGoldenPrune:
+    d = golden("prune")
+
+    def test_all_cases(self):
+        d = self.d
+        for i in range(int(d["n"])):
+            w, g = d[f"c{i}_w"], d[f"c{i}_g"]
+            b, s = int(d[f"c{i}_bs"][0]), float(d[f"c{i}_bs"][1])
+            nw = bs.block_norms(w, b)
+            np.testing.assert_allclose(nw, d[f"c{i}_nw"], rtol=1e-14, atol=0, equal_nan=True)
+            np.testing.assert_array_equal(bs.prune_s(d[f"c{i}_nw"], s), d[f"c{i}_keep"])
+            mask, rep = bs.generate_masks(w, g, b, s)
+            np.testing.assert_array_equal(mask.kept, d[f"c{i}_kept"])
+            np.testing.assert_array_equal(mask.regrown, d[f"c{i}_regrown"])
+            assert [rep.kept, rep.regrown, rep.regrown_ratio, rep.s_achieved] == \
+                list(d[f"c{i}_report"])
+            for zr, tag in ((True, "z"), (False, "nz")):
+                masked, cache = bs.apply_mask(w, mask, b, zero_regrown=zr)
+                np.testing.assert_array_equal(masked.view(np.uint32),
+                                              d[f"c{i}_{tag}_masked"].view(np.uint32))
+                assert_cache_equal(cache, golden_bcsc(d, f"c{i}_{tag}"))
+
+    def test_prune_s_ties_and_nan(self):
+        d = self.d
+        for j in range(int(d["n_prune_s"])):
+            np.testing.assert_array_equal(bs.prune_s(d[f"p{j}_norms"], float(d[f"p{j}_s"])),
+                                          d[f"p{j}_keep"])
+
+
+class TestGoldenFormat:
+    d = golden("format")
+
+    def test_from_dense_and_serialize(self):
+        d = self.d
+        for i in range(int(d["n"])):
+            dense, b = d[f"c{i}_dense"], int(d[f"c{i}_b"])
+            assert_cache_equal(bs.from_dense(dense, b), golden_bcsc(d, f"c{i}_auto"))
+            m = bs.BlockMask(kept=d[f"c{i}_kept"], regrown=d[f"c{i}_regrown"])
+            w = bs.from_dense(dense, b, m)
+            assert_cache_equal(w, golden_bcsc(d, f"c{i}_mask"))
+            assert bs.serialize(w) == d[f"c{i}_bytes"].tobytes()
+            w2 = bs.deserialize(d[f"c{i}_bytes"].tobytes())
+            assert_cache_equal(w2, golden_bcsc(d, f"c{i}_mask"))
+
+
+class TestPruneS:
+    def test_count_exactness(self):
+        rng = np.random.default_rng(1)
+        for _ in range(100):
+            gr, gc = int(rng.integers(1, 17)), int(rng.integers(1, 17))
+            s = float(rng.random())
+            keep = bs.prune_s(rng.random((gr, gc)), s)
+            assert keep.sum() == int(np.floor((1.0 - s) * gr * gc + 0.5))
+
+    def test_matches_sort_oracle_duplicates(self):
+        rng = np.random.default_rng(3)
+        for _ in range(100):
+            gr, gc = int(rng.integers(1, 13)), int(rng.integers(1, 13))
+            norms = rng.integers(0, 4, size=(gr, gc)).astype(np.float64)
+            s = float(rng.random())
+            np.testing.assert_array_equal(bs.prune_s(norms, s), oracle.prune_s(norms, s))
+
+    def test_scale_invariance(self):
+        rng = np.random.default_rng(2)
+        norms = rng.random((6, 6))
+        base = bs.prune_s(norms, 0.4)
+        for alpha in (1e-6, 0.5, 3.0, 1e6):
+            np.testing.assert_array_equal(bs.prune_s(alpha * norms, 0.4), base)
+
+    def test_special_values(self):
+        norms = np.array([[np.inf, 0.0, -0.0, np.nan], [1.0, np.nan, 2.0, 0.0]])
+        for s in np.linspace(0, 1, 9):
+            np.testing.assert_array_equal(bs.prune_s(norms, s), oracle.prune_s(norms, s))
+
+    def test_invalid_sparsity(self):
+        with pytest.raises(ValueError, match="sparsity"):
+            bs.prune_s(np.ones((2, 2)), 1.5)
+
+    @pytest.mark.parametrize("gr,gc", [(64, 224), (224, 64), (128, 448), (512, 1792)])
+    @pytest.mark.parametrize("s", [0.5, 0.9, 0.95])
+    def test_large_grids_match_oracle(self, gr, gc, s):
+        rng = np.random.default_rng(gr + gc)
+        norms = rng.random((gr, gc))
+        norms[rng.random((gr, gc)) < 0.05] = 0.5  # exact ties
+        np.testing.assert_array_equal(bs.prune_s(norms, s), oracle.prune_s(norms, s))
+
+
+class TestFullSizeMasks:
+    """Llama-3-8B and Llama-3-70B MLP gate grids at b = 64: masks bit-exact vs the
+    oracle run on the same inputs (and counts exact)."""
+
+    @pytest.mark.parametrize("rows,cols,s", [(4096, 14336, 0.9), (8192, 28672, 0.9),
+                                             (14336, 4096, 0.95)])
+    def test_generate_and_apply(self, rows, cols, s):
+        b = 64
+        gen = torch.Generator(device="cuda").manual_seed(rows)
+        w = torch.randn(rows, cols, device="cuda", generator=gen) * (rows ** -0.5)
+        g = torch.randn(rows, cols, device="cuda", generator=gen)
+        mask, rep = bs.generate_masks(w, g, b, s)
+        w_np, g_np = w.cpu().numpy(), g.cpu().numpy()
+        nw = bs.block_norms(w, b).cpu().numpy()
+        np.testing.assert_allclose(nw, oracle.block_norms(w_np, b), rtol=1e-13)
+        ref_mask, ref_rep = oracle.generate_masks(w_np, g_np, b, s)
+        np.testing.assert_array_equal(mask.kept.cpu().numpy(), ref_mask.kept)
+        np.testing.assert_array_equal(mask.regrown.cpu().numpy(), ref_mask.regrown)
+        assert (rep.kept, rep.regrown) == ref_rep[:2]
+        masked, cache = bs.apply_mask(w, mask, b)
+        ref_masked, ref_cache = oracle.apply_mask(w_np, ref_mask, b)
+        h = cache.to_host()
+        np.testing.assert_array_equal(h.col_ptr, ref_cache.col_ptr)
+        np.testing.assert_array_equal(h.block_row_idx, ref_cache.block_row_idx)
+        np.testing.assert_array_equal(h.values.view(np.uint32), ref_cache.values.view(np.uint32))
+        assert torch.equal(masked.cpu(), torch.from_numpy(ref_masked))
+
+
+class TestGenerateMasks:
+    def test_equal_inputs_no_regrowth(self):
+        w = np.random.default_rng(4).standard_normal((16, 16)).astype(np.float32)
+        mask, rep = bs.generate_masks(w, w.copy(), 4, 0.5)
+        assert rep.regrown == 0 and not mask.regrown.any() and mask.kept.sum() == rep.kept == 8
+
+    def test_shape_mismatch(self):
+        with pytest.raises(ValueError, match="shape"):
+            bs.generate_masks(np.ones((4, 4)), np.ones((4, 2)), 2, 0.5)
+
+    def test_regrow_disjoint_always(self):
+        rng = np.random.default_rng(7)
+        for _ in range(20):
+            w = rng.standard_normal((12, 12)).astype(np.float32)
+            g = rng.standard_normal((12, 12)).astype(np.float32)
+            mask, _ = bs.generate_masks(w, g, 3, float(rng.random()))
+            assert not (mask.kept & mask.regrown).any()
+
+    def test_bf16_device_inputs(self):
+        rng = np.random.default_rng(9)
+        w = rng.standard_normal((256, 512)).astype(np.float32)
+        g = rng.standard_normal((256, 512)).astype(np.float32)
+        wb = torch.from_numpy(w).cuda().bfloat16()
+        gb = torch.from_numpy(g).cuda().bfloat16()
+        mask, _ = bs.generate_masks(wb, gb, 32, 0.8)
+        ref, _ = oracle.generate_masks(wb.float().cpu().numpy(), gb.float().cpu().numpy(), 32, 0.8)
+        np.testing.assert_array_equal(mask.kept.cpu().numpy(), ref.kept)
+        np.testing.assert_array_equal(mask.regrown.cpu().numpy(), ref.regrown)
+
+
+class TestApplyMask:
+    def test_grid_mismatch(self):
+        with pytest.raises(ValueError, match="grid"):
+            bs.apply_mask(np.ones((8, 8), np.float32), bs.BlockMask.all_active(3, 3), 4)
+
+    def test_idempotent(self):
+        rng = np.random.default_rng(10)
+        w = rng.standard_normal((12, 12)).astype(np.float32)
+        g = rng.standard_normal((12, 12)).astype(np.float32)
+        mask, _ = bs.generate_masks(w, g, 3, 0.6)
+        once, c1 = bs.apply_mask(w, mask, 3)
+        twice, c2 = bs.apply_mask(once, mask, 3)
+        np.testing.assert_array_equal(once, twice)
+        assert torch.equal(c1.values, c2.values) and torch.equal(c1.block_row_idx, c2.block_row_idx)
+
+    def test_bf16_cache_values(self):
+        rng = np.random.default_rng(11)
+        w = rng.standard_normal((128, 192)).astype(np.float32)
+        mask, _ = bs.generate_masks(w, rng.standard_normal((128, 192)).astype(np.float32), 64, 0.5)
+        _, c32 = bs.apply_mask(w, mask, 64)
+        _, c16 = bs.apply_mask(w, mask, 64, dtype=torch.bfloat16)
+        assert torch.equal(c32.values.bfloat16(), c16.values)
