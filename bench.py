@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark: block-sparse gated MLP forward on B200 (BLaST hot path).
+
+Workload (BASELINE.json north star / configs[3]): Llama-3-8B MLP shape
+d=4096, h=14336, b=64 blocks, 90% block sparsity (exact-k uniform placement as
+the reference's bench.random_bcsc), bf16, 8192 tokens per GPU. One step = one
+sparse MLP forward y = (silu(x Wg) * (x Wu)) Wd over the step's tokens through
+the package API (2 kernel launches: fused gate/up + down).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 runs under torchrun: every rank processes its own 8192 tokens with the
+same weights (token-sharded data parallelism: the MLP has no cross-token
+dependency, so there is no data-path collective; scaling "weak"). Timing: CUDA
+events per step on the launching stream, L2 flushed (256 MiB write) between
+steps outside the events, barrier + synchronize around the K timed steps, max
+over ranks.
+
+``--impl reference`` times the reference algorithm on the host CPU (the numpy
+restatement in oracle/, the reference being pure numpy) on bounded token
+samples of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+D, H, BLOCK, SPARSITY, TOKENS = 4096, 14336, 64, 0.9, 8192
+METRIC = "sparse-MLP tokens/s (fused block-sparse gated MLP fwd, Llama-3-8B MLP shape, b=64, 90% block sparsity)"
+
+
+def synth_bcsc(rows: int, cols: int, b: int, s: float, rng: np.random.Generator, scale: float):
+    """Exact-k uniform block placement (reference bench.random_bcsc, bench.py:50-72) with
+    N(0, scale^2) values (SparseMlp.create scaling, mlp.py:61-68)."""
+    gr, gc = -(-rows // b), -(-cols // b)
+    total = gr * gc
+    nnzb = int(np.floor((1.0 - s) * total + 0.5))
+    flat = np.sort(rng.choice(total, size=nnzb, replace=False))
+    cols_of, rows_of = flat // gr, flat % gr
+    col_ptr = np.zeros(gc + 1, dtype=np.int64)
+    np.add.at(col_ptr, cols_of + 1, 1)
+    col_ptr = np.cumsum(col_ptr)
+    values = (rng.standard_normal((nnzb, b, b), dtype=np.float32) * np.float32(scale))
+    from types import SimpleNamespace
+    return SimpleNamespace(rows=rows, cols=cols, block=b, col_ptr=col_ptr,
+                           block_row_idx=rows_of.astype(np.uint32), values=values)
+
+
+def make_weights(d, h, b, s, seed):
+    rng = np.random.default_rng(seed)
+    return (synth_bcsc(d, h, b, s, rng, 1.0 / np.sqrt(d)),
+            synth_bcsc(d, h, b, s, rng, 1.0 / np.sqrt(d)),
+            synth_bcsc(h, d, b, s, rng, 0.5 / np.sqrt(h)))
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return j.get("hbm_gbs", 6553.0), j.get("bf16_tflops", 1636.8), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled in a background thread."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                if util > 0:
+                    self.samples.append(mhz)
+                    for bit, name in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_reference_time(weights, tokens: int, reps: int, warmup: int, seed: int):
+    """Time the reference algorithm (oracle port of mlp.py:102-115) on the host cores."""
+    import oracle
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    cores = len(os.sched_getaffinity(0))
+    mats = [oracle.Bcsc(w.rows, w.cols, w.block, w.col_ptr, w.block_row_idx, w.values)
+            for w in weights]
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((tokens, mats[0].rows)).astype(np.float32)
+    import contextlib
+    ctx = threadpool_limits(limits=cores) if threadpool_limits else contextlib.nullcontext()
+    times = []
+    with ctx:
+        for i in range(warmup + reps):
+            t0 = time.perf_counter()
+            oracle.mlp_forward(x, *mats)
+            if i >= warmup:
+                times.append(time.perf_counter() - t0)
+    return times, cores
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    weights = make_weights(D, H, BLOCK, SPARSITY, args.seed)
+    tokens = args.ref_tokens
+    times, cores = cpu_reference_time(weights, tokens, args.steps, args.warmup, args.seed)
+    step = float(np.mean(times))
+    value = tokens / step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg3 Llama-3-8B MLP fwd (d=4096 h=14336 b=64 s=0.9)",
+                   "tokens_per_step": tokens, "parallelism": "host cores"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{tokens} tokens per step of the cfg3 forward, numpy/OpenBLAS "
+                                   f"fp32 (reference algorithm restated in oracle/)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_blast(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2507_03117_b200 as bs
+    from paper_2507_03117_b200 import _lib as L
+    import ctypes as C
+
+    m = args.tokens
+    weights = make_weights(D, H, BLOCK, SPARSITY, args.seed)
+    mats = [bs.from_host(w, torch.bfloat16) for w in weights]
+    net = bs.SparseMlp.from_caches(*mats)
+    gen = torch.Generator(device="cuda").manual_seed(args.seed + 1000 * rank)
+    x = torch.randn(m, D, device="cuda", generator=gen).bfloat16()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    nnzb = [w.nnzb for w in mats]
+    flops_gu = 2 * m * (nnzb[0] + nnzb[1]) * BLOCK * BLOCK
+    flops_down = 2 * m * nnzb[2] * BLOCK * BLOCK
+    flops_total = flops_gu + flops_down
+    w_bytes = sum(n * BLOCK * BLOCK * 2 for n in nnzb)
+    idx_bytes = sum((w.grid_cols + 1) * 8 + w.nnzb * 4 for w in mats)
+    step_bytes = w_bytes + idx_bytes + m * D * 2 * 2  # weights + X read + Y write
+    hbm_peak, tf_peak, peak_kind = load_peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        y, _ = bs.mlp_forward(x, net, save_activations=False)
+        return y
+
+    # warm-up (also builds the execution plans)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t_total.item()) / args.steps
+    value = world * m / (ms_per_step * 1e-3)
+
+    # ---- per-kernel split of the same step (events on the launching stream)
+    lib = L.load()
+    g = torch.empty(m, H, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(m, D, dtype=torch.bfloat16, device="cuda")
+    dg, du, dd = (w.desc() for w in mats)
+    plan = net.plan()
+    s = L.stream()
+    k_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        k_ev[i][0].record()
+        L.check(lib.blast_mlp_gate_up(x.data_ptr(), m, C.byref(dg), C.byref(du), C.byref(plan),
+                                      g.data_ptr(), None, None, s))
+        k_ev[i][1].record()
+        L.check(lib.blast_bspmm(g.data_ptr(), m, C.byref(dd), 0, y.data_ptr(), s))
+        k_ev[i][2].record()
+    torch.cuda.synchronize()
+    t_gu = float(np.mean([a.elapsed_time(b) for a, b, _ in k_ev])) * 1e-3
+    t_dn = float(np.mean([b.elapsed_time(c) for _, b, c in k_ev])) * 1e-3
+
+    # ---- end to end through the public API with host buffers
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty(m, D, dtype=torch.bfloat16).pin_memory()
+    for _ in range(2):
+        xd = x_host.to("cuda", non_blocking=True)
+        y_host.copy_(bs.mlp_forward(xd, net, save_activations=False)[0], non_blocking=True)
+    torch.cuda.synchronize()
+    e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        e_ev[i][0].record()
+        xd = x_host.to("cuda", non_blocking=True)
+        yd, _ = bs.mlp_forward(xd, net, save_activations=False)
+        y_host.copy_(yd, non_blocking=True)
+        e_ev[i][1].record()
+    barrier()
+    e_total = torch.tensor([sum(a.elapsed_time(b) for a, b in e_ev)], dtype=torch.float64,
+                           device="cuda")
+    if world > 1:
+        dist.all_reduce(e_total, op=dist.ReduceOp.MAX)
+    e2e_value = world * m / (float(e_total.item()) / args.steps * 1e-3)
+
+    # ---- dense cuBLAS MLP of the same shape (HF LlamaMLP formulation), same protocol
+    dense_ms = None
+    if not args.no_dense:
+        wg = torch.randn(H, D, device="cuda", dtype=torch.bfloat16) * D ** -0.5
+        wu = torch.randn(H, D, device="cuda", dtype=torch.bfloat16) * D ** -0.5
+        wd = torch.randn(D, H, device="cuda", dtype=torch.bfloat16) * H ** -0.5
+        F = torch.nn.functional
+
+        def dense_step():
+            return F.linear(F.silu(F.linear(x, wg)) * F.linear(x, wu), wd)
+
+        for _ in range(3):
+            dense_step()
+        d_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(max(3, args.steps // 4))]
+        torch.cuda.synchronize()
+        for a, b in d_ev:
+            flush.zero_()
+            a.record()
+            dense_step()
+            b.record()
+        torch.cuda.synchronize()
+        dense_ms = float(np.mean([a.elapsed_time(b) for a, b in d_ev]))
+        del wg, wu, wd
+
+    # ---- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        times, cores = cpu_reference_time(weights, args.cpu_tokens, args.cpu_reps, 1, args.seed)
+        med = float(np.median(times))
+        cpu = {"value": args.cpu_tokens / med, "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_tokens} tokens of the cfg3 forward (same weights), median of "
+                         f"{args.cpu_reps} after 1 warm-up, numpy/OpenBLAS fp32, {cores} threads"}
+
+    traffic = None
+    tp = ROOT / "profiles" / "traffic_gate_up.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    ach_gu = flops_gu / t_gu / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1/d) weights, exact-k uniform block placement; N(0,1) tokens)",
+        "config": {"workload": "cfg3 Llama-3-8B MLP fwd", "d": D, "h": H, "block": BLOCK,
+                   "sparsity": SPARSITY, "nnzb_per_matrix": nnzb, "tokens_per_gpu": m,
+                   "global_tokens": world * m, "parallelism": f"dp{world} (token-sharded replicas)",
+                   "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+        "roofline": {"bound": "tensor", "achieved": ach_gu, "peak": tf_peak, "unit": "TFLOP/s",
+                     "frac": ach_gu / tf_peak, "traffic": traffic,
+                     "kernel": "spmm_tc gated gate+up (2 of 3 sparse products)",
+                     "flops_per_launch": flops_gu, "ms_per_launch": t_gu * 1e3,
+                     "peak_source": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)"},
+        "mlp_roofline": {
+            "flops_per_step": flops_total, "bytes_per_step": step_bytes,
+            "roofline_ms": max(flops_total / (tf_peak * 1e12), step_bytes / (hbm_peak * 1e9)) * 1e3,
+            "frac": max(flops_total / (tf_peak * 1e12), step_bytes / (hbm_peak * 1e9))
+            / (ms_per_step * 1e-3),
+            "achieved_tflops": flops_total / (ms_per_step * 1e-3) / 1e12,
+            "kernel_ms": {"gate_up": t_gu * 1e3, "down": t_dn * 1e3}},
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": m * D * 2,
+                "d2h_bytes_per_step": m * D * 2,
+                "path": "pinned host x -> mlp_forward (public API) -> pinned host y"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": sampler.summary(),
+        "cpu_baseline": cpu,
+    }
+    if dense_ms is not None:
+        line["dense_cublas"] = {"ms_per_step": dense_ms, "tokens_per_s": world * m / (dense_ms * 1e-3),
+                                "speedup_sparse_vs_dense": dense_ms / ms_per_step,
+                                "formulation": "torch bf16 F.linear x3 + silu*mul (HF LlamaMLP)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="blast", choices=["blast", "reference"])
+    ap.add_argument("--tokens", type=int, default=TOKENS)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=2048)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--ref-tokens", type=int, default=512)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_blast(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -112,6 +112,12 @@ int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
                       const blast_bcsc_t* up, const blast_bcsc_t* down,
                       const blast_mlp_plan_t* plan, void* y, void* gate_pre, void* up_out,
                       void* gated, void* stream);
+/* First half of blast_mlp_forward: gate and up products of every block column from one
+ * load of each activation panel, g = (a*sigmoid(a))*b in the epilogue (mlp.py:111-113).
+ * gated is required; gate_pre/up_out optional. */
+int blast_mlp_gate_up(const void* x, int64_t m, const blast_bcsc_t* gate, const blast_bcsc_t* up,
+                      const blast_mlp_plan_t* plan, void* gated, void* gate_pre, void* up_out,
+                      void* stream);
 /* Gated MLP backward, activation gradients (mlp.py:133-139, :142):
  *   dg = dY Wd^T; db = dg*s; da = (dg*b)*dsilu(a); dX = da Wg^T + db Wu^T.
  * da/db (M x h) are returned for the weight gradients. */

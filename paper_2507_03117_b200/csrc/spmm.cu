@@ -336,13 +336,35 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
   }
   if (m <= 0) return BLAST_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int dt = gate->dtype;
-  const size_t elt = bytes_of(dt);
+  const size_t elt = bytes_of(gate->dtype);
   Scratch sg;
   if (!gated) {
     if (!sg.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch G");
     gated = sg.ptr;
   }
+  int r = blast_mlp_gate_up(x, m, gate, up, plan, gated, gate_pre, up_out, stream);
+  if (r) return r;
+  return blast_bspmm(gated, m, down, BLAST_ACT_NONE, y, stream);
+}
+
+extern "C" int blast_mlp_gate_up(const void* x, int64_t m, const blast_bcsc_t* gate,
+                                 const blast_bcsc_t* up, const blast_mlp_plan_t* plan,
+                                 void* gated, void* gate_pre, void* up_out, void* stream) {
+  if (!check_w(gate) || !check_w(up)) return BLAST_EINVAL;
+  const int64_t e = gate->rows, h = gate->cols;
+  const int b = gate->block;
+  if (up->rows != e || up->cols != h || up->block != b || up->dtype != gate->dtype) {
+    set_error("gated MLP shape mismatch");
+    return BLAST_EMISMATCH;
+  }
+  if (m <= 0) return BLAST_OK;
+  if (!gated) {
+    set_error("gate_up: output buffer required");
+    return BLAST_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int dt = gate->dtype;
+  const size_t elt = bytes_of(dt);
   int r;
   const bool fused = dt == BLAST_BF16 && plan && plan->gu_step_ptr;
   if (fused) {
@@ -393,7 +415,7 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
                                                     static_cast<float*>(gated), n);
     if ((r = check_launch("gated_fwd"))) return r;
   }
-  return blast_bspmm(gated, m, down, BLAST_ACT_NONE, y, stream);
+  return BLAST_OK;
 }
 
 extern "C" int blast_mlp_backward_dgrad(const void* dy, int64_t m, const void* gate_pre,

@@ -67,11 +67,20 @@ class SparseMlp:
 
     @property
     def embed_dim(self) -> int:
-        return self.gate.dense.shape[0]
+        return self.gate.cache.rows
 
     @property
     def hidden_dim(self) -> int:
-        return self.gate.dense.shape[1]
+        return self.gate.cache.cols
+
+    @classmethod
+    def from_caches(cls, gate: BlockSparseMatrix, up: BlockSparseMatrix,
+                    down: BlockSparseMatrix) -> "SparseMlp":
+        """Inference-only network from BCSC matrices (no dense masters kept in HBM)."""
+        def mm(w):
+            km = w._kmap()
+            return MaskedMatrix(dense=None, mask=BlockMask(kept=km >= 0, regrown=torch.zeros_like(km, dtype=torch.bool)), cache=w)
+        return cls(mm(gate), mm(up), mm(down))
 
     @property
     def block(self) -> int:

@@ -12,12 +12,21 @@ pytestmark = pytest.mark.gpu
 bs = pytest.importorskip("paper_2507_03117_b200")
 
 
+def assert_bits_equal(got, ref):
+    """Bitwise float32 equality (so -0.0 != +0.0) with NaN == NaN: the NaN bit
+    pattern of w * 0 is platform-defined (x86 returns 0xffc00000, the GPU 0x7fffffff)."""
+    got, ref = np.asarray(got, np.float32), np.asarray(ref, np.float32)
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(ref))
+    ok = ~np.isnan(ref)
+    np.testing.assert_array_equal(got[ok].view(np.uint32), ref[ok].view(np.uint32))
+
+
 def assert_cache_equal(cache, ref: oracle.Bcsc):
     h = cache.to_host()
     assert (h.rows, h.cols, h.block) == (ref.rows, ref.cols, ref.block)
     np.testing.assert_array_equal(h.col_ptr, ref.col_ptr)
     np.testing.assert_array_equal(h.block_row_idx, ref.block_row_idx)
-    np.testing.assert_array_equal(h.values.view(np.uint32), ref.values.view(np.uint32))
+    assert_bits_equal(h.values, ref.values)
 
 
 class TestGoldenPrune:
@@ -38,8 +47,7 @@ class TestGoldenPrune:
                 list(d[f"c{i}_report"])
             for zr, tag in ((True, "z"), (False, "nz")):
                 masked, cache = bs.apply_mask(w, mask, b, zero_regrown=zr)
-                np.testing.assert_array_equal(masked.view(np.uint32),
-                                              d[f"c{i}_{tag}_masked"].view(np.uint32))
+                assert_bits_equal(masked, d[f"c{i}_{tag}_masked"])
                 assert_cache_equal(cache, golden_bcsc(d, f"c{i}_{tag}"))
 
     def test_prune_s_ties_and_nan(self):
@@ -131,7 +139,7 @@ class TestFullSizeMasks:
         h = cache.to_host()
         np.testing.assert_array_equal(h.col_ptr, ref_cache.col_ptr)
         np.testing.assert_array_equal(h.block_row_idx, ref_cache.block_row_idx)
-        np.testing.assert_array_equal(h.values.view(np.uint32), ref_cache.values.view(np.uint32))
+        assert_bits_equal(h.values, ref_cache.values)
         assert torch.equal(masked.cpu(), torch.from_numpy(ref_masked))
 
 
