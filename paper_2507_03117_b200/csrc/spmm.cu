@@ -110,7 +110,8 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
-  kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
+  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo,
+                                                  p);
   return check_launch("spmm_tc");
 }
 

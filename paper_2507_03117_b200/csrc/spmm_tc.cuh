@@ -155,9 +155,13 @@ __device__ __forceinline__ void load_chunk16(const T* src, float (&v)[16], int v
     for (int i = 0; i < 16; ++i) v[i] = (i < valid) ? to_f32<T>(src[i]) : 0.0f;
   }
 }
+// 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
+// (two warps per TMEM lane quarter, splitting the 16-column chunks).
+constexpr int kTcThreads = 384;
+constexpr int kEpiWarps = 8;
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kTcThreads, 1)
 spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
                const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA1lo,
                const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW0lo,
@@ -172,7 +176,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
-  const uint32_t warp = warp_id();
+  const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
   const int n_items = p.n_tok_tiles * p.n_lines;
 
@@ -187,7 +191,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
-      mbar_init(&tmem_empty[s], 4);
+      mbar_init(&tmem_empty[s], kEpiWarps);
     }
     fence_mbar_init();
   }
@@ -202,17 +206,19 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_last();
-      uint32_t stage = 0, phase = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int t = item / p.n_lines;
-        const int j = item - t * p.n_lines;
-        const int s0 = p.step_ptr[j], s1 = p.step_ptr[j + 1];
-        for (int s = s0; s < s1; ++s) {
-          const int4 st = __ldg(&p.steps[s]);
-          const int kb[2] = {st.y, st.z};
-          mbar_wait(&empty[stage], phase ^ 1);
+    // The whole warp walks the schedule (warp-uniform control flow keeps the loop
+    // state in uniform registers); one elected lane issues the copies.
+    const uint64_t pol_w = policy_evict_last();
+    uint32_t stage = 0, phase = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int t = item / p.n_lines;
+      const int j = item - t * p.n_lines;
+      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      for (int s = s0; s < s1; ++s) {
+        const int4 st = __ldg(&p.steps[s]);
+        const int kb[2] = {st.y, st.z};
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
           uint32_t bytes = 0;
 #pragma unroll
           for (int a = 0; a < C::NA; ++a)
@@ -250,72 +256,111 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
                                  at * C::SWE, kb[mm] * B, pol_w);
             }
           }
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0, it = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int t = item / p.n_lines;
-        const int j = item - t * p.n_lines;
-        (void)t;
-        const uint32_t as = it & 1, use = it >> 1;
-        mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+    // Descriptors are built once for stage 0 and advanced by adding byte offsets
+    // >> 4 to the start-address field (no carry: shared addresses < 2^18).
+    const uint32_t smem0 = smem_u32(smem);
+    const uint64_t a_desc0 = kmajor_desc<C::SW, C::MMA_K, ELT>(smem0, C::BM, 0);
+    const uint32_t b_off = C::NA * C::NCOPY * C::A_TILE;
+    const uint64_t b_desc0 = B_KMAJOR ? kmajor_desc<C::SW, C::MMA_K, ELT>(smem0 + b_off, B, 0)
+                                      : mnmajor_desc<C::SW, C::MMA_K, B>(smem0 + b_off, 0);
+    // merged gate+up: one N = 2B MMA over [W_gate | W_up] (adjacent MN-major atoms)
+    constexpr bool kMerge = (NMAT == 2) && !SUMACC && !B_KMAJOR && (2 * B <= 256) &&
+                            (C::NATOM == 1 || C::B_TILE == C::NATOM * B * C::SW);
+    constexpr uint32_t kMergeLbo = C::NATOM == 1 ? C::B_TILE : B * C::SW;
+    const uint64_t b_desc0_merged =
+        make_sdesc(smem0 + b_off, kMergeLbo, 8u * C::SW, swizzle_layout_code(C::SW));
+    constexpr uint32_t kIdescMerged = make_idesc(C::BM, kMerge ? 2 * B : B, ELT == 2 ? 1u : 2u, 0u,
+                                                 B_KMAJOR ? 0u : 1u);
+    // per-K-slice descriptor increments (in 16-byte units)
+    auto a_koff = [](int ks) -> uint32_t {
+      const uint32_t byte_k = static_cast<uint32_t>(ks) * C::MMA_K * ELT;
+      return ((byte_k / C::SW) * C::BM * C::SW + (byte_k % C::SW)) >> 4;
+    };
+    auto b_koff = [](int ks) -> uint32_t {
+      if (B_KMAJOR) {
+        const uint32_t byte_k = static_cast<uint32_t>(ks) * C::MMA_K * ELT;
+        return ((byte_k / C::SW) * B * C::SW + (byte_k % C::SW)) >> 4;
+      }
+      return (static_cast<uint32_t>(ks) * C::MMA_K * C::SW) >> 4;
+    };
+    uint32_t stage = 0, phase = 0, it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      const int t = item / p.n_lines;
+      const int j = item - t * p.n_lines;
+      (void)t;
+      const uint32_t as = it & 1, use = it >> 1;
+      mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+      tc_fence_after();
+      uint32_t init0 = 0, init1 = 0;
+      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
+      for (int s = s0; s < s1; ++s) {
+        const int4 st = __ldg(&p.steps[s]);
+        const bool has0 = st.y >= 0, has1 = NMAT > 1 && st.z >= 0;
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        bool init[2] = {false, false};
-        const int s0 = p.step_ptr[j], s1 = p.step_ptr[j + 1];
-        for (int s = s0; s < s1; ++s) {
-          const int4 st = __ldg(&p.steps[s]);
-          const int kb[2] = {st.y, st.z};
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sbase = smem_u32(smem + stage * C::STAGE);
+        if (elect_one()) {
+          const uint32_t soff = (stage * C::STAGE) >> 4;
+          const uint64_t ad = a_desc0 + soff;
+          const uint64_t bd = b_desc0 + soff;
+          if (kMerge && has0 && has1 && init0 == init1) {
 #pragma unroll
-          for (int mm = 0; mm < NMAT; ++mm) {
-            if (kb[mm] < 0) continue;
-            const int acc_i = SUMACC ? 0 : mm;
-            const int a_i = SUMACC ? mm : 0;
-            const uint32_t d = tmem_base + as * C::ACC_STRIDE + acc_i * B;
-            const uint32_t a_hi = sbase + (a_i * C::NCOPY) * C::A_TILE;
-            const uint32_t a_lo = a_hi + C::A_TILE;
-            const uint32_t b_hi = sbase + C::NA * C::NCOPY * C::A_TILE + (mm * C::NCOPY) * C::B_TILE;
-            const uint32_t b_lo = b_hi + C::B_TILE;
+            for (int ks = 0; ks < C::KSL; ++ks)
+              mma_f16(d_base, ad + a_koff(ks), b_desc0_merged + soff + b_koff(ks), kIdescMerged,
+                      (init0 | ks) ? 1u : 0u);
+          } else {
 #pragma unroll
-            for (int ks = 0; ks < C::KSL; ++ks) {
-              const uint64_t ad = kmajor_desc<C::SW, C::MMA_K, ELT>(a_hi, C::BM, ks);
-              const uint64_t bd = B_KMAJOR ? kmajor_desc<C::SW, C::MMA_K, ELT>(b_hi, B, ks)
-                                           : mnmajor_desc<C::SW, C::MMA_K, B>(b_hi, ks);
-              const uint32_t acc_flag = (init[acc_i] || ks > 0) ? 1u : 0u;
-              if constexpr (NPASS == 3) {
-                const uint64_t adl = kmajor_desc<C::SW, C::MMA_K, ELT>(a_lo, C::BM, ks);
-                const uint64_t bdl = B_KMAJOR ? kmajor_desc<C::SW, C::MMA_K, ELT>(b_lo, B, ks)
-                                              : mnmajor_desc<C::SW, C::MMA_K, B>(b_lo, ks);
-                // small cross terms first, then the hi*hi product
-                mma_tf32(d, adl, bd, C::IDESC, acc_flag);
-                mma_tf32(d, ad, bdl, C::IDESC, 1u);
-                mma_tf32(d, ad, bd, C::IDESC, 1u);
-              } else if constexpr (ELT == 4) {
-                mma_tf32(d, ad, bd, C::IDESC, acc_flag);
-              } else {
-                mma_f16(d, ad, bd, C::IDESC, acc_flag);
+            for (int mm = 0; mm < NMAT; ++mm) {
+              if (!(mm == 0 ? has0 : has1)) continue;
+              const int acc_i = SUMACC ? 0 : mm;
+              const int a_i = SUMACC ? mm : 0;
+              const uint32_t d = d_base + acc_i * B;
+              const uint64_t a_hi = ad + ((a_i * C::NCOPY * C::A_TILE) >> 4);
+              const uint64_t a_lo = a_hi + (C::A_TILE >> 4);
+              const uint64_t b_hi = bd + ((mm * C::NCOPY * C::B_TILE) >> 4);
+              const uint64_t b_lo = b_hi + (C::B_TILE >> 4);
+              const uint32_t init = acc_i == 0 ? init0 : init1;
+#pragma unroll
+              for (int ks = 0; ks < C::KSL; ++ks) {
+                const uint32_t acc_flag = (init | ks) ? 1u : 0u;
+                if constexpr (NPASS == 3) {
+                  // small cross terms first, then the hi*hi product
+                  mma_tf32(d, a_lo + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
+                  mma_tf32(d, a_hi + a_koff(ks), b_lo + b_koff(ks), C::IDESC, 1u);
+                  mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, 1u);
+                } else if constexpr (ELT == 4) {
+                  mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
+                } else {
+                  mma_f16(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
+                }
               }
+              if (acc_i == 0) init0 = 1; else init1 = 1;
             }
-            init[acc_i] = true;
           }
           mma_commit(&empty[stage]);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tmem_full[as]);
+        __syncwarp();
+        if (kMerge && has0 && has1) { init0 = 1; init1 = 1; }
+        else {
+          if (has0) init0 = 1;
+          if (has1) { if (SUMACC) init0 = 1; else init1 = 1; }
+        }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) mma_commit(&tmem_full[as]);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const uint32_t q = warp - 4;  // TMEM lane quarter
+    const uint32_t q = warp & 3;                 // TMEM lane quarter
+    const int half = static_cast<int>(warp - 4) >> 2;  // which 16-column chunks
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
@@ -329,7 +374,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
       const bool row_ok = row < p.m;
       const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
 #pragma unroll 1
-      for (int c = 0; c < B / 16; ++c) {
+      for (int c = half; c < B / 16; c += 2) {
         const int col = j * B + c * 16;
         const int valid = p.n_valid - col;
         const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
