@@ -76,6 +76,10 @@ typedef struct blast_mlp_plan {
 const char* blast_last_error(void);
 int blast_version(void);
 int blast_num_sms(void);
+/* Engine selection for bf16 products with >= 256 rows and b in {32, 64}: 1 = CTA-pair
+ * engine with resident weights (default), 0 = single-CTA engine. Returns the previous
+ * setting. Both give the same accumulation order; used for ablations and tests. */
+int blast_set_pair_engine(int enabled);
 
 /* ---------------------------------------------------------------- format / plans */
 /* kmap from col_ptr/row_idx (inverse index of bcsc.py:205-210). */

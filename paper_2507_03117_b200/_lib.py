@@ -47,6 +47,7 @@ _PROTOS = {
     "blast_last_error": (C.c_char_p, []),
     "blast_version": (C.c_int, []),
     "blast_num_sms": (C.c_int, []),
+    "blast_set_pair_engine": (C.c_int, [C.c_int]),
     "blast_kmap_from_bcsc": (C.c_int, [vp, vp, i64, i64, vp, vp]),
     "blast_build_plan": (C.c_int, [vp, vp, i64, i64, C.c_int, vp, vp, vp, vp]),
     "blast_split_tf32": (C.c_int, [vp, vp, vp, i64, vp]),

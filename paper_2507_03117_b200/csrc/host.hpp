@@ -9,6 +9,8 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <string>
 
 #include "../../include/blast.h"

@@ -3,6 +3,7 @@
 // blast_mlp_forward (mlp.py:102), blast_mlp_backward_dgrad (mlp.py:118-142).
 #include "host.hpp"
 #include "spmm_simt.cuh"
+#include "spmm_pair.cuh"
 #include "spmm_tc.cuh"
 
 namespace blast {
@@ -153,6 +154,83 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
   return -1;  // not available on the tensor-core path
 }
 
+// ---------------------------------------------------------------- CTA-pair engine
+template <int B, int NMAT, bool SUM, bool BK, int EPI>
+static int launch_pair(const EngineCall& c, cudaStream_t st) {
+  using Cfg = PairCfg<B, NMAT, SUM, BK>;
+  auto kern = spmm_pair_kernel<B, NMAT, SUM, BK, EPI, __nv_bfloat16>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "spmm_pair smem attribute");
+    configured = true;
+  }
+  CUtensorMap mA0, mA1, mW0, mW1;
+  auto mkA = [&](CUtensorMap* mp, const void* ptr) {
+    return encode_map_2d(mp, ptr, BLAST_BF16, c.a_cols, c.m, c.a_cols * 2, Cfg::SWE, Cfg::BM,
+                         Cfg::SW);
+  };
+  auto mkW = [&](CUtensorMap* mp, const void* ptr, int64_t nnzb) {
+    if (ptr == nullptr || nnzb <= 0) {
+      ptr = c.a0;
+      nnzb = 1;
+    }
+    if (BK)  // [B/2 rows x B cols] halves, rows r*B + rank*B/2
+      return encode_map_2d(mp, ptr, BLAST_BF16, B, nnzb * B, B * 2, Cfg::WH_SW / 2, B / 2,
+                           Cfg::WH_SW);
+    return encode_map_2d(mp, ptr, BLAST_BF16, B, nnzb * B, B * 2, B / 2, B, Cfg::WH_SW);
+  };
+  bool ok = mkA(&mA0, c.a0);
+  mA1 = mA0;
+  if (ok && SUM) ok = mkA(&mA1, c.a1);
+  if (ok) ok = mkW(&mW0, c.w0, c.nnzb0);
+  mW1 = mW0;
+  if (ok && NMAT > 1) ok = mkW(&mW1, c.w1, c.nnzb1);
+  if (!ok) return BLAST_EINVAL;
+  PairParams pp{};
+  pp.p = make_params(c);
+  pp.n_pair_tiles = static_cast<int32_t>(cdiv(c.m, 256));
+  const int64_t n_pairs = num_sms() / 2;
+  int64_t r = (c.n_lines * pp.n_pair_tiles) / (12 * n_pairs);
+  r = std::max<int64_t>(1, std::min<int64_t>(r, pp.n_pair_tiles));
+  pp.tiles_per_item = static_cast<int32_t>(r);
+  pp.n_chunks = static_cast<int32_t>(cdiv(pp.n_pair_tiles, r));
+  const int64_t items = static_cast<int64_t>(pp.n_chunks) * c.n_lines;
+  if (items <= 0) return BLAST_OK;
+  const int grid = static_cast<int>(2 * std::min<int64_t>(items, n_pairs));
+  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mA0, mA1, mW0, mW1, pp);
+  return check_launch("spmm_pair");
+}
+
+template <int B>
+static int dispatch_pair_b(const EngineCall& c, cudaStream_t st) {
+  if (!c.transposed) {
+    if (c.nmat == 1 && c.epi == EPI_STORE && c.act == ACT_NONE && !c.accumulate)
+      return launch_pair<B, 1, false, false, EPI_STORE>(c, st);
+    if (c.nmat == 2 && c.epi == EPI_GATED_FWD)
+      return launch_pair<B, 2, false, false, EPI_GATED_FWD>(c, st);
+  } else {
+    if (c.nmat == 1 && c.epi == EPI_STORE)
+      return launch_pair<B, 1, false, true, EPI_STORE>(c, st);
+    if (c.nmat == 1 && c.epi == EPI_GATED_BWD)
+      return launch_pair<B, 1, false, true, EPI_GATED_BWD>(c, st);
+    if (c.nmat == 2 && c.sumacc && c.epi == EPI_STORE)
+      return launch_pair<B, 2, true, true, EPI_STORE>(c, st);
+  }
+  return -1;
+}
+
+static int g_pair_engine = -1;  // -1: from BLAST_DISABLE_PAIR, else 0/1
+
+static bool pair_disabled() {
+  if (g_pair_engine < 0) {
+    const char* e = getenv("BLAST_DISABLE_PAIR");
+    g_pair_engine = (e && e[0] == '1') ? 0 : 1;
+  }
+  return g_pair_engine == 0;
+}
+
 // Which configurations the tensor-core engine takes (the rest run on CUDA cores).
 static bool tc_shape_ok(const EngineCall& c) {
   const int elt = bytes_of(c.dtype);
@@ -207,6 +285,11 @@ int run_engine(const EngineCall& c_in, cudaStream_t st) {
   }
   if (tc_shape_ok(c_in)) {
     if (c_in.dtype == BLAST_BF16) {
+      // CTA pairs with resident weights once there is at least one 256-token tile
+      if (!pair_disabled() && c_in.m >= 256 && (c_in.block == 32 || c_in.block == 64)) {
+        int r = c_in.block == 64 ? dispatch_pair_b<64>(c_in, st) : dispatch_pair_b<32>(c_in, st);
+        if (r >= 0) return r;
+      }
       int r = dispatch_tc<__nv_bfloat16, 2, 1>(c_in, nullptr, nullptr, st);
       if (r >= 0) return r;
     } else {
@@ -255,6 +338,12 @@ static bool check_w(const blast_bcsc_t* w) {
 }  // namespace blast
 
 using namespace blast;
+
+extern "C" int blast_set_pair_engine(int enabled) {
+  const int prev = pair_disabled() ? 0 : 1;
+  g_pair_engine = enabled ? 1 : 0;
+  return prev;
+}
 
 extern "C" int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
                            void* stream) {

@@ -1,0 +1,398 @@
+// CTA-pair block-sparse engine (tcgen05 cta_group::2, M = 256 tokens per MMA)
+// with weight blocks kept resident in shared memory across token tiles.
+//
+// Why: at 90% block sparsity the single-CTA engine (spmm_tc.cuh) streams one
+// 128 x b activation panel plus one b x b weight block per 128 x b x b product
+// and is bound by L2 -> SM bandwidth (profiles/r01_*). Here
+//   * a CTA pair computes 256 tokens per MMA: each CTA loads its own 128 rows of
+//     the activation panel (A is M-split) and HALF of every weight block (B is
+//     N-split), halving weight traffic and MMA issue count;
+//   * an item is (output line j, a range of R token tiles): the line's weight
+//     halves are loaded into a resident shared-memory region once per item and
+//     reused for all R tiles, so the weight stream almost disappears. Blocks
+//     beyond the resident capacity are streamed with the activation panel.
+// Same plans, step order (fixed accumulation order) and epilogues as
+// spmm_tc.cuh, so results match the single-CTA engine's contract.
+//
+// Roles per CTA (384 threads): warp 0 TMA producer (both CTAs), warp 1 MMA
+// issuer (leader CTA only), warp 2 TMEM allocator, warps 4..11 epilogue.
+#pragma once
+
+#include "spmm_tc.cuh"
+
+namespace blast {
+
+template <int B, int NMAT, bool SUMACC, bool B_KMAJOR>
+struct PairCfg {
+  static constexpr int ELT = 2;
+  static constexpr int BM = 128;                          // rows per CTA (M = 256 per pair)
+  static constexpr int ROWB = B * ELT;                    // bytes of an activation panel row
+  static constexpr int SW = ROWB < 128 ? ROWB : 128;
+  static constexpr int SWE = SW / ELT;
+  static constexpr int NATOM = ROWB / SW;
+  static constexpr int MMA_K = 16;
+  static constexpr int KSL = B / MMA_K;
+  static constexpr int NA = SUMACC ? NMAT : 1;
+  static constexpr int A_TILE = (BM * ROWB + 1023) / 1024 * 1024;
+  // weight half: MN-major (forward) = [B k-rows x B/2 n-cols]; K-major (transposed
+  // product) = [B/2 n-rows x B k-cols]. Either way B*B/2 elements.
+  static constexpr int WH = B * (B / 2) * ELT;
+  static constexpr int WH_ROWB = B_KMAJOR ? ROWB : (B / 2) * ELT;  // bytes per smem row
+  static constexpr int WH_SW = WH_ROWB < 128 ? WH_ROWB : 128;
+  static constexpr int WH_NATOM = WH_ROWB / WH_SW;
+  static constexpr int WH_ROWS = B_KMAJOR ? B / 2 : B;
+  static constexpr int STAGES = SUMACC ? 3 : 4;
+  static constexpr int STAGE = NA * A_TILE + NMAT * WH;
+  static constexpr int SMEM_BUDGET = 200 * 1024;
+  static constexpr int RES_CAP = (SMEM_BUDGET - STAGES * STAGE) / WH;  // resident blocks
+  static constexpr int NACC = SUMACC ? 1 : NMAT;
+  static constexpr int ACC_STRIDE = NACC * B;
+  static constexpr int TMEM_COLS = 2 * ACC_STRIDE <= 32    ? 32
+                                   : 2 * ACC_STRIDE <= 64  ? 64
+                                   : 2 * ACC_STRIDE <= 128 ? 128
+                                   : 2 * ACC_STRIDE <= 256 ? 256
+                                                           : 512;
+  static constexpr uint32_t IDESC = make_idesc(256, B, 1u, 0u, B_KMAJOR ? 0u : 1u);
+  static constexpr int SMEM_BYTES = STAGES * STAGE + RES_CAP * WH + 256 + 1024;
+  static_assert(RES_CAP >= 4, "resident weight region too small");
+  static_assert(B == 32 || B == 64, "pair engine block sizes");
+  static_assert(2 * ACC_STRIDE <= 512, "accumulators exceed TMEM");
+};
+
+struct PairParams {
+  SpmmParams p;
+  int32_t n_pair_tiles;  // ceil(m / 256)
+  int32_t tiles_per_item;
+  int32_t n_chunks;      // ceil(n_pair_tiles / tiles_per_item)
+};
+
+// descriptor of a weight half for K slice ks (start-address units of 16 B added)
+template <int B, bool B_KMAJOR>
+__device__ __forceinline__ uint32_t wh_koff(int ks) {
+  using C = PairCfg<B, 1, false, B_KMAJOR>;
+  if (B_KMAJOR) {
+    const uint32_t byte_k = static_cast<uint32_t>(ks) * 16 * 2;
+    return ((byte_k / C::WH_SW) * C::WH_ROWS * C::WH_SW + (byte_k % C::WH_SW)) >> 4;
+  }
+  return (static_cast<uint32_t>(ks) * 16 * C::WH_SW) >> 4;
+}
+
+template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+                 const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW1,
+                 const PairParams pp) {
+  using C = PairCfg<B, NMAT, SUMACC, B_KMAJOR>;
+  const SpmmParams& p = pp.p;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* res = smem + C::STAGES * C::STAGE;  // resident weight halves
+  uint64_t* full = reinterpret_cast<uint64_t*>(res + C::RES_CAP * C::WH);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tmem_full = empty + C::STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint64_t* wfull = tmem_empty + 2;
+  uint64_t* wempty = wfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+
+  const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMAs)
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int n_items = pp.n_chunks * p.n_lines;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA0);
+    tma_prefetch(&mapW0);
+    if (NMAT > 1) tma_prefetch(&mapW1);
+    if (SUMACC) tma_prefetch(&mapA1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], 2 * kEpiWarps);
+    }
+    mbar_init(wfull, 1);
+    mbar_init(wempty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    const uint64_t pol_w = policy_evict_last();
+    const uint64_t pol_a = policy_evict_first();
+    const uint32_t full0 = mapa_shared(&full[0], 0);
+    const uint32_t wfull0 = mapa_shared(wfull, 0);
+    uint32_t stage = 0, phase = 0, it = 0;
+    for (int item = pair; item < n_items; item += n_pairs, ++it) {
+      const int chunk = item / p.n_lines;
+      const int j = item - chunk * p.n_lines;
+      const int t0 = chunk * pp.tiles_per_item;
+      const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
+      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      // resident weight halves of this line (first RES_CAP blocks in step order)
+      mbar_wait(wempty, (it & 1) ^ 1);
+      int nres = 0;
+      for (int s = s0; s < s1 && nres < C::RES_CAP; ++s) {
+        const int4 st = __ldg(&p.steps[s]);
+        const int kb[2] = {st.y, st.z};
+#pragma unroll
+        for (int mm = 0; mm < NMAT; ++mm) {
+          if (kb[mm] < 0 || nres >= C::RES_CAP) continue;
+          ++nres;
+        }
+      }
+      if (elect_one()) {
+        if (rank == 0) mbar_expect_tx(wfull, 2u * nres * C::WH);
+        int r = 0;
+        for (int s = s0; s < s1 && r < nres; ++s) {
+          const int4 st = __ldg(&p.steps[s]);
+          const int kb[2] = {st.y, st.z};
+#pragma unroll
+          for (int mm = 0; mm < NMAT; ++mm) {
+            if (kb[mm] < 0 || r >= nres) continue;
+            const CUtensorMap* mw = mm == 0 ? &mapW0 : &mapW1;
+            uint8_t* dst = res + r * C::WH;
+#pragma unroll
+            for (int at = 0; at < C::WH_NATOM; ++at) {
+              if (B_KMAJOR)
+                tma_load_2d_pair(dst + at * C::WH_ROWS * C::WH_SW, mw, wfull0, at * (C::WH_SW / 2),
+                                 kb[mm] * B + static_cast<int>(rank) * (B / 2), pol_w);
+              else
+                tma_load_2d_pair(dst, mw, wfull0, static_cast<int>(rank) * (B / 2), kb[mm] * B,
+                                 pol_w);
+            }
+            ++r;
+          }
+        }
+      }
+      __syncwarp();
+      for (int t = t0; t < t1; ++t) {
+        int rcount = 0;
+        for (int s = s0; s < s1; ++s) {
+          const int4 st = __ldg(&p.steps[s]);
+          const int kb[2] = {st.y, st.z};
+          bool streamed[2] = {false, false};
+          int nstream = 0;
+#pragma unroll
+          for (int mm = 0; mm < NMAT; ++mm) {
+            if (kb[mm] < 0) continue;
+            if (rcount < nres) ++rcount;
+            else { streamed[mm] = true; ++nstream; }
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (elect_one()) {
+            uint32_t bytes = 0;
+#pragma unroll
+            for (int a = 0; a < C::NA; ++a)
+              if (!SUMACC || kb[a] >= 0) bytes += C::BM * C::ROWB;
+            bytes += nstream * C::WH;
+            if (rank == 0) mbar_expect_tx(&full[stage], 2u * bytes);
+            const uint32_t fb = full0 + stage * 8;
+            uint8_t* sbase = smem + stage * C::STAGE;
+            const int row0 = t * 256 + static_cast<int>(rank) * C::BM;
+#pragma unroll
+            for (int a = 0; a < C::NA; ++a) {
+              if (SUMACC && kb[a] < 0) continue;
+              const CUtensorMap* ma = a == 0 ? &mapA0 : &mapA1;
+#pragma unroll
+              for (int at = 0; at < C::NATOM; ++at)
+                tma_load_2d_pair(sbase + a * C::A_TILE + at * C::BM * C::SW, ma, fb,
+                                 st.x * B + at * C::SWE, row0, pol_a);
+            }
+#pragma unroll
+            for (int mm = 0; mm < NMAT; ++mm) {
+              if (!streamed[mm]) continue;
+              const CUtensorMap* mw = mm == 0 ? &mapW0 : &mapW1;
+              uint8_t* dst = sbase + C::NA * C::A_TILE + mm * C::WH;
+#pragma unroll
+              for (int at = 0; at < C::WH_NATOM; ++at) {
+                if (B_KMAJOR)
+                  tma_load_2d_pair(dst + at * C::WH_ROWS * C::WH_SW, mw, fb, at * (C::WH_SW / 2),
+                                   kb[mm] * B + static_cast<int>(rank) * (B / 2), pol_w);
+                else
+                  tma_load_2d_pair(dst, mw, fb, static_cast<int>(rank) * (B / 2), kb[mm] * B,
+                                   pol_w);
+              }
+            }
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1 && rank == 0) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    const uint32_t smem0 = smem_u32(smem);
+    const uint32_t res0 = smem_u32(res);
+    const uint64_t a_desc0 = kmajor_desc<C::SW, C::MMA_K, 2>(smem0, C::BM, 0);
+    const uint64_t wdesc_res0 =
+        B_KMAJOR ? kmajor_desc<C::WH_SW, C::MMA_K, 2>(res0, C::WH_ROWS, 0)
+                 : make_sdesc(res0, C::WH, 8u * C::WH_SW, swizzle_layout_code(C::WH_SW));
+    const uint32_t wstream_off = C::NA * C::A_TILE;
+    const uint64_t wdesc_str0 =
+        B_KMAJOR ? kmajor_desc<C::WH_SW, C::MMA_K, 2>(smem0 + wstream_off, C::WH_ROWS, 0)
+                 : make_sdesc(smem0 + wstream_off, C::WH, 8u * C::WH_SW,
+                              swizzle_layout_code(C::WH_SW));
+    auto a_koff = [](int ks) -> uint32_t {
+      const uint32_t byte_k = static_cast<uint32_t>(ks) * 32;
+      return ((byte_k / C::SW) * C::BM * C::SW + (byte_k % C::SW)) >> 4;
+    };
+    uint32_t stage = 0, phase = 0, it = 0, tile_it = 0;
+    for (int item = pair; item < n_items; item += n_pairs, ++it) {
+      const int chunk = item / p.n_lines;
+      const int j = item - chunk * p.n_lines;
+      const int t0 = chunk * pp.tiles_per_item;
+      const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
+      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      mbar_wait(wfull, it & 1);
+      tc_fence_after();
+      for (int t = t0; t < t1; ++t, ++tile_it) {
+        const uint32_t as = tile_it & 1, use = tile_it >> 1;
+        mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
+        uint32_t init0 = 0, init1 = 0;
+        int rcount = 0;
+        for (int s = s0; s < s1; ++s) {
+          const int4 st = __ldg(&p.steps[s]);
+          const int kb[2] = {st.y, st.z};
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t soff = (stage * C::STAGE) >> 4;
+          int ridx[2] = {-1, -1};
+#pragma unroll
+          for (int mm = 0; mm < NMAT; ++mm) {
+            if (kb[mm] < 0) continue;
+            ridx[mm] = rcount < C::RES_CAP ? rcount : -1;
+            ++rcount;
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int mm = 0; mm < NMAT; ++mm) {
+              if (kb[mm] < 0) continue;
+              const int acc_i = SUMACC ? 0 : mm;
+              const int a_i = SUMACC ? mm : 0;
+              const uint32_t d = d_base + acc_i * B;
+              const uint64_t ad = a_desc0 + soff + ((a_i * C::A_TILE) >> 4);
+              const uint64_t wd = ridx[mm] >= 0 ? wdesc_res0 + ((ridx[mm] * C::WH) >> 4)
+                                                : wdesc_str0 + soff + ((mm * C::WH) >> 4);
+              const uint32_t init = acc_i == 0 ? init0 : init1;
+#pragma unroll
+              for (int ks = 0; ks < C::KSL; ++ks)
+                mma_f16_pair(d, ad + a_koff(ks), wd + wh_koff<B, B_KMAJOR>(ks), C::IDESC,
+                             (init | ks) ? 1u : 0u);
+              if (acc_i == 0) init0 = 1; else init1 = 1;
+            }
+            mma_commit_pair(&empty[stage]);
+          }
+          __syncwarp();
+          if (kb[0] >= 0) init0 = 1;
+          if (NMAT > 1 && kb[1] >= 0) { if (SUMACC) init0 = 1; else init1 = 1; }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) mma_commit_pair(&tmem_full[as]);
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit_pair(wempty);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint32_t q = warp & 3;
+    const int half = static_cast<int>(warp - 4) >> 2;
+    const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
+    uint32_t tile_it = 0;
+    for (int item = pair; item < n_items; item += n_pairs) {
+      const int chunk = item / p.n_lines;
+      const int j = item - chunk * p.n_lines;
+      const int t0 = chunk * pp.tiles_per_item;
+      const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
+      const int flags = __ldg(&p.line_flags[j]);
+      for (int t = t0; t < t1; ++t, ++tile_it) {
+        const uint32_t as = tile_it & 1, use = tile_it >> 1;
+        mbar_wait(&tmem_full[as], use & 1);
+        tc_fence_after();
+        const int row = t * 256 + static_cast<int>(rank) * C::BM + static_cast<int>(q * 32 + lane);
+        const bool row_ok = row < p.m;
+        const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
+#pragma unroll 1
+        for (int c = half; c < B / 16; c += 2) {
+          const int col = j * B + c * 16;
+          const int valid = p.n_valid - col;
+          const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
+          float v0[16];
+          tmem_ld16(tbase + c * 16, v0);
+          const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
+          if (!acc0_init) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
+          }
+          if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
+            if (row_ok && valid > 0) {
+              if (p.accumulate) {
+                float prev[16];
+                load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.out0) + off, prev, valid, vec_ok);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v0[i] = __fadd_rn(prev[i], v0[i]);
+              }
+              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
+            }
+          } else if constexpr (EPI == EPI_GATED_FWD) {
+            float v1[16];
+            tmem_ld16(tbase + B + c * 16, v1);
+            if (!(flags & 2)) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v1[i] = 0.0f;
+            }
+            if (row_ok && valid > 0) {
+              if (p.out1) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
+              if (p.out2) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out2) + off, v1, valid, vec_ok);
+              float g[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) g[i] = gated_fwd(v0[i], v1[i]);
+              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
+            }
+          } else {
+            if (row_ok && valid > 0) {
+              float a[16], b[16], da[16], db[16];
+              load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, a, valid, vec_ok);
+              load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in1) + off, b, valid, vec_ok);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
+              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, da, valid, vec_ok);
+              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, db, valid, vec_ok);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&tmem_empty[as]);
+          else mbar_arrive_cluster(&tmem_empty[as], 0);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace blast
