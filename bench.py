@@ -93,17 +93,16 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
                 mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 try:
                     r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 except AttributeError:
                     r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                if util > 0:
-                    self.samples.append(mhz)
-                    for bit, name in self.REASONS.items():
-                        if r & bit:
-                            self.reasons.add(name)
+                # the sampler only runs while the timed region is executing
+                self.samples.append(mhz)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
             except Exception:
                 pass
             time.sleep(0.002)

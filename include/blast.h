@@ -77,8 +77,9 @@ const char* blast_last_error(void);
 int blast_version(void);
 int blast_num_sms(void);
 /* Engine selection for bf16 products with >= 256 rows and b in {32, 64}: 1 = CTA-pair
- * engine with resident weights (default), 0 = single-CTA engine. Returns the previous
- * setting. Both give the same accumulation order; used for ablations and tests. */
+ * engine (cta_group::2) with resident weights, 0 = single-CTA engine (default; also
+ * BLAST_PAIR_ENGINE=1 in the environment). Returns the previous setting. Both give the
+ * same accumulation order (bitwise equal results); used for ablations and tests. */
 int blast_set_pair_engine(int enabled);
 
 /* ---------------------------------------------------------------- format / plans */

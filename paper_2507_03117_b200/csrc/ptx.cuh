@@ -230,12 +230,16 @@ __device__ __forceinline__ void cluster_sync() {
                    : "memory");
 }
 // Arrive on the mbarrier at the same shared offset in CTA `rank` of the cluster.
+// Default (.release.cta) semantics: a .cluster release would fence every
+// outstanding global store of the arriving warp (MEMBAR.ALL.GPU), stalling the
+// epilogue; the only hazard it guards (TMEM reads before the accumulator is
+// reused) is ordered by tcgen05.fence::before_thread_sync instead.
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   asm volatile(
       "{\n"
       ".reg .b32 ra;\n"
       "mapa.shared::cluster.u32 ra, %0, %1;\n"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(rank)
       : "memory");

@@ -41,8 +41,37 @@ struct EngineCall {
   int64_t ld_out = 0;
 };
 
+// BLAST_DEBUG_COUNTERS=1: per-role wait cycles of every tensor-core launch to stderr
+// (synchronizes after each launch; diagnosis only).
+static unsigned long long* dbg_buffer() {
+  static unsigned long long* buf = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BLAST_DEBUG_COUNTERS");
+    on = (e && e[0] == '1') ? 1 : 0;
+    if (on && cudaMalloc(&buf, 8 * sizeof(unsigned long long)) != cudaSuccess) on = 0;
+  }
+  return on ? buf : nullptr;
+}
+static void dbg_begin(cudaStream_t st) {
+  if (auto* b = dbg_buffer()) cudaMemsetAsync(b, 0, 8 * sizeof(unsigned long long), st);
+}
+static void dbg_end(const char* name, cudaStream_t st, int ctas) {
+  auto* b = dbg_buffer();
+  if (!b) return;
+  unsigned long long h[8];
+  cudaMemcpyAsync(h, b, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  const double n = ctas > 0 ? ctas : 1;
+  fprintf(stderr,
+          "[blast dbg] %s ctas=%d per-CTA cycles: prod.wait_empty=%.0f prod.wait_wempty=%.0f "
+          "mma.wait_full=%.0f mma.wait_acc=%.0f mma.wait_w=%.0f epi.wait_acc=%.0f steps=%.0f\n",
+          name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[7] / n);
+}
+
 static SpmmParams make_params(const EngineCall& c) {
   SpmmParams p{};
+  p.dbg = dbg_buffer();
   p.m = static_cast<int32_t>(c.m);
   p.n_lines = static_cast<int32_t>(c.n_lines);
   p.n_valid = static_cast<int32_t>(c.n_valid);
@@ -111,9 +140,12 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
+  dbg_begin(st);
   kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo,
                                                   p);
-  return check_launch("spmm_tc");
+  const int rc = check_launch("spmm_tc");
+  dbg_end("spmm_tc", st, grid);
+  return rc;
 }
 
 // Compile-time guard: does this configuration have >= 2 pipeline stages?
@@ -155,6 +187,15 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
 }
 
 // ---------------------------------------------------------------- CTA-pair engine
+static int pair_stages_override() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("BLAST_PAIR_STAGES");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int B, int NMAT, bool SUM, bool BK, int EPI>
 static int launch_pair(const EngineCall& c, cudaStream_t st) {
   using Cfg = PairCfg<B, NMAT, SUM, BK>;
@@ -193,14 +234,26 @@ static int launch_pair(const EngineCall& c, cudaStream_t st) {
   pp.n_pair_tiles = static_cast<int32_t>(cdiv(c.m, 256));
   const int64_t n_pairs = num_sms() / 2;
   int64_t r = (c.n_lines * pp.n_pair_tiles) / (12 * n_pairs);
+  if (const char* e = getenv("BLAST_PAIR_R")) r = atoi(e);
   r = std::max<int64_t>(1, std::min<int64_t>(r, pp.n_pair_tiles));
   pp.tiles_per_item = static_cast<int32_t>(r);
   pp.n_chunks = static_cast<int32_t>(cdiv(pp.n_pair_tiles, r));
+  // Pipeline depth vs resident weights: deep enough to cover the L2 latency
+  // (~1.5 us at load), the remaining shared memory holds resident weight halves.
+  int stages = pair_stages_override();
+  if (stages <= 0) stages = std::min(Cfg::MAX_STAGES, (120 * 1024) / (Cfg::NA * Cfg::A_TILE) + 1);
+  stages = std::max(2, std::min(stages, std::min(Cfg::MAX_STAGES, Cfg::DATA_BYTES / Cfg::STAGE)));
+  pp.n_stages = stages;
+  pp.res_cap = (Cfg::DATA_BYTES - stages * Cfg::STAGE) / Cfg::WH;
+  if (const char* e = getenv("BLAST_PAIR_RESCAP")) pp.res_cap = std::min(pp.res_cap, atoi(e));
   const int64_t items = static_cast<int64_t>(pp.n_chunks) * c.n_lines;
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(2 * std::min<int64_t>(items, n_pairs));
+  dbg_begin(st);
   kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mA0, mA1, mW0, mW1, pp);
-  return check_launch("spmm_pair");
+  const int rc = check_launch("spmm_pair");
+  dbg_end("spmm_pair", st, grid);
+  return rc;
 }
 
 template <int B>
@@ -221,12 +274,16 @@ static int dispatch_pair_b(const EngineCall& c, cudaStream_t st) {
   return -1;
 }
 
-static int g_pair_engine = -1;  // -1: from BLAST_DISABLE_PAIR, else 0/1
+// The pair engine halves weight traffic but both engines sit on the same
+// shared-memory operand bandwidth ceiling at b = 64 (tools/mma_rate.cu,
+// profiles/); measured on cfg3 the single-CTA engine is still faster, so the
+// pair engine is opt-in (BLAST_PAIR_ENGINE=1 or blast_set_pair_engine(1)).
+static int g_pair_engine = -1;  // -1: from the environment, else 0/1
 
 static bool pair_disabled() {
   if (g_pair_engine < 0) {
-    const char* e = getenv("BLAST_DISABLE_PAIR");
-    g_pair_engine = (e && e[0] == '1') ? 0 : 1;
+    const char* e = getenv("BLAST_PAIR_ENGINE");
+    g_pair_engine = (e && e[0] == '1') ? 1 : 0;
   }
   return g_pair_engine == 0;
 }

@@ -41,10 +41,11 @@ struct PairCfg {
   static constexpr int WH_SW = WH_ROWB < 128 ? WH_ROWB : 128;
   static constexpr int WH_NATOM = WH_ROWB / WH_SW;
   static constexpr int WH_ROWS = B_KMAJOR ? B / 2 : B;
-  static constexpr int STAGES = SUMACC ? 3 : 4;
+  static constexpr int MAX_STAGES = 12;
   static constexpr int STAGE = NA * A_TILE + NMAT * WH;
-  static constexpr int SMEM_BUDGET = 200 * 1024;
-  static constexpr int RES_CAP = (SMEM_BUDGET - STAGES * STAGE) / WH;  // resident blocks
+  // dynamic shared memory: [1 KiB barriers][n_stages x STAGE][res_cap x WH]
+  static constexpr int SMEM_BYTES = 220 * 1024;
+  static constexpr int DATA_BYTES = SMEM_BYTES - 2048;  // minus barriers and alignment slack
   static constexpr int NACC = SUMACC ? 1 : NMAT;
   static constexpr int ACC_STRIDE = NACC * B;
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE <= 32    ? 32
@@ -53,8 +54,6 @@ struct PairCfg {
                                    : 2 * ACC_STRIDE <= 256 ? 256
                                                            : 512;
   static constexpr uint32_t IDESC = make_idesc(256, B, 1u, 0u, B_KMAJOR ? 0u : 1u);
-  static constexpr int SMEM_BYTES = STAGES * STAGE + RES_CAP * WH + 256 + 1024;
-  static_assert(RES_CAP >= 4, "resident weight region too small");
   static_assert(B == 32 || B == 64, "pair engine block sizes");
   static_assert(2 * ACC_STRIDE <= 512, "accumulators exceed TMEM");
 };
@@ -64,6 +63,8 @@ struct PairParams {
   int32_t n_pair_tiles;  // ceil(m / 256)
   int32_t tiles_per_item;
   int32_t n_chunks;      // ceil(n_pair_tiles / tiles_per_item)
+  int32_t n_stages;      // pipeline depth (activation panels in flight per CTA)
+  int32_t res_cap;       // resident weight halves per line (the rest is streamed)
 };
 
 // descriptor of a weight half for K slice ks (start-address units of 16 B added)
@@ -86,14 +87,17 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
   const SpmmParams& p = pp.p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* res = smem + C::STAGES * C::STAGE;  // resident weight halves
-  uint64_t* full = reinterpret_cast<uint64_t*>(res + C::RES_CAP * C::WH);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tmem_full = empty + C::STAGES;
+  const int NST = pp.n_stages;
+  const int RCAP = pp.res_cap;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + C::MAX_STAGES;
+  uint64_t* tmem_full = empty + C::MAX_STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
   uint64_t* wfull = tmem_empty + 2;
   uint64_t* wempty = wfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
+  uint8_t* stages = smem + 1024;               // activation panels (+ streamed weights)
+  uint8_t* res = stages + NST * C::STAGE;      // resident weight halves
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -106,7 +110,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
     tma_prefetch(&mapW0);
     if (NMAT > 1) tma_prefetch(&mapW1);
     if (SUMACC) tma_prefetch(&mapA1);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -126,11 +130,14 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  WaitClock wc;
+  const bool dbg_on = p.dbg != nullptr;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     const uint64_t pol_w = policy_evict_last();
-    const uint64_t pol_a = policy_evict_first();
+    // activation panels are re-read by every line of the same token tile: keep them in L2
+    const uint64_t pol_a = policy_evict_last();
     const uint32_t full0 = mapa_shared(&full[0], 0);
     const uint32_t wfull0 = mapa_shared(wfull, 0);
     uint32_t stage = 0, phase = 0, it = 0;
@@ -141,46 +148,54 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
       const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
       const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
       // resident weight halves of this line (first RES_CAP blocks in step order)
-      mbar_wait(wempty, (it & 1) ^ 1);
+      wc.wait(1, wempty, (it & 1) ^ 1, dbg_on);
       int nres = 0;
-      for (int s = s0; s < s1 && nres < C::RES_CAP; ++s) {
-        const int4 st = __ldg(&p.steps[s]);
-        const int kb[2] = {st.y, st.z};
-#pragma unroll
-        for (int mm = 0; mm < NMAT; ++mm) {
-          if (kb[mm] < 0 || nres >= C::RES_CAP) continue;
-          ++nres;
+      {
+        StepCursor cur;
+        cur.start(p.steps, s0, s1);
+        for (int s = s0; s < s1 && nres < RCAP; ++s) {
+          const int4 st = cur.get(s);
+          nres += (st.y >= 0 ? 1 : 0);
+          if (NMAT > 1 && nres < RCAP) nres += (st.z >= 0 ? 1 : 0);
         }
       }
-      if (elect_one()) {
-        if (rank == 0) mbar_expect_tx(wfull, 2u * nres * C::WH);
+      if (rank == 0 && elect_one()) mbar_expect_tx(wfull, 2u * nres * C::WH);
+      __syncwarp();
+      {
+        StepCursor cur;
+        cur.start(p.steps, s0, s1);
         int r = 0;
         for (int s = s0; s < s1 && r < nres; ++s) {
-          const int4 st = __ldg(&p.steps[s]);
+          const int4 st = cur.get(s);
           const int kb[2] = {st.y, st.z};
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm) {
             if (kb[mm] < 0 || r >= nres) continue;
-            const CUtensorMap* mw = mm == 0 ? &mapW0 : &mapW1;
-            uint8_t* dst = res + r * C::WH;
+            if (elect_one()) {
+              const CUtensorMap* mw = mm == 0 ? &mapW0 : &mapW1;
+              uint8_t* dst = res + r * C::WH;
 #pragma unroll
-            for (int at = 0; at < C::WH_NATOM; ++at) {
-              if (B_KMAJOR)
-                tma_load_2d_pair(dst + at * C::WH_ROWS * C::WH_SW, mw, wfull0, at * (C::WH_SW / 2),
-                                 kb[mm] * B + static_cast<int>(rank) * (B / 2), pol_w);
-              else
-                tma_load_2d_pair(dst, mw, wfull0, static_cast<int>(rank) * (B / 2), kb[mm] * B,
-                                 pol_w);
+              for (int at = 0; at < C::WH_NATOM; ++at) {
+                if (B_KMAJOR)
+                  tma_load_2d_pair(dst + at * C::WH_ROWS * C::WH_SW, mw, wfull0,
+                                   at * (C::WH_SW / 2),
+                                   kb[mm] * B + static_cast<int>(rank) * (B / 2), pol_w);
+                else
+                  tma_load_2d_pair(dst, mw, wfull0, static_cast<int>(rank) * (B / 2), kb[mm] * B,
+                                   pol_w);
+              }
             }
+            __syncwarp();
             ++r;
           }
         }
       }
-      __syncwarp();
       for (int t = t0; t < t1; ++t) {
         int rcount = 0;
+        StepCursor cur;
+        cur.start(p.steps, s0, s1);
         for (int s = s0; s < s1; ++s) {
-          const int4 st = __ldg(&p.steps[s]);
+          const int4 st = cur.get(s);
           const int kb[2] = {st.y, st.z};
           bool streamed[2] = {false, false};
           int nstream = 0;
@@ -190,7 +205,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
             if (rcount < nres) ++rcount;
             else { streamed[mm] = true; ++nstream; }
           }
-          mbar_wait(&empty[stage], phase ^ 1);
+          wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
           if (elect_one()) {
             uint32_t bytes = 0;
 #pragma unroll
@@ -199,7 +214,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
             bytes += nstream * C::WH;
             if (rank == 0) mbar_expect_tx(&full[stage], 2u * bytes);
             const uint32_t fb = full0 + stage * 8;
-            uint8_t* sbase = smem + stage * C::STAGE;
+            uint8_t* sbase = stages + stage * C::STAGE;
             const int row0 = t * 256 + static_cast<int>(rank) * C::BM;
 #pragma unroll
             for (int a = 0; a < C::NA; ++a) {
@@ -227,13 +242,13 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
             }
           }
           __syncwarp();
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1 && rank == 0) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
-    const uint32_t smem0 = smem_u32(smem);
+    const uint32_t smem0 = smem_u32(stages);
     const uint32_t res0 = smem_u32(res);
     const uint64_t a_desc0 = kmajor_desc<C::SW, C::MMA_K, 2>(smem0, C::BM, 0);
     const uint64_t wdesc_res0 =
@@ -255,26 +270,29 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
       const int t0 = chunk * pp.tiles_per_item;
       const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
       const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
-      mbar_wait(wfull, it & 1);
+      wc.wait(4, wfull, it & 1, dbg_on);
       tc_fence_after();
       for (int t = t0; t < t1; ++t, ++tile_it) {
         const uint32_t as = tile_it & 1, use = tile_it >> 1;
-        mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+        wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
         tc_fence_after();
         const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
         uint32_t init0 = 0, init1 = 0;
         int rcount = 0;
+        StepCursor cur;
+        cur.start(p.steps, s0, s1);
         for (int s = s0; s < s1; ++s) {
-          const int4 st = __ldg(&p.steps[s]);
+          const int4 st = cur.get(s);
           const int kb[2] = {st.y, st.z};
-          mbar_wait(&full[stage], phase);
+          wc.wait(2, &full[stage], phase, dbg_on);
+          wc.acc[7] += dbg_on;
           tc_fence_after();
           const uint32_t soff = (stage * C::STAGE) >> 4;
           int ridx[2] = {-1, -1};
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm) {
             if (kb[mm] < 0) continue;
-            ridx[mm] = rcount < C::RES_CAP ? rcount : -1;
+            ridx[mm] = rcount < RCAP ? rcount : -1;
             ++rcount;
           }
           if (elect_one()) {
@@ -299,7 +317,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
           __syncwarp();
           if (kb[0] >= 0) init0 = 1;
           if (NMAT > 1 && kb[1] >= 0) { if (SUMACC) init0 = 1; else init1 = 1; }
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         if (elect_one()) mma_commit_pair(&tmem_full[as]);
         __syncwarp();
@@ -321,7 +339,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
       const int flags = __ldg(&p.line_flags[j]);
       for (int t = t0; t < t1; ++t, ++tile_it) {
         const uint32_t as = tile_it & 1, use = tile_it >> 1;
-        mbar_wait(&tmem_full[as], use & 1);
+        wc.wait(5, &tmem_full[as], use & 1, dbg_on);
         tc_fence_after();
         const int row = t * 256 + static_cast<int>(rank) * C::BM + static_cast<int>(q * 32 + lane);
         const bool row_ok = row < p.m;
@@ -387,6 +405,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
     }
   }
 
+  if (warp == 0 || warp == 1 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {

@@ -45,6 +45,59 @@ struct SpmmParams {
   const void* in0;  // bwd: gate_pre
   const void* in1;  // bwd: up_out
   int64_t ld_out;   // row stride (elements) of every out*/in* array
+  unsigned long long* dbg;  // optional per-role wait-cycle counters (BLAST_DEBUG_COUNTERS)
+};
+
+// Role-level wait accounting for pipeline diagnosis (only when p.dbg is set):
+// 0 producer waits on empty, 1 producer waits on resident-weight release,
+// 2 MMA waits on full, 3 MMA waits on accumulator release, 4 MMA waits on
+// resident weights, 5 epilogue waits on accumulator, 6 epilogue busy, 7 MMA steps.
+struct WaitClock {
+  unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  __device__ __forceinline__ void wait(int slot, uint64_t* bar, uint32_t parity, bool on) {
+    if (!on) {
+      mbar_wait(bar, parity);
+      return;
+    }
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc[slot] += static_cast<unsigned long long>(clock64() - t0);
+  }
+  __device__ __forceinline__ void flush(unsigned long long* dbg) {
+    if (!dbg || lane_id() != 0) return;
+    for (int i = 0; i < 8; ++i)
+      if (acc[i]) atomicAdd(&dbg[i], acc[i]);
+  }
+};
+
+// Warp-cooperative reader of a line's step list: one coalesced load fetches 32
+// steps (one per lane) and each step is then broadcast with shuffles, so the
+// producer / MMA loops never wait on a dependent global load per step. Must be
+// used by a full, converged warp.
+struct StepCursor {
+  const int4* steps;
+  int end;
+  int base;
+  int4 mine;
+  __device__ __forceinline__ void fetch() {
+    const int idx = base + static_cast<int>(lane_id());
+    mine = idx < end ? __ldg(&steps[idx]) : make_int4(0, -1, -1, 0);
+  }
+  __device__ __forceinline__ void start(const int4* s, int s0, int s1) {
+    steps = s;
+    end = s1;
+    base = s0;
+    fetch();
+  }
+  __device__ __forceinline__ int4 get(int s) {
+    if (s - base >= 32) {
+      base += 32;
+      fetch();
+    }
+    const int i = s - base;
+    return make_int4(__shfl_sync(0xffffffffu, mine.x, i), __shfl_sync(0xffffffffu, mine.y, i),
+                     __shfl_sync(0xffffffffu, mine.z, i), 0);
+  }
 };
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR>
@@ -203,6 +256,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  WaitClock wc;
+  const bool dbg_on = p.dbg != nullptr;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -214,10 +269,12 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
       const int t = item / p.n_lines;
       const int j = item - t * p.n_lines;
       const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      StepCursor cur;
+      cur.start(p.steps, s0, s1);
       for (int s = s0; s < s1; ++s) {
-        const int4 st = __ldg(&p.steps[s]);
+        const int4 st = cur.get(s);
         const int kb[2] = {st.y, st.z};
-        mbar_wait(&empty[stage], phase ^ 1);
+        wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
         if (elect_one()) {
           uint32_t bytes = 0;
 #pragma unroll
@@ -296,15 +353,18 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
       const int j = item - t * p.n_lines;
       (void)t;
       const uint32_t as = it & 1, use = it >> 1;
-      mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+      wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
       tc_fence_after();
       uint32_t init0 = 0, init1 = 0;
       const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
       const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
+      StepCursor cur;
+      cur.start(p.steps, s0, s1);
       for (int s = s0; s < s1; ++s) {
-        const int4 st = __ldg(&p.steps[s]);
+        const int4 st = cur.get(s);
         const bool has0 = st.y >= 0, has1 = NMAT > 1 && st.z >= 0;
-        mbar_wait(&full[stage], phase);
+        wc.wait(2, &full[stage], phase, dbg_on);
+        wc.acc[7] += dbg_on;
         tc_fence_after();
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
@@ -368,7 +428,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
       const int j = item - t * p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
       const int flags = __ldg(&p.line_flags[j]);
-      mbar_wait(&tmem_full[as], use & 1);
+      wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
       const int row = t * C::BM + static_cast<int>(q * 32 + lane);
       const bool row_ok = row < p.m;
@@ -430,6 +490,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
     }
   }
 
+  if (warp == 0 || warp == 1 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {

@@ -98,6 +98,15 @@ class SparseMlp:
         total = sum(m.mask.grid_rows * m.mask.grid_cols for m in self.matrices())
         return 1.0 - active / total
 
+    def workspace(self, m: int) -> torch.Tensor:
+        """Intermediate-activation buffer reused across inference calls (grow-only), so a
+        forward never pays an allocation."""
+        ws = self._plan_cache.get("ws")
+        if ws is None or ws.dtype != self.dtype or ws.numel() < m * self.hidden_dim:
+            ws = torch.empty(max(m, 1) * self.hidden_dim, dtype=self.dtype, device=A.DEVICE)
+            self._plan_cache["ws"] = ws
+        return ws[: m * self.hidden_dim].view(m, self.hidden_dim)
+
     def plan(self) -> L.MlpPlanDesc:
         """Merged gate/up step lists (csrc/plan.cu), rebuilt when a cache is replaced."""
         g, u = self.gate.cache, self.up.cache
@@ -107,7 +116,10 @@ class SparseMlp:
             gu = bcsc.build_plan(g._kmap(), u._kmap(), gr, gc, 0)
             dx = bcsc.build_plan(g._kmap(), u._kmap(), gr, gc, 1)
             desc = L.MlpPlanDesc(*(t.data_ptr() for t in gu), *(t.data_ptr() for t in dx))
+            ws = self._plan_cache.get("ws")
             self._plan_cache = {"key": key, "tensors": (gu, dx, g, u), "desc": desc}
+            if ws is not None:
+                self._plan_cache["ws"] = ws
         return self._plan_cache["desc"]
 
 
@@ -140,9 +152,11 @@ def mlp_forward(x, mlp: SparseMlp, save_activations: bool = True):
     xt = A.to_device(x, dt)
     m, e, h = xt.shape[0], mlp.embed_dim, mlp.hidden_dim
     y = torch.empty(m, e, dtype=dt, device=A.DEVICE)
-    a = b = g = None
+    a = b = None
     if save_activations:
         a, b, g = (torch.empty(m, h, dtype=dt, device=A.DEVICE) for _ in range(3))
+    else:
+        g = mlp.workspace(m)
     if m:
         dg, du, dd = (mat.cache.desc() for mat in mlp.matrices())
         plan = mlp.plan()
