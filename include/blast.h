@@ -104,6 +104,11 @@ int blast_tf32_prepare(const float* values, int64_t nnzb, int32_t block, float* 
 /* Y[m, w.cols] = act(X[m, w.rows] @ W)       kernels.py:86 bspmm / :127 bspmm_fused */
 int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
                 void* stream);
+/* Y = act(X @ W + bias): bias is float32 [w.cols] (or NULL), added in the epilogue before
+ * the activation. Used by the GPT-2 MLP integration (Conv1D carries a bias; the
+ * reference bspmm_fused has none, kernels.py:127). */
+int blast_bspmm_bias(const void* x, int64_t m, const blast_bcsc_t* w, const float* bias, int act,
+                     void* y, void* stream);
 /* Y[m, w.rows] = X[m, w.cols] @ W^T           kernels.py:143 bspmm_rt */
 int blast_bspmm_rt(const void* x, int64_t m, const blast_bcsc_t* w, void* y, void* stream);
 /* Elementwise activation (kernels.py:50-62 apply_nonlinearity); in-place allowed. */

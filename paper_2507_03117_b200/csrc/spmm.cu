@@ -39,6 +39,7 @@ struct EngineCall {
   const void* in0 = nullptr;
   const void* in1 = nullptr;
   int64_t ld_out = 0;
+  const float* bias = nullptr;
 };
 
 // BLAST_DEBUG_COUNTERS=1: per-role wait cycles of every tensor-core launch to stderr
@@ -87,6 +88,7 @@ static SpmmParams make_params(const EngineCall& c) {
   p.in0 = c.in0;
   p.in1 = c.in1;
   p.ld_out = c.ld_out;
+  p.bias = c.bias;
   return p;
 }
 
@@ -404,6 +406,11 @@ extern "C" int blast_set_pair_engine(int enabled) {
 
 extern "C" int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
                            void* stream) {
+  return blast_bspmm_bias(x, m, w, nullptr, act, y, stream);
+}
+
+extern "C" int blast_bspmm_bias(const void* x, int64_t m, const blast_bcsc_t* w,
+                                const float* bias, int act, void* y, void* stream) {
   if (!check_w(w)) return BLAST_EINVAL;
   if (act < 0 || act > 3) {
     set_error("unknown nonlinearity code %d", act);
@@ -413,6 +420,7 @@ extern "C" int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int 
   c.dtype = w->dtype;
   c.block = w->block;
   c.act = act;
+  c.bias = bias;
   c.m = m;
   c.a_cols = w->rows;
   c.a0 = x;

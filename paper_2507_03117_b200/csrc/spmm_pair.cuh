@@ -357,6 +357,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
             for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
           }
           if constexpr (EPI == EPI_STORE) {
+            add_bias16(v0, p.bias, col, valid);
 #pragma unroll
             for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
             if (row_ok && valid > 0) {

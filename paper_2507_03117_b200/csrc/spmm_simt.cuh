@@ -70,7 +70,9 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const SpmmParams p, cons
     (void)flags;
     const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
     if (s.epi == EPI_STORE) {
-      float v = apply_act(acc[0], p.act);
+      float v = acc[0];
+      if (p.bias) v = __fadd_rn(v, p.bias[col]);
+      v = apply_act(v, p.act);
       if (p.accumulate) v = __fadd_rn(to_f32<T>(static_cast<T*>(p.out0)[off]), v);
       static_cast<T*>(p.out0)[off] = from_f32<T>(v);
     } else if (s.epi == EPI_GATED_FWD) {

@@ -46,7 +46,16 @@ struct SpmmParams {
   const void* in1;  // bwd: up_out
   int64_t ld_out;   // row stride (elements) of every out*/in* array
   unsigned long long* dbg;  // optional per-role wait-cycle counters (BLAST_DEBUG_COUNTERS)
+  const float* bias;        // EPI_STORE: optional per-output-column bias, added before act
 };
+
+// v[i] += bias[col + i] for the valid columns of a 16-column chunk
+__device__ __forceinline__ void add_bias16(float (&v)[16], const float* bias, int col, int valid) {
+  if (!bias) return;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (i < valid) v[i] = __fadd_rn(v[i], __ldg(&bias[col + i]));
+}
 
 // Role-level wait accounting for pipeline diagnosis (only when p.dbg is set):
 // 0 producer waits on empty, 1 producer waits on resident-weight release,
@@ -446,6 +455,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
           for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
         }
         if constexpr (EPI == EPI_STORE) {
+          add_bias16(v0, p.bias, col, valid);
 #pragma unroll
           for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
           if (row_ok && valid > 0) {

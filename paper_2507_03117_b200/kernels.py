@@ -104,19 +104,25 @@ def _check_lhs(x, w: BlockSparseMatrix, expected_cols: int) -> torch.Tensor:
     return A.to_device(x, w.values.dtype)
 
 
-def _product(x, w: BlockSparseMatrix, act: int, transposed: bool):
+def _product(x, w: BlockSparseMatrix, act: int, transposed: bool, bias=None):
     host = A.is_host(x) or (w.host_api and not isinstance(x, torch.Tensor))
     xt = _check_lhs(x, w, w.cols if transposed else w.rows)
     m = xt.shape[0]
     out_cols = w.rows if transposed else w.cols
     y = torch.empty(m, out_cols, dtype=w.values.dtype, device=A.DEVICE)
+    bias_t = None
+    if bias is not None:
+        bias_t = A.to_device(bias, torch.float32).reshape(-1)
+        if bias_t.numel() != out_cols:
+            raise ValueError(f"bias has {bias_t.numel()} entries, expected {out_cols}")
     if m:
         d = w.desc()
         lib = L.load()
         if transposed:
             rc = lib.blast_bspmm_rt(xt.data_ptr(), m, C.byref(d), y.data_ptr(), L.stream())
         else:
-            rc = lib.blast_bspmm(xt.data_ptr(), m, C.byref(d), act, y.data_ptr(), L.stream())
+            rc = lib.blast_bspmm_bias(xt.data_ptr(), m, C.byref(d), L.ptr(bias_t), act,
+                                      y.data_ptr(), L.stream())
         L.check(rc, "bspmm_rt" if transposed else "bspmm")
     return A.like_input(y, host)
 
@@ -134,12 +140,15 @@ def bspmm(x, w: BlockSparseMatrix, blk_m: int | None = None):
     return _product(x, w, 0, False)
 
 
-def bspmm_fused(x, w: BlockSparseMatrix, f: str = "none", blk_m: int | None = None):
-    """f(X @ W) with f applied in the kernel epilogue (kernels.py:127-140)."""
+def bspmm_fused(x, w: BlockSparseMatrix, f: str = "none", blk_m: int | None = None,
+                bias=None):
+    """f(X @ W [+ bias]) with bias and f applied in the kernel epilogue
+    (kernels.py:127-140; the optional bias serves biased model layers such as
+    GPT-2's Conv1D)."""
     code = _act_code(f)
     if blk_m is not None and blk_m < 1:
         raise ValueError(f"blk_m must be >= 1, got {blk_m}")
-    return _product(x, w, code, False)
+    return _product(x, w, code, False, bias)
 
 
 def bspmm_rt(x, w: BlockSparseMatrix):
