@@ -105,10 +105,15 @@ int blast_tf32_prepare(const float* values, int64_t nnzb, int32_t block, float* 
 int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
                 void* stream);
 /* Y = act(X @ W + bias): bias is float32 [w.cols] (or NULL), added in the epilogue before
- * the activation. Used by the GPT-2 MLP integration (Conv1D carries a bias; the
- * reference bspmm_fused has none, kernels.py:127). */
-int blast_bspmm_bias(const void* x, int64_t m, const blast_bcsc_t* w, const float* bias, int act,
-                     void* y, void* stream);
+ * the activation; pre (optional, same shape/dtype as Y) receives X @ W + bias for the
+ * backward. Used by the GPT-2 MLP integration (Conv1D carries a bias; the reference
+ * bspmm_fused has none, kernels.py:127). */
+int blast_bspmm_ex(const void* x, int64_t m, const blast_bcsc_t* w, const float* bias, int act,
+                   void* y, void* pre, void* stream);
+/* Backward of a fused activation: Y[m, w.rows] = (X[m, w.cols] @ W^T) * act'(pre), where pre
+ * [m, w.rows] is the saved pre-activation of the layer feeding W. */
+int blast_bspmm_rt_act(const void* x, int64_t m, const blast_bcsc_t* w, int act, const void* pre,
+                       void* y, void* stream);
 /* Y[m, w.rows] = X[m, w.cols] @ W^T           kernels.py:143 bspmm_rt */
 int blast_bspmm_rt(const void* x, int64_t m, const blast_bcsc_t* w, void* y, void* stream);
 /* Elementwise activation (kernels.py:50-62 apply_nonlinearity); in-place allowed. */

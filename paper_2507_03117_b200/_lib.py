@@ -54,7 +54,8 @@ _PROTOS = {
     "blast_tf32_prepare": (C.c_int, [vp, i64, i32, vp, vp, vp, vp, vp]),
     "blast_bspmm": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.c_int, vp, vp]),
     "blast_bspmm_rt": (C.c_int, [vp, i64, C.POINTER(BcscDesc), vp, vp]),
-    "blast_bspmm_bias": (C.c_int, [vp, i64, C.POINTER(BcscDesc), vp, C.c_int, vp, vp]),
+    "blast_bspmm_ex": (C.c_int, [vp, i64, C.POINTER(BcscDesc), vp, C.c_int, vp, vp, vp]),
+    "blast_bspmm_rt_act": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.c_int, vp, vp, vp]),
     "blast_activation": (C.c_int, [vp, vp, i64, C.c_int, C.c_int, vp]),
     "blast_mlp_forward": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                     C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp, vp, vp,

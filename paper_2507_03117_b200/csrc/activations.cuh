@@ -46,6 +46,27 @@ __device__ __forceinline__ float apply_act(float x, int act) {
     default: return x;
   }
 }
+// d act / d x at x (backward of bspmm_fused for model layers): relu' = [x > 0],
+// silu' = s (1 + x (1 - s)) (kernels.py:37-39), gelu' of the tanh form.
+__device__ __forceinline__ float apply_act_grad(float x, int act) {
+  switch (act) {
+    case ACT_RELU: return x > 0.0f ? 1.0f : 0.0f;
+    case ACT_SILU: {
+      const float s = act_sigmoid(x);
+      return __fmul_rn(s, __fadd_rn(1.0f, __fmul_rn(x, __fsub_rn(1.0f, s))));
+    }
+    case ACT_GELU: {
+      const float c = 0.7978845834732056f, a = 0.044714998453855515f;
+      const float x2 = __fmul_rn(x, x);
+      const float t = tanhf(__fmul_rn(c, __fadd_rn(x, __fmul_rn(__fmul_rn(a, x2), x))));
+      const float du = __fmul_rn(c, __fadd_rn(1.0f, __fmul_rn(3.0f * a, x2)));
+      return __fadd_rn(__fmul_rn(0.5f, __fadd_rn(1.0f, t)),
+                       __fmul_rn(__fmul_rn(__fmul_rn(0.5f, x), __fsub_rn(1.0f, __fmul_rn(t, t))),
+                                 du));
+    }
+    default: return 1.0f;
+  }
+}
 // g = (a * sigmoid(a)) * b
 __device__ __forceinline__ float gated_fwd(float a, float b) {
   return __fmul_rn(__fmul_rn(a, act_sigmoid(a)), b);

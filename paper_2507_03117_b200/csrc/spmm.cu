@@ -406,11 +406,11 @@ extern "C" int blast_set_pair_engine(int enabled) {
 
 extern "C" int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
                            void* stream) {
-  return blast_bspmm_bias(x, m, w, nullptr, act, y, stream);
+  return blast_bspmm_ex(x, m, w, nullptr, act, y, nullptr, stream);
 }
 
-extern "C" int blast_bspmm_bias(const void* x, int64_t m, const blast_bcsc_t* w,
-                                const float* bias, int act, void* y, void* stream) {
+extern "C" int blast_bspmm_ex(const void* x, int64_t m, const blast_bcsc_t* w, const float* bias,
+                              int act, void* y, void* pre, void* stream) {
   if (!check_w(w)) return BLAST_EINVAL;
   if (act < 0 || act > 3) {
     set_error("unknown nonlinearity code %d", act);
@@ -434,7 +434,39 @@ extern "C" int blast_bspmm_bias(const void* x, int64_t m, const blast_bcsc_t* w,
   c.steps = w->fwd_steps;
   c.flags = w->fwd_flags;
   c.out0 = y;
+  c.out1 = pre;
   c.ld_out = w->cols;
+  return run_engine(c, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int blast_bspmm_rt_act(const void* x, int64_t m, const blast_bcsc_t* w, int act,
+                                  const void* pre, void* y, void* stream) {
+  if (!check_w(w)) return BLAST_EINVAL;
+  if (act < 0 || act > 3 || !pre) {
+    set_error("bspmm_rt_act: activation code %d / pre-activation required", act);
+    return BLAST_EINVAL;
+  }
+  EngineCall c;
+  c.dtype = w->dtype;
+  c.block = w->block;
+  c.transposed = true;
+  c.epi = EPI_GATED_BWD;  // single-input form: y = (x W^T) * act'(pre)
+  c.act = act;
+  c.m = m;
+  c.a_cols = w->cols;
+  c.a0 = x;
+  c.w0 = w->values;
+  c.w0_hi = w->tf32_rt_hi;
+  c.w0_lo = w->tf32_rt_lo;
+  c.nnzb0 = w->nnzb;
+  c.n_lines = cdiv(w->rows, w->block);
+  c.n_valid = w->rows;
+  c.step_ptr = w->rt_step_ptr;
+  c.steps = w->rt_steps;
+  c.flags = w->rt_flags;
+  c.out0 = y;
+  c.in0 = pre;
+  c.ld_out = w->rows;
   return run_engine(c, static_cast<cudaStream_t>(stream));
 }
 

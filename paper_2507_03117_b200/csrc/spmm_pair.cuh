@@ -356,45 +356,8 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
 #pragma unroll
             for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
           }
-          if constexpr (EPI == EPI_STORE) {
-            add_bias16(v0, p.bias, col, valid);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
-            if (row_ok && valid > 0) {
-              if (p.accumulate) {
-                float prev[16];
-                load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.out0) + off, prev, valid, vec_ok);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v0[i] = __fadd_rn(prev[i], v0[i]);
-              }
-              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
-            }
-          } else if constexpr (EPI == EPI_GATED_FWD) {
-            float v1[16];
-            tmem_ld16(tbase + B + c * 16, v1);
-            if (!(flags & 2)) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v1[i] = 0.0f;
-            }
-            if (row_ok && valid > 0) {
-              if (p.out1) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
-              if (p.out2) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out2) + off, v1, valid, vec_ok);
-              float g[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) g[i] = gated_fwd(v0[i], v1[i]);
-              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
-            }
-          } else {
-            if (row_ok && valid > 0) {
-              float a[16], b[16], da[16], db[16];
-              load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, a, valid, vec_ok);
-              load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in1) + off, b, valid, vec_ok);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
-              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, da, valid, vec_ok);
-              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, db, valid, vec_ok);
-            }
-          }
+          epilogue_chunk<EPI, OutT>(p, v0, tbase + B + c * 16, flags, row_ok, col, valid, off,
+                                    vec_ok);
         }
         tc_fence_before();
         __syncwarp();

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const SpmmParams p, cons
     if (s.epi == EPI_STORE) {
       float v = acc[0];
       if (p.bias) v = __fadd_rn(v, p.bias[col]);
+      if (p.out1) static_cast<T*>(p.out1)[off] = from_f32<T>(v);
       v = apply_act(v, p.act);
       if (p.accumulate) v = __fadd_rn(to_f32<T>(static_cast<T*>(p.out0)[off]), v);
       static_cast<T*>(p.out0)[off] = from_f32<T>(v);
@@ -79,6 +80,9 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const SpmmParams p, cons
       if (p.out1) static_cast<T*>(p.out1)[off] = from_f32<T>(acc[0]);
       if (p.out2) static_cast<T*>(p.out2)[off] = from_f32<T>(acc[1]);
       static_cast<T*>(p.out0)[off] = from_f32<T>(gated_fwd(acc[0], acc[1]));
+    } else if (!p.in1) {
+      const float pre = to_f32<T>(static_cast<const T*>(p.in0)[off]);
+      static_cast<T*>(p.out0)[off] = from_f32<T>(__fmul_rn(acc[0], apply_act_grad(pre, p.act)));
     } else {
       const float a = to_f32<T>(static_cast<const T*>(p.in0)[off]);
       const float b = to_f32<T>(static_cast<const T*>(p.in1)[off]);

@@ -217,6 +217,69 @@ __device__ __forceinline__ void load_chunk16(const T* src, float (&v)[16], int v
     for (int i = 0; i < 16; ++i) v[i] = (i < valid) ? to_f32<T>(src[i]) : 0.0f;
   }
 }
+// One 16-column chunk of an output tile, shared by the single-CTA and CTA-pair
+// engines. v0 holds the first accumulator (already zeroed if it received no
+// MMA); acc1_addr is the TMEM address of the second accumulator's chunk (gated
+// forward). Must be called by the whole warp (tcgen05.ld is warp-collective).
+//   EPI_STORE      out0 = act(v0 + bias) [+= out0]; out1 (optional) = v0 + bias
+//   EPI_GATED_FWD  out0 = silu(a) * b; out1 = a, out2 = b (optional)   (mlp.py:111-113)
+//   EPI_GATED_BWD  in1 set: out0 = dA, out1 = dB from dG = v0          (mlp.py:133-139)
+//                  in1 NULL: out0 = v0 * act'(in0)  (backward of a fused activation)
+template <int EPI, typename OutT>
+__device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[16],
+                                               uint32_t acc1_addr, int flags, bool row_ok,
+                                               int col, int valid, int64_t off, bool vec_ok) {
+  const bool live = row_ok && valid > 0;
+  if constexpr (EPI == EPI_STORE) {
+    add_bias16(v0, p.bias, col, valid);
+    if (p.out1 && live)
+      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
+    if (live) {
+      if (p.accumulate) {
+        float prev[16];
+        load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.out0) + off, prev, valid, vec_ok);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v0[i] = __fadd_rn(prev[i], v0[i]);
+      }
+      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
+    }
+  } else if constexpr (EPI == EPI_GATED_FWD) {
+    float v1[16];
+    tmem_ld16(acc1_addr, v1);
+    if (!(flags & 2)) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v1[i] = 0.0f;
+    }
+    if (live) {
+      if (p.out1) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
+      if (p.out2) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out2) + off, v1, valid, vec_ok);
+      float g[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) g[i] = gated_fwd(v0[i], v1[i]);
+      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
+    }
+  } else {
+    if (!live) return;
+    if (p.in1) {
+      float a[16], b[16], da[16], db[16];
+      load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, a, valid, vec_ok);
+      load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in1) + off, b, valid, vec_ok);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
+      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, da, valid, vec_ok);
+      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, db, valid, vec_ok);
+    } else {
+      float pre[16];
+      load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, pre, valid, vec_ok);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v0[i] = __fmul_rn(v0[i], apply_act_grad(pre[i], p.act));
+      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
+    }
+  }
+}
+
 // 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (two warps per TMEM lane quarter, splitting the 16-column chunks).
 constexpr int kTcThreads = 384;
@@ -454,45 +517,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
 #pragma unroll
           for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
         }
-        if constexpr (EPI == EPI_STORE) {
-          add_bias16(v0, p.bias, col, valid);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
-          if (row_ok && valid > 0) {
-            if (p.accumulate) {
-              float prev[16];
-              load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.out0) + off, prev, valid, vec_ok);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v0[i] = __fadd_rn(prev[i], v0[i]);
-            }
-            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
-          }
-        } else if constexpr (EPI == EPI_GATED_FWD) {
-          float v1[16];
-          tmem_ld16(tbase + B + c * 16, v1);
-          if (!(flags & 2)) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v1[i] = 0.0f;
-          }
-          if (row_ok && valid > 0) {
-            if (p.out1) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
-            if (p.out2) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out2) + off, v1, valid, vec_ok);
-            float g[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) g[i] = gated_fwd(v0[i], v1[i]);
-            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
-          }
-        } else {  // EPI_GATED_BWD: v0 = dG
-          if (row_ok && valid > 0) {
-            float a[16], b[16], da[16], db[16];
-            load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, a, valid, vec_ok);
-            load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in1) + off, b, valid, vec_ok);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
-            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, da, valid, vec_ok);
-            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, db, valid, vec_ok);
-          }
-        }
+        epilogue_chunk<EPI, OutT>(p, v0, tbase + B + c * 16, flags, row_ok, col, valid, off,
+                                  vec_ok);
       }
       tc_fence_before();
       __syncwarp();

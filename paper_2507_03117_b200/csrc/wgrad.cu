@@ -10,6 +10,7 @@
 // panel), one block for b = 128. Both operands are MN-major (A^T and D are read
 // straight from the row-major activations), K = tokens in 64-token stages.
 #include "host.hpp"
+#include "scan.cuh"
 #include "spmm_tc.cuh"
 
 namespace blast {
@@ -23,6 +24,14 @@ struct WgradParams {
   const int32_t* row_of;  // slot -> block row (row_idx); nullptr in dense mode (slot = row)
   float* out_blocks;   // [nnzb, b, b] (selected mode)
   float* dense_out;    // [rows, cols]  (dense mode)
+  // split-K over tokens when there are too few blocks to fill the GPU: work item
+  // (item, split) covers token stages [split*kps, (split+1)*kps) and writes an fp32
+  // partial block; wgrad_reduce_kernel sums the partials in split order.
+  int32_t n_split;
+  int32_t kps;
+  float* partial;      // [n_split][n_slots][b][b]
+  int64_t n_slots;     // selected blocks, or gr*gc in dense mode (slot = c*gr + r)
+  int64_t gr;
 };
 
 template <int B>
@@ -53,7 +62,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int ksteps = (p.m + C::TK - 1) / C::TK;
-  const int n_items = static_cast<int>(*p.n_items_dev);
+  const int n_work = static_cast<int>(*p.n_items_dev) * p.n_split;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapA);
@@ -79,16 +88,26 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 
   auto block_row = [&](int slot) -> int { return p.row_of ? p.row_of[slot] : slot; };
 
+  // token-stage range of a work item (split-K)
+  auto krange = [&](int w, int& k0, int& k1) {
+    const int sp = w % p.n_split;
+    k0 = sp * p.kps;
+    k1 = min(ksteps, k0 + p.kps);
+  };
+
   if (warp == 0) {
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int4 it = p.items[item];
-        const int c = it.x;
-        const int r0 = block_row(it.y);
-        const int r1 = it.z >= 0 ? block_row(it.z) : r0;
-        for (int ks = 0; ks < ksteps; ++ks) {
-          mbar_wait(&empty[stage], phase ^ 1);
+    // whole warp walks the work list; one elected lane issues the copies
+    uint32_t stage = 0, phase = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int4 it = __ldg(&p.items[w / p.n_split]);
+      const int c = it.x;
+      const int r0 = block_row(it.y);
+      const int r1 = it.z >= 0 ? block_row(it.z) : r0;
+      int k0, k1;
+      krange(w, k0, k1);
+      for (int ks = k0; ks < k1; ++ks) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
           mbar_expect_tx(&full[stage], C::STAGE);
           uint8_t* sa = smem + stage * C::STAGE;
           uint8_t* sb = sa + C::A_TILE;
@@ -103,43 +122,49 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 #pragma unroll
           for (int a = 0; a < C::NB_ATOM; ++a)
             tma_load_2d(sb + a * C::ATOM, &mapD, &full[stage], c * B + a * 64, tok);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0, it = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const uint32_t as = it & 1, use = it >> 1;
-        mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+    // MN-major operands: K slice kk = 16 token rows (2 KB); LBO = 64-wide atom stride
+    const uint64_t a_desc0 = make_sdesc(smem_u32(smem), C::ATOM, 1024, 2);
+    const uint64_t b_desc0 = make_sdesc(smem_u32(smem) + C::A_TILE, C::ATOM, 1024, 2);
+    uint32_t stage = 0, phase = 0, it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      const uint32_t as = it & 1, use = it >> 1;
+      int k0, k1;
+      krange(w, k0, k1);
+      mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + as * B;
+      for (int ks = k0; ks < k1; ++ks) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d = tmem_base + as * B;
-        for (int ks = 0; ks < ksteps; ++ks) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::STAGE);
-          const uint32_t sb = sa + C::A_TILE;
+        if (elect_one()) {
+          const uint32_t soff = (stage * C::STAGE) >> 4;
 #pragma unroll
-          for (int kk = 0; kk < C::TK / 16; ++kk) {
-            // MN-major: K slice kk = 16 token rows (2048 B); LBO = stride between 64-wide atoms
-            const uint64_t ad = make_sdesc(sa + kk * 16 * 128, C::ATOM, 1024, 2);
-            const uint64_t bd = make_sdesc(sb + kk * 16 * 128, C::ATOM, 1024, 2);
-            mma_f16(d, ad, bd, C::IDESC, (ks > 0 || kk > 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < C::TK / 16; ++kk)
+            mma_f16(d, a_desc0 + soff + ((kk * 16 * 128) >> 4),
+                    b_desc0 + soff + ((kk * 16 * 128) >> 4), C::IDESC,
+                    (ks > k0 || kk > 0) ? 1u : 0u);
           mma_commit(&empty[stage]);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tmem_full[as]);
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) mma_commit(&tmem_full[as]);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;
     uint32_t it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int4 itm = p.items[item];
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      const int4 itm = __ldg(&p.items[w / p.n_split]);
+      const int sp = w % p.n_split;
+      int k0, k1;
+      krange(w, k0, k1);
       const uint32_t as = it & 1, use = it >> 1;
       mbar_wait(&tmem_full[as], use & 1);
       tc_fence_after();
@@ -158,12 +183,16 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       for (int ch = 0; ch < B / 16; ++ch) {
         float v[16];
         tmem_ld16(tbase + ch * 16, v);
-        if (ksteps == 0) {
+        if (k1 <= k0) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.0f;
         }
         if (slot < 0) continue;
-        if (p.dense_out) {
+        if (p.n_split > 1) {  // fp32 partial, reduced in split order afterwards
+          const int64_t flat = p.dense_out ? static_cast<int64_t>(itm.x) * p.gr + r : slot;
+          float* dst = p.partial + ((sp * p.n_slots + flat) * B + li) * B + ch * 16;
+          store_chunk16<float>(dst, v, 16, true);
+        } else if (p.dense_out) {
           const int64_t row = static_cast<int64_t>(r) * B + li;
           const int64_t col = static_cast<int64_t>(itm.x) * B + ch * 16;
           if (row < p.rows) {
@@ -267,9 +296,23 @@ __global__ void wgrad_item_count_kernel(const int64_t* col_ptr, int64_t gr, int6
   const int64_t n = col_ptr ? col_ptr[c + 1] - col_ptr[c] : gr;
   item_ptr[c + 1] = (n + per_item - 1) / per_item;
 }
-__global__ void scan_inplace_i64(int64_t* ptr, int64_t n) {  // tiny, single thread
-  if (threadIdx.x == 0 && blockIdx.x == 0)
-    for (int64_t i = 1; i <= n; ++i) ptr[i] += ptr[i - 1];
+// split-K reduction: out = sum_{sp=0..n_split-1} partial[sp] (fixed order -> deterministic)
+__global__ void wgrad_reduce_kernel(const WgradParams p, int b) {
+  const int64_t bb = static_cast<int64_t>(b) * b;
+  const int64_t total = p.n_slots * bb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = p.partial[i];
+    for (int sp = 1; sp < p.n_split; ++sp) acc = __fadd_rn(acc, p.partial[sp * total + i]);
+    const int64_t slot = i / bb, e = i - slot * bb;
+    if (p.dense_out) {
+      const int64_t c = slot / p.gr, r = slot - c * p.gr;
+      const int64_t row = r * b + e / b, col = c * b + e % b;
+      if (row < p.rows && col < p.cols) p.dense_out[row * p.cols + col] = acc;
+    } else {
+      p.out_blocks[i] = acc;
+    }
+  }
 }
 // simt items: one per (slot, 64x64 sub-tile)
 __global__ void wgrad_simt_items_kernel(const int64_t* col_ptr, int64_t gr, int64_t gc, int tiles,
@@ -302,9 +345,17 @@ static int launch_wgrad_tc(const void* a, const void* d, const WgradParams& p, c
   if (!encode_map_2d(&ma, a, BLAST_BF16, p.rows, p.m, p.rows * 2, 64, C::TK, 128)) return BLAST_EINVAL;
   if (!encode_map_2d(&md, d, BLAST_BF16, p.cols, p.m, p.cols * 2, 64, C::TK, 128)) return BLAST_EINVAL;
   if (p.n_items <= 0) return BLAST_OK;
-  const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
+  const int64_t work = static_cast<int64_t>(p.n_items) * p.n_split;
+  const int grid = static_cast<int>(work < num_sms() ? work : num_sms());
   kern<<<grid, 256, C::SMEM_BYTES, st>>>(ma, md, p);
-  return check_launch("wgrad_tc");
+  int rc = check_launch("wgrad_tc");
+  if (rc == BLAST_OK && p.n_split > 1) {
+    const int64_t total = p.n_slots * B * B;
+    const int rg = static_cast<int>(std::min<int64_t>(cdiv(total, 256), (int64_t)num_sms() * 8));
+    wgrad_reduce_kernel<<<rg, 256, 0, st>>>(p, B);
+    rc = check_launch("wgrad_reduce");
+  }
+  return rc;
 }
 
 }  // namespace blast
@@ -352,11 +403,27 @@ extern "C" int blast_block_wgrad(const void* a, const void* d, int64_t m, int64_
     if (!si.alloc(sizeof(int4) * nsel, st)) return cuda_status(cudaGetLastError(), "wgrad");
     const int thr = 256, blk = static_cast<int>(cdiv(gc, thr));
     wgrad_item_count_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>());
-    scan_inplace_i64<<<1, 32, 0, st>>>(sp.as<int64_t>(), gc);
+    offsets_scan_kernel<int64_t><<<1, 1024, 0, st>>>(sp.as<int64_t>(), gc);
     wgrad_items_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>(), si.as<int4>());
     p.n_items = static_cast<int32_t>((nsel + gc + per_item - 1) / per_item);
     p.n_items_dev = sp.as<int64_t>() + gc;
     p.items = si.as<int4>();
+    // split-K when the blocks cannot fill the GPU (e.g. GPT-2 small at 90%: ~60 blocks)
+    const int ksteps = static_cast<int>(cdiv(m, 64));
+    int n_split = 1;
+    if (p.n_items < 2 * num_sms() && ksteps >= 8)
+      n_split = std::min<int>({static_cast<int>(cdiv(2 * num_sms(), p.n_items)), ksteps / 4, 32});
+    n_split = std::max(1, n_split);
+    p.kps = static_cast<int32_t>(cdiv(ksteps, n_split));
+    p.n_split = static_cast<int32_t>(cdiv(ksteps, p.kps));
+    p.n_slots = nsel;
+    p.gr = gr;
+    Scratch spart;
+    if (p.n_split > 1) {
+      if (!spart.alloc(sizeof(float) * p.n_split * nsel * block * block, st))
+        return cuda_status(cudaGetLastError(), "wgrad partials");
+      p.partial = spart.as<float>();
+    }
     return block == 64 ? launch_wgrad_tc<64>(a, d, p, st) : launch_wgrad_tc<128>(a, d, p, st);
   }
   const int tiles = static_cast<int>(cdiv(block, 64));

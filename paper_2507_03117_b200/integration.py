@@ -21,7 +21,7 @@ from torch import nn
 
 from . import bcsc
 from .bcsc import BlockMask, BlockSparseMatrix
-from .kernels import bspmm, bspmm_fused, bspmm_rt
+from .kernels import bspmm_act_save, bspmm_fused, bspmm_rt, bspmm_rt_act_grad
 from .mlp import SparseMlp, _wgrad, mlp_backward, mlp_forward
 from .pruner import block_norms, prune_s
 
@@ -86,8 +86,7 @@ class SparseGatedMLP(nn.Module):
 class _GeluFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x2d, w1: BlockSparseMatrix, b1, w2: BlockSparseMatrix, b2, v1, v2):
-        pre = bspmm_fused(x2d, w1, "none", bias=b1)
-        hid = _gelu_tanh(pre.float()).to(pre.dtype)
+        hid, pre = bspmm_act_save(x2d, w1, "gelu", bias=b1)   # bias + GELU in the epilogue
         y = bspmm_fused(hid, w2, "none", bias=b2)
         ctx.save_for_backward(x2d, pre, hid)
         ctx.w = (w1, w2)
@@ -98,8 +97,7 @@ class _GeluFn(torch.autograd.Function):
         x2d, pre, hid = ctx.saved_tensors
         w1, w2 = ctx.w
         dy = dy.contiguous().to(hid.dtype)
-        dhid = bspmm_rt(dy, w2)
-        dpre = (dhid.float() * _gelu_tanh_grad(pre.float())).to(hid.dtype).contiguous()
+        dpre = bspmm_rt_act_grad(dy, w2, "gelu", pre)          # (dY W2^T) * gelu'(pre), fused
         dx = bspmm_rt(dpre, w1)
         dv2 = _wgrad(hid, dy, w2.rows, w2.cols, w2, full=False)
         dv1 = _wgrad(x2d, dpre, w1.rows, w1.cols, w1, full=False)

@@ -121,10 +121,40 @@ def _product(x, w: BlockSparseMatrix, act: int, transposed: bool, bias=None):
         if transposed:
             rc = lib.blast_bspmm_rt(xt.data_ptr(), m, C.byref(d), y.data_ptr(), L.stream())
         else:
-            rc = lib.blast_bspmm_bias(xt.data_ptr(), m, C.byref(d), L.ptr(bias_t), act,
-                                      y.data_ptr(), L.stream())
+            rc = lib.blast_bspmm_ex(xt.data_ptr(), m, C.byref(d), L.ptr(bias_t), act,
+                                    y.data_ptr(), None, L.stream())
         L.check(rc, "bspmm_rt" if transposed else "bspmm")
     return A.like_input(y, host)
+
+
+def bspmm_act_save(x: torch.Tensor, w: BlockSparseMatrix, f: str, bias=None):
+    """(f(X @ W + bias), X @ W + bias) in one launch: the activation and the
+    pre-activation the backward needs (device tensors)."""
+    code = _act_code(f)
+    xt = _check_lhs(x, w, w.rows)
+    m = xt.shape[0]
+    y = torch.empty(m, w.cols, dtype=w.values.dtype, device=A.DEVICE)
+    pre = torch.empty_like(y)
+    bias_t = None if bias is None else A.to_device(bias, torch.float32).reshape(-1)
+    if m:
+        L.check(L.load().blast_bspmm_ex(xt.data_ptr(), m, C.byref(w.desc()), L.ptr(bias_t), code,
+                                        y.data_ptr(), pre.data_ptr(), L.stream()), "bspmm_ex")
+    return y, pre
+
+
+def bspmm_rt_act_grad(dy: torch.Tensor, w: BlockSparseMatrix, f: str, pre: torch.Tensor):
+    """(dY @ W^T) * f'(pre): the gradient through W and the activation that produced
+    its input, fused in one launch (device tensors)."""
+    code = _act_code(f)
+    dyt = _check_lhs(dy, w, w.cols)
+    m = dyt.shape[0]
+    out = torch.empty(m, w.rows, dtype=w.values.dtype, device=A.DEVICE)
+    if m:
+        pre_t = pre.to(w.values.dtype).contiguous()
+        L.check(L.load().blast_bspmm_rt_act(dyt.data_ptr(), m, C.byref(w.desc()), code,
+                                            pre_t.data_ptr(), out.data_ptr(), L.stream()),
+                "bspmm_rt_act")
+    return out
 
 
 def bspmm(x, w: BlockSparseMatrix, blk_m: int | None = None):
