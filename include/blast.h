@@ -161,6 +161,12 @@ int blast_block_norms(const void* x, const void* x2, int64_t rows, int64_t cols,
  * keep: uint8[gr][gc]. Scratch is internal. */
 int blast_topk_mask(const double* norms, int64_t grid_rows, int64_t grid_cols, int64_t k,
                     uint8_t* keep, void* stream);
+/* Two independent selections with the same k (weight and gradient norms of
+ * generate_masks, pruner.py:142-143) in one launch when the grid fits one CTA's
+ * shared memory (<= 24576 blocks), else two launches of blast_topk_mask. */
+int blast_topk_mask2(const double* norms_a, const double* norms_b, int64_t grid_rows,
+                     int64_t grid_cols, int64_t k, uint8_t* keep_a, uint8_t* keep_b,
+                     void* stream);
 /* regrown = grad_sel & ~kept; counts[0] = |kept|, counts[1] = |regrown| (device int64[2]).
  * (pruner.py:142-156) */
 int blast_mask_difference(const uint8_t* kept, const uint8_t* grad_sel, int64_t n,

@@ -69,6 +69,7 @@ _PROTOS = {
                                     vp]),
     "blast_block_norms": (C.c_int, [vp, vp, i64, i64, i32, C.c_int, vp, vp, vp]),
     "blast_topk_mask": (C.c_int, [vp, i64, i64, i64, vp, vp]),
+    "blast_topk_mask2": (C.c_int, [vp, vp, i64, i64, i64, vp, vp, vp]),
     "blast_mask_difference": (C.c_int, [vp, vp, i64, vp, vp, vp]),
     "blast_repack_index": (C.c_int, [vp, vp, vp, i64, i64, i32, C.c_int, vp, vp, vp]),
     "blast_repack_rows": (C.c_int, [vp, vp, i64, i64, vp, vp]),

@@ -215,6 +215,92 @@ __global__ void __launch_bounds__(1024) topk_kernel(const double* __restrict__ n
   }
 }
 
+// Single-CTA top-k for grids whose keys fit in shared memory (the common case:
+// the Llama-3-8B grid is 14,336 cells, 70B 57,344 at b=64 goes to topk_kernel).
+// Same composite key and selection as topk_kernel, radix passes of 8 bits over
+// the 64-bit norm key, then over the column-major index among exact ties. No
+// grid barriers and no scratch; blockIdx.x selects one of two independent grids
+// (the weight and gradient selections of generate_masks run in one launch).
+constexpr int kTopkSmemMax = 24576;
+
+__global__ void __launch_bounds__(1024) topk_smem_kernel(const double* __restrict__ norms0,
+                                                         uint8_t* __restrict__ keep0,
+                                                         const double* __restrict__ norms1,
+                                                         uint8_t* __restrict__ keep1, int64_t gr,
+                                                         int64_t gc, int64_t k) {
+  extern __shared__ uint64_t keys[];
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned int sel_bucket, sel_below;
+  const double* norms = blockIdx.x == 0 ? norms0 : norms1;
+  uint8_t* keep = blockIdx.x == 0 ? keep0 : keep1;
+  const int n = static_cast<int>(gr * gc);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = norm_key(norms[i]);
+  uint64_t pre1 = 0;
+  uint32_t pre2 = 0;
+  unsigned int krem = static_cast<unsigned int>(k);
+  // 8 passes over K1, then 2 over lin (n <= 24576 < 2^16)
+  for (int pass = 0; pass < 10; ++pass) {
+    const bool on_lin = pass >= 8;
+    const int sh = on_lin ? (9 - pass) * 8 : (7 - pass) * 8;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      const uint64_t k1 = keys[idx];
+      unsigned int digit;
+      if (!on_lin) {
+        const int top = sh + 8;
+        if (top < 64 && (k1 >> top) != (pre1 >> top)) continue;
+        digit = static_cast<unsigned int>((k1 >> sh) & 0xFF);
+      } else {
+        if (k1 != pre1) continue;
+        const int r = idx / static_cast<int>(gc), c = idx - r * static_cast<int>(gc);
+        const uint32_t lin = static_cast<uint32_t>(c * gr + r);
+        const int top = sh + 8;
+        if (top < 16 && (lin >> top) != (pre2 >> top)) continue;
+        digit = (lin >> sh) & 0xFF;
+      }
+      atomicAdd(&hist[digit], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one warp scans the 256 bins, 8 per lane
+      unsigned int local[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        local[j] = hist[threadIdx.x * 8 + j];
+        sum += local[j];
+      }
+      unsigned int incl = sum;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (threadIdx.x >= o) incl += t;
+      }
+      unsigned int below = incl - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (below < krem && krem <= below + local[j]) {
+          sel_bucket = threadIdx.x * 8 + j;
+          sel_below = below;
+        }
+        below += local[j];
+      }
+    }
+    __syncthreads();
+    krem -= sel_below;
+    if (!on_lin) pre1 |= static_cast<uint64_t>(sel_bucket) << sh;
+    else pre2 |= static_cast<uint32_t>(sel_bucket) << sh;
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const uint64_t k1 = keys[idx];
+    bool kp = k1 < pre1;
+    if (k1 == pre1) {
+      const int r = idx / static_cast<int>(gc), c = idx - r * static_cast<int>(gc);
+      kp = static_cast<uint32_t>(c * gr + r) <= pre2;
+    }
+    keep[idx] = kp ? 1 : 0;
+  }
+}
+
 __global__ void fill_u8_kernel(uint8_t* p, int64_t n, uint8_t v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -384,6 +470,46 @@ __global__ void apply_mask_gather_kernel(const T* __restrict__ x, int64_t rows, 
   }
 }
 
+// Vectorised form for float32 masters with cols % 4 == 0 and b % 4 == 0: four
+// consecutive columns share a block, so one mask / kmap lookup and one 16-byte
+// load serve four elements. Same arithmetic as apply_mask_gather_kernel.
+template <typename V>
+__global__ void __launch_bounds__(256) apply_mask_gather_vec4_kernel(
+    const float4* __restrict__ x, int64_t rows, int64_t cols4, int b, int64_t gc,
+    const uint8_t* __restrict__ kept, const uint8_t* __restrict__ regrown, int mode,
+    const int32_t* __restrict__ kmap, float4* masked, V* values) {
+  const int64_t n4 = rows * cols4;
+  const int64_t bb = static_cast<int64_t>(b) * b;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cols4, col = (i - row * cols4) * 4;
+    const int64_t r = row / b, c = col / b;
+    const int64_t cell = r * gc + c;
+    const float4 v = __ldg(&x[i]);
+    float4 m = v;
+    if (mode != 0) {
+      const bool surv = kept[cell] != 0 || (mode == 2 && regrown[cell] != 0);
+      const float s = surv ? 1.0f : 0.0f;
+      m = make_float4(__fmul_rn(v.x, s), __fmul_rn(v.y, s), __fmul_rn(v.z, s), __fmul_rn(v.w, s));
+    }
+    if (masked) masked[i] = m;
+    const int32_t k = __ldg(&kmap[cell]);
+    if (k >= 0) {
+      const int64_t off = k * bb + (row - r * b) * b + (col - c * b);
+      if constexpr (sizeof(V) == 4) {
+        *reinterpret_cast<float4*>(values + off) = mode == 0 ? v : m;
+      } else {
+        const float4 s = mode == 0 ? v : m;
+        __nv_bfloat162 lo = __floats2bfloat162_rn(s.x, s.y), hi = __floats2bfloat162_rn(s.z, s.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(values + off) = pk;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ optimizer glue
 __global__ void sgd_kernel(float* w, const float* g, int64_t n, float lr) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -415,6 +541,21 @@ __global__ void sumsq_final_kernel(const double* partial, int n, double* out) {
     for (int i = 0; i < n; ++i) s += partial[i];
     out[0] += s;
   }
+}
+
+static int topk_smem_launch(const double* n0, uint8_t* k0, const double* n1, uint8_t* k1,
+                            int64_t gr, int64_t gc, int64_t k, cudaStream_t st) {
+  static bool configured = false;
+  const int smem = kTopkSmemMax * 8;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(topk_smem_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_status(e, "topk smem attribute");
+    configured = true;
+  }
+  const int n = static_cast<int>(gr * gc);
+  topk_smem_kernel<<<n1 ? 2 : 1, 1024, n * 8, st>>>(n0, k0, n1, k1, gr, gc, k);
+  return check_launch("topk_smem");
 }
 
 static int grid_for(int64_t n, int threads, int per_sm = 16) {
@@ -479,6 +620,8 @@ extern "C" int blast_topk_mask(const double* norms, int64_t grid_rows, int64_t g
     fill_u8_kernel<<<grid_for(n, 256), 256, 0, st>>>(keep, n, k <= 0 ? 0 : 1);
     return check_launch("topk fill");
   }
+  if (n <= kTopkSmemMax) return topk_smem_launch(norms, keep, nullptr, nullptr, grid_rows,
+                                                 grid_cols, k, st);
   Scratch s;
   if (!s.alloc(sizeof(TopkState), st)) return cuda_status(cudaGetLastError(), "topk scratch");
   cudaMemsetAsync(s.ptr, 0, sizeof(TopkState), st);
@@ -492,6 +635,18 @@ extern "C" int blast_topk_mask(const double* norms, int64_t grid_rows, int64_t g
   cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(topk_kernel), dim3(grid),
                                               dim3(1024), args, 0, st);
   return cuda_status(e, "topk launch");
+}
+
+extern "C" int blast_topk_mask2(const double* norms_a, const double* norms_b, int64_t grid_rows,
+                                int64_t grid_cols, int64_t k, uint8_t* keep_a, uint8_t* keep_b,
+                                void* stream) {
+  const int64_t n = grid_rows * grid_cols;
+  if (n > 0 && k > 0 && k < n && n <= kTopkSmemMax)
+    return topk_smem_launch(norms_a, keep_a, norms_b, keep_b, grid_rows, grid_cols, k,
+                            static_cast<cudaStream_t>(stream));
+  const int r = blast_topk_mask(norms_a, grid_rows, grid_cols, k, keep_a, stream);
+  if (r) return r;
+  return blast_topk_mask(norms_b, grid_rows, grid_cols, k, keep_b, stream);
 }
 
 extern "C" int blast_mask_difference(const uint8_t* kept, const uint8_t* grad_sel, int64_t n,
@@ -557,6 +712,20 @@ extern "C" int blast_apply_mask_gather(const void* dense, int64_t rows, int64_t 
     return BLAST_EINVAL;
   }
   const int grid = grid_for(n, 256, 32);
+  const bool vec = dtype == BLAST_F32 && cols % 4 == 0 && block % 4 == 0 && aligned16(dense) &&
+                   (!masked_out || aligned16(masked_out)) && aligned16(values);
+  if (vec) {
+    const int g4 = grid_for(n / 4, 256, 32);
+    if (values_dtype == BLAST_F32)
+      apply_mask_gather_vec4_kernel<float><<<g4, 256, 0, st>>>(
+          static_cast<const float4*>(dense), rows, cols / 4, block, gc, kept, regrown, mode, kmap,
+          static_cast<float4*>(masked_out), static_cast<float*>(values));
+    else
+      apply_mask_gather_vec4_kernel<__nv_bfloat16><<<g4, 256, 0, st>>>(
+          static_cast<const float4*>(dense), rows, cols / 4, block, gc, kept, regrown, mode, kmap,
+          static_cast<float4*>(masked_out), static_cast<__nv_bfloat16*>(values));
+    return check_launch("apply_mask_gather_vec4");
+  }
 #define BLAST_GATHER(T, V)                                                                    \
   apply_mask_gather_kernel<T, V><<<grid, 256, 0, st>>>(                                       \
       static_cast<const T*>(dense), rows, cols, block, gc, kept, regrown, mode, kmap,         \

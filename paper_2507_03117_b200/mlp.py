@@ -110,7 +110,8 @@ class SparseMlp:
     def plan(self) -> L.MlpPlanDesc:
         """Merged gate/up step lists (csrc/plan.cu), rebuilt when a cache is replaced."""
         g, u = self.gate.cache, self.up.cache
-        key = (id(g), id(u))
+        # keyed on the index maps: caches re-gathered for an unchanged mask share them
+        key = (id(g._kmap()), id(u._kmap()))
         if self._plan_cache.get("key") != key:
             gr, gc = g.grid_rows, g.grid_cols
             gu = bcsc.build_plan(g._kmap(), u._kmap(), gr, gc, 0)

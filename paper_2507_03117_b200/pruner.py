@@ -167,8 +167,10 @@ def generate_masks(w_dense, g_dense, b: int, s: float, iteration: int = 0):
     gr, gc = nw.shape
     total = gr * gc
     k = _k_of(s, total)
-    kept = _topk_device(nw, k)
-    gsel = _topk_device(ng, k)
+    kept = torch.empty(gr, gc, dtype=torch.uint8, device=A.DEVICE)
+    gsel = torch.empty_like(kept)
+    L.check(L.load().blast_topk_mask2(nw.data_ptr(), ng.data_ptr(), gr, gc, k, kept.data_ptr(),
+                                      gsel.data_ptr(), L.stream()), "topk")
     regrown = torch.empty_like(kept)
     counts = torch.empty(2, dtype=torch.int64, device=A.DEVICE)
     L.check(L.load().blast_mask_difference(kept.data_ptr(), gsel.data_ptr(), total,
@@ -183,11 +185,15 @@ def generate_masks(w_dense, g_dense, b: int, s: float, iteration: int = 0):
 
 
 def apply_mask(w_dense, mask: BlockMask, b: int, zero_regrown: bool = True,
-               dtype: torch.dtype | None = None):
+               dtype: torch.dtype | None = None, structure: BlockSparseMatrix | None = None):
     """masked = W * expand(survivors); BCSC of the masked matrix over the active blocks
     (pruner.py:160-186). survivors = kept (zero_regrown, a fresh mask: regrown blocks
     enter as explicit zero blocks) or kept | regrown (re-application between refreshes).
-    ``dtype`` is the stored value type of the returned matrix (default float32)."""
+    ``dtype`` is the stored value type of the returned matrix (default float32).
+
+    ``structure``: a matrix already built for this very mask (the trainer's cache between
+    refreshes). Its index arrays and execution plans are reused, so a re-application is
+    a single gather launch with no host synchronisation."""
     host = A.is_host(w_dense)
     w = A.to_device(w_dense, torch.float32)
     rows, cols = w.shape
@@ -197,7 +203,14 @@ def apply_mask(w_dense, mask: BlockMask, b: int, zero_regrown: bool = True,
                          f"matrix grid {gr}x{gc} for block size {b}")
     kept, regrown = mask.device_u8()
     vdt = dtype or torch.float32
-    col_ptr, row_idx, kmap, values = bcsc._repack(w, b, kept, regrown, vdt)
+    if structure is not None and (structure.rows, structure.cols, structure.block) == (rows, cols, b):
+        col_ptr, row_idx, kmap = structure.col_ptr, structure.block_row_idx, structure._kmap()
+        alloc = torch.zeros if (rows % b or cols % b) else torch.empty
+        values = alloc((structure.nnzb, b, b), dtype=vdt, device=A.DEVICE)
+        plans = {k: v for k, v in structure._cache.items() if k[0] == "plan"}
+    else:
+        col_ptr, row_idx, kmap, values = bcsc._repack(w, b, kept, regrown, vdt)
+        plans = {}
     masked = torch.empty_like(w)
     L.check(L.load().blast_apply_mask_gather(w.data_ptr(), rows, cols, b, L.F32, kept.data_ptr(),
                                              regrown.data_ptr(), 1 if zero_regrown else 0,
@@ -205,4 +218,5 @@ def apply_mask(w_dense, mask: BlockMask, b: int, zero_regrown: bool = True,
                                              values.data_ptr() if values.numel() else None,
                                              L.dtype_code(vdt), L.stream()), "apply_mask")
     cache = BlockSparseMatrix(rows, cols, b, col_ptr, row_idx, values, kmap, host)
+    cache._cache.update(plans)
     return A.like_input(masked, host), cache

@@ -188,6 +188,28 @@ class TestApplyMask:
         np.testing.assert_array_equal(once, twice)
         assert torch.equal(c1.values, c2.values) and torch.equal(c1.block_row_idx, c2.block_row_idx)
 
+    @pytest.mark.parametrize("rows,cols,b", [(12, 12, 3), (130, 70, 16), (512, 768, 64)])
+    def test_structure_reuse_matches_repack(self, rows, cols, b):
+        """Re-application between refreshes with the previous cache's structure gives
+        the same masked matrix and BCSC bits as a full repack, and shares its plans."""
+        rng = np.random.default_rng(rows + cols)
+        w = torch.from_numpy(rng.standard_normal((rows, cols)).astype(np.float32)).cuda()
+        g = torch.from_numpy(rng.standard_normal((rows, cols)).astype(np.float32)).cuda()
+        mask, _ = bs.generate_masks(w, g, b, 0.7)
+        _, fresh = bs.apply_mask(w, mask, b, zero_regrown=True)
+        fresh.desc()
+        w2 = w + 0.25 * g
+        for dt in (torch.float32, torch.bfloat16):
+            ref_m, ref_c = bs.apply_mask(w2, mask, b, zero_regrown=False, dtype=dt)
+            got_m, got_c = bs.apply_mask(w2, mask, b, zero_regrown=False, dtype=dt,
+                                         structure=fresh)
+            assert torch.equal(got_m, ref_m)
+            assert torch.equal(got_c.col_ptr, ref_c.col_ptr)
+            assert torch.equal(got_c.block_row_idx, ref_c.block_row_idx)
+            assert torch.equal(got_c.values.view(torch.int16 if dt == torch.bfloat16 else torch.int32),
+                               ref_c.values.view(torch.int16 if dt == torch.bfloat16 else torch.int32))
+            assert got_c._cache[("plan", 0)] is fresh._cache[("plan", 0)]
+
     def test_bf16_cache_values(self):
         rng = np.random.default_rng(11)
         w = rng.standard_normal((128, 192)).astype(np.float32)
