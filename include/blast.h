@@ -127,6 +127,16 @@ int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
                       const blast_bcsc_t* up, const blast_bcsc_t* down,
                       const blast_mlp_plan_t* plan, void* y, void* gate_pre, void* up_out,
                       void* gated, void* stream);
+/* blast_mlp_forward on HOST buffers, the reference's boundary (mlp.py:102 takes and returns
+ * ndarrays): x_host [m, e] and y_host [m, e] in the network dtype. The tokens are cut into
+ * chunks of chunk_tokens rows (0: automatic) and the host->device copy of chunk c+1, the
+ * MLP of chunk c and the device->host copy of chunk c-1 run concurrently on two copy
+ * streams and the caller's stream. Stream-ordered: y_host is complete once `stream`
+ * reaches the point of the call. Host buffers should be page-locked for overlap. */
+int blast_mlp_forward_host(const void* x_host, int64_t m, const blast_bcsc_t* gate,
+                           const blast_bcsc_t* up, const blast_bcsc_t* down,
+                           const blast_mlp_plan_t* plan, void* y_host, int64_t chunk_tokens,
+                           void* stream);
 /* First half of blast_mlp_forward: gate and up products of every block column from one
  * load of each activation panel, g = (a*sigmoid(a))*b in the epilogue (mlp.py:111-113).
  * gated is required; gate_pre/up_out optional. */

@@ -60,7 +60,10 @@ _PROTOS = {
     "blast_mlp_forward": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                     C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp, vp, vp,
                                     vp]),
-    "blast_mlp_gate_up": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
+    "blast_mlp_forward_host": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
+                                         C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, i64,
+                                         vp]),
+    "blast_mlp_gate_up":(C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                     C.POINTER(MlpPlanDesc), vp, vp, vp, vp]),
     "blast_mlp_backward_dgrad": (C.c_int, [vp, i64, vp, vp, C.POINTER(BcscDesc),
                                            C.POINTER(BcscDesc), C.POINTER(BcscDesc),

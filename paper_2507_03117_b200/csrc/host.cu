@@ -34,6 +34,21 @@ int num_sms() {
 
 int bytes_of(int dtype) { return dtype == BLAST_BF16 ? 2 : 4; }
 
+void retain_pool_memory() {
+  // The default stream-ordered pool returns freed memory to the driver at every
+  // synchronisation (release threshold 0), so each call's scratch would be re-mapped.
+  // Keep up to 8 GiB cached instead, like torch's caching allocator does for its blocks.
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = 8ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;

@@ -21,6 +21,7 @@ void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
 int num_sms();
 int bytes_of(int dtype);  // BLAST_F32 -> 4, BLAST_BF16 -> 2
+void retain_pool_memory();  // keep freed cudaMallocAsync blocks cached in the default pool
 
 inline int check_launch(const char* what) { return cuda_status(cudaGetLastError(), what); }
 
@@ -41,6 +42,7 @@ struct Scratch {
     if (ptr) cudaFreeAsync(ptr, stream);
   }
   bool alloc(size_t bytes, cudaStream_t s) {
+    retain_pool_memory();
     stream = s;
     if (bytes == 0) bytes = 16;
     return cudaMallocAsync(&ptr, bytes, s) == cudaSuccess;

@@ -138,16 +138,57 @@ def _to_host_acts(acts: MlpActivations) -> MlpActivations:
                                                     acts.gated)))
 
 
-def mlp_forward(x, mlp: SparseMlp, save_activations: bool = True):
+def _host_tensor(x, dt: torch.dtype) -> torch.Tensor:
+    """Contiguous CPU tensor of X in the network dtype (no copy when it already is one)."""
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    if t.dtype != dt:
+        t = t.to(dt)
+    return t.contiguous()
+
+
+def _forward_host(x, mlp: SparseMlp, out: torch.Tensor | None, chunk_tokens: int):
+    """Inference on host buffers: chunked copy-in / MLP / copy-out pipeline in the library
+    (blast_mlp_forward_host). Returns once the host result is complete."""
+    dt = mlp.dtype
+    xt = _host_tensor(x, dt)
+    m, e = xt.shape
+    if out is None:
+        y = torch.empty(m, e, dtype=dt, pin_memory=xt.is_pinned())
+    else:
+        if out.is_cuda or out.dtype != dt or tuple(out.shape) != (m, e) or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous host {dt} tensor of shape {(m, e)}")
+        y = out
+    if m:
+        dg, du, dd = (mat.cache.desc() for mat in mlp.matrices())
+        plan = mlp.plan()
+        L.check(L.load().blast_mlp_forward_host(xt.data_ptr(), m, C.byref(dg), C.byref(du),
+                                                C.byref(dd), C.byref(plan), y.data_ptr(),
+                                                chunk_tokens, L.stream()), "mlp_forward")
+        torch.cuda.current_stream().synchronize()
+    if isinstance(x, torch.Tensor):
+        return y
+    return A.to_host(y)
+
+
+def mlp_forward(x, mlp: SparseMlp, save_activations: bool = True, out=None,
+                chunk_tokens: int = 0):
     """Run the gated MLP; returns (y, MlpActivations) (mlp.py:102-115).
 
     With ``save_activations=False`` (inference) the intermediate never leaves
-    the library and the second element is None.
+    the library and the second element is None. Host inputs (numpy, or a CPU
+    tensor — page-locked for full overlap) then go through the library's
+    chunked transfer pipeline and the result is returned on the host (``out``:
+    optional preallocated host tensor; ``chunk_tokens``: 0 = automatic).
     """
     if A.ndim(x) != 2:
         raise ValueError(f"X must be 2-D (flatten batch/sequence first), got ndim={A.ndim(x)}")
     if A.shape(x)[1] != mlp.embed_dim:
         raise ValueError(f"X feature dim {A.shape(x)[1]} != embedding dim {mlp.embed_dim}")
+    on_host = not (isinstance(x, torch.Tensor) and x.is_cuda)
+    if not save_activations and on_host:
+        return _forward_host(x, mlp, out, chunk_tokens), None
+    if out is not None:
+        raise ValueError("out= is only supported for host inputs with save_activations=False")
     host = A.is_host(x)
     dt = mlp.dtype
     xt = A.to_device(x, dt)

@@ -143,6 +143,36 @@ class TestForward:
         y2, none = bs.mlp_forward(x, net, save_activations=False)
         assert none is None and torch.equal(y1, y2)
 
+    @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+    @pytest.mark.parametrize("chunk", [0, 128, 300, 5000])
+    def test_host_pipeline_matches_device(self, dtype, chunk):
+        """Host buffers through the chunked copy/compute pipeline: bit-identical to the
+        device-resident forward (rows are independent, so chunking changes nothing)."""
+        rng = np.random.default_rng(13)
+        net = build_mlp(rng, 256, 512, 64, 0.8, dtype)
+        x = torch.randn(2100, 256, device="cuda").to(dtype)  # auto: half/full/ragged chunks
+        y_dev, _ = bs.mlp_forward(x, net, save_activations=False)
+        xh = x.cpu().pin_memory()
+        y_pin, none = bs.mlp_forward(xh, net, save_activations=False, chunk_tokens=chunk)
+        assert none is None and not y_pin.is_cuda and y_pin.is_pinned()
+        assert torch.equal(y_pin, y_dev.cpu())
+        out = torch.full((2100, 256), float("nan"), dtype=dtype)  # pageable preallocated out
+        y_out, _ = bs.mlp_forward(x.cpu(), net, save_activations=False, out=out,
+                                  chunk_tokens=chunk)
+        assert y_out is out and torch.equal(out, y_dev.cpu())
+        if dtype == torch.float32:
+            y_np, _ = bs.mlp_forward(x.cpu().numpy(), net, save_activations=False)
+            assert isinstance(y_np, np.ndarray)
+            np.testing.assert_array_equal(y_np, y_dev.cpu().numpy())
+
+    def test_host_pipeline_errors(self):
+        net = build_mlp(np.random.default_rng(2), 8, 8, 4)
+        with pytest.raises(ValueError, match="out"):
+            bs.mlp_forward(np.ones((3, 8), np.float32), net, save_activations=False,
+                           out=torch.empty(3, 7))
+        y, _ = bs.mlp_forward(np.ones((0, 8), np.float32), net, save_activations=False)
+        assert y.shape == (0, 8)
+
 
 class TestBackward:
     def test_zero_upstream_zero_grads(self):
