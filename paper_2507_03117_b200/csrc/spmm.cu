@@ -92,10 +92,11 @@ static SpmmParams make_params(const EngineCall& c) {
   return p;
 }
 
-template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT>
+template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
+          int OUT_ELT = 0>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
-  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK>;
-  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT>;
+  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT>;
+  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -137,14 +138,21 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
     mW1lo = mW1;
     if (ok && NPASS == 3) ok = mkW(&mW1lo, c.w1_lo, c.nnzb1);
   }
+  // staged output: out0 [m x n_valid], row pitch ld_out, box = one swizzle atom x 128 rows
+  CUtensorMap mO = mA0;
+  if (ok && OUT_ELT > 0)
+    ok = encode_map_2d(&mO, c.out0, OUT_ELT == 2 ? BLAST_BF16 : BLAST_F32,
+                       static_cast<uint64_t>(c.n_valid), static_cast<uint64_t>(c.m),
+                       static_cast<uint64_t>(c.ld_out) * OUT_ELT, Cfg::OUT_SW / (OUT_ELT ? OUT_ELT : 1),
+                       Cfg::BM, Cfg::OUT_SW);
   if (!ok) return BLAST_EINVAL;
   const SpmmParams p = make_params(c);
   const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
   dbg_begin(st);
-  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo,
-                                                  p);
+  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1,
+                                                  mW1lo, p);
   const int rc = check_launch("spmm_tc");
   dbg_end("spmm_tc", st, grid);
   return rc;
@@ -163,18 +171,59 @@ constexpr bool tc_fits() {
   return (200 * 1024) / stage >= 2 && 2 * nacc * B <= 512;
 }
 
+// Staged (TMA-store) output for out0: bf16 outputs whose rows are 16-byte aligned, when
+// the staging buffers still leave >= 3 pipeline stages. BLAST_DIRECT_STORES=1 disables it.
+static bool staged_out_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_DIRECT_STORES");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+// >= 3 pipeline stages next to the double-buffered bf16 output staging (TcCfg arithmetic)
+template <int B, int ELT, int NPASS, int NMAT, bool SUM>
+constexpr bool staged_fits() {
+  if (ELT != 2 || NPASS != 1) return false;
+  constexpr int rowb = B * ELT;
+  constexpr int a_tile = (128 * rowb + 1023) / 1024 * 1024;
+  constexpr int b_tile = (B * rowb + 1023) / 1024 * 1024;
+  constexpr int na = SUM ? NMAT : 1;
+  constexpr int stage = na * a_tile + NMAT * b_tile;
+  constexpr int staging = 2 * ((128 * B * 2 + 1023) / 1024 * 1024);
+  return (216 * 1024 - staging) / stage >= 3;
+}
+template <int B, int ELT, int NPASS, int NMAT, bool SUM>
+static bool use_staged(const EngineCall& c) {
+  if (!staged_fits<B, ELT, NPASS, NMAT, SUM>() || staged_out_disabled()) return false;
+  if (c.accumulate || !aligned16(c.out0) || (c.ld_out * 2) % 16 != 0) return false;
+  return c.epi == EPI_STORE || c.epi == EPI_GATED_FWD;
+}
+
 template <int B, int ELT, int NPASS, typename OutT>
 static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
+  constexpr int SO = (ELT == 2 && NPASS == 1) ? 2 : 0;  // staged-output element size
   if (!c.transposed) {
     if (c.nmat == 1 && c.epi == EPI_STORE) {
-      if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
+      if constexpr (tc_fits<B, ELT, NPASS, 1, false>()) {
+        if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
+          if (use_staged<B, ELT, NPASS, 1, false>(c))
+            return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
         return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT>(c, a0lo, a1lo, st);
+      }
     } else if (c.nmat == 2 && c.epi == EPI_GATED_FWD) {
-      if constexpr (tc_fits<B, ELT, NPASS, 2, false>())
+      if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
+        if constexpr (staged_fits<B, ELT, NPASS, 2, false>())
+          if (use_staged<B, ELT, NPASS, 2, false>(c))
+            return launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO>(c, a0lo, a1lo, st);
         return launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT>(c, a0lo, a1lo, st);
+      }
     }
   } else {
     if (c.nmat == 1 && c.epi == EPI_STORE) {
+      if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
+        if (use_staged<B, ELT, NPASS, 1, false>(c))
+          return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
     } else if (c.nmat == 1 && c.epi == EPI_GATED_BWD) {

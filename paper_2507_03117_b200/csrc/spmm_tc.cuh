@@ -109,7 +109,9 @@ struct StepCursor {
   }
 };
 
-template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR>
+// OUT_ELT > 0: out0 is staged in shared memory (double-buffered, swizzled) and
+// written by TMA stores (whole 128-byte lines) instead of per-thread row-strided stores.
+template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0>
 struct TcCfg {
   static constexpr int BM = 128;
   static constexpr int ROWB = B * ELT;                    // bytes of one block row
@@ -124,7 +126,12 @@ struct TcCfg {
   static constexpr int A_TILE = round1k(BM * ROWB);
   static constexpr int B_TILE = round1k(B * ROWB);
   static constexpr int STAGE = NA * NCOPY * A_TILE + NMAT * NCOPY * B_TILE;
-  static constexpr int SMEM_BUDGET = 200 * 1024;
+  static constexpr int OUT_ROWB = B * OUT_ELT;                          // bytes of an output tile row
+  static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
+  static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
+  static constexpr int OUT_TILE = OUT_ELT ? round1k(BM * OUT_ROWB) : 0;
+  static constexpr int STAGING = 2 * OUT_TILE;
+  static constexpr int SMEM_BUDGET = OUT_ELT ? 216 * 1024 - STAGING : 200 * 1024;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int NACC = SUMACC ? 1 : NMAT;
@@ -139,12 +146,44 @@ struct TcCfg {
       make_idesc(BM, B, ELT == 2 ? 1u : 2u, 0u, B_KMAJOR ? 0u : 1u);
   // barriers + tmem slot live after the stages
   static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM_BYTES = STAGES * STAGE + BAR_BYTES + 1024;  // +1024 alignment slack
+  static constexpr int SMEM_BYTES = STAGES * STAGE + STAGING + BAR_BYTES + 1024;  // +1024 alignment slack
   static_assert(STAGES >= 2, "stage does not fit twice in shared memory");
   static_assert(B % 16 == 0 && B >= 16 && B <= 256, "tensor-core block size");
   static_assert(TMEM_COLS_RAW <= 512, "accumulators exceed TMEM");
   static_assert(ROWB % SW == 0, "row must be whole swizzle atoms");
+  static_assert(OUT_ELT == 0 || (OUT_ROWB >= 32 && OUT_ROWB % (OUT_SW ? OUT_SW : 1) == 0), "staged output rows");
 };
+
+// Write 16 consecutive output values of tile row `row` starting at tile column `col`
+// into a staged output tile laid out as OUT_NATOM swizzle atoms of [128 rows x SW bytes]
+// (the layout a SWIZZLE_<SW> TMA store reads): 16-byte unit u of a row lands at
+// u ^ ((row * SW / 128) mod (SW / 16)).
+template <typename OutT, int SW>
+__device__ __forceinline__ void stage_chunk16(uint8_t* tile, int row, int col, const float (&v)[16]) {
+  constexpr int E = sizeof(OutT);
+  constexpr int UNITS = 16 * E / 16;  // 16-byte units of this chunk
+  const int byte0 = col * E;
+  uint8_t* atom = tile + (byte0 / SW) * (128 * SW) + row * SW;
+  const int u0 = (byte0 % SW) / 16;
+  const int x = ((row * SW) >> 7) & (SW / 16 - 1);
+#pragma unroll
+  for (int k = 0; k < UNITS; ++k) {
+    uint4 w;
+    if constexpr (E == 4) {
+      w = make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                     __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+    } else {
+      uint32_t h[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 pr = __floats2bfloat162_rn(v[8 * k + 2 * i], v[8 * k + 2 * i + 1]);
+        h[i] = *reinterpret_cast<uint32_t*>(&pr);
+      }
+      w = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+    *reinterpret_cast<uint4*>(atom + (((u0 + k) ^ x) * 16)) = w;
+  }
+}
 
 // K-major operand (rows x B elements, stored as NATOM swizzle atoms of `rows` x SW bytes):
 // descriptor for K slice `ks`.
@@ -225,10 +264,14 @@ __device__ __forceinline__ void load_chunk16(const T* src, float (&v)[16], int v
 //   EPI_GATED_FWD  out0 = silu(a) * b; out1 = a, out2 = b (optional)   (mlp.py:111-113)
 //   EPI_GATED_BWD  in1 set: out0 = dA, out1 = dB from dG = v0          (mlp.py:133-139)
 //                  in1 NULL: out0 = v0 * act'(in0)  (backward of a fused activation)
-template <int EPI, typename OutT>
+// STG_SW > 0: out0 goes to the staged tile `stg` (tile row `trow`, tile column `tcol`)
+// instead of global memory; rows / columns outside the tensor are clipped by the TMA store.
+template <int EPI, typename OutT, int STG_SW = 0>
 __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[16],
                                                uint32_t acc1_addr, int flags, bool row_ok,
-                                               int col, int valid, int64_t off, bool vec_ok) {
+                                               int col, int valid, int64_t off, bool vec_ok,
+                                               uint8_t* stg = nullptr, int trow = 0,
+                                               int tcol = 0) {
   const bool live = row_ok && valid > 0;
   if constexpr (EPI == EPI_STORE) {
     add_bias16(v0, p.bias, col, valid);
@@ -236,7 +279,9 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
       store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
 #pragma unroll
     for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
-    if (live) {
+    if constexpr (STG_SW > 0) {
+      stage_chunk16<OutT, STG_SW>(stg, trow, tcol, v0);
+    } else if (live) {
       if (p.accumulate) {
         float prev[16];
         load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.out0) + off, prev, valid, vec_ok);
@@ -255,10 +300,15 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
     if (live) {
       if (p.out1) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
       if (p.out2) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out2) + off, v1, valid, vec_ok);
+    }
+    if (live || STG_SW > 0) {
       float g[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) g[i] = gated_fwd(v0[i], v1[i]);
-      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
+      if constexpr (STG_SW > 0)
+        stage_chunk16<OutT, STG_SW>(stg, trow, tcol, g);
+      else
+        store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
     }
   } else {
     if (!live) return;
@@ -285,17 +335,21 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
 constexpr int kTcThreads = 384;
 constexpr int kEpiWarps = 8;
 
-template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT>
+template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
+          int OUT_ELT = 0>
 __global__ void __launch_bounds__(kTcThreads, 1)
-spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
+spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
+               const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
                const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA1lo,
                const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW0lo,
                const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW1lo,
                const SpmmParams p) {
-  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR>;
+  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT>;
+  static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint8_t* staging = smem + C::STAGES * C::STAGE;  // [2][OUT_TILE] when OUT_ELT > 0
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE + C::STAGING);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tmem_full = empty + C::STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
@@ -306,6 +360,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   const int n_items = p.n_tok_tiles * p.n_lines;
 
   if (warp == 0 && lane == 0) {
+    if (OUT_ELT) tma_prefetch(&mapO);
     tma_prefetch(&mapA0);
     tma_prefetch(&mapW0);
     if (NMAT > 1) tma_prefetch(&mapW1);
@@ -493,6 +548,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;                 // TMEM lane quarter
     const int half = static_cast<int>(warp - 4) >> 2;  // which 16-column chunks
+    const uint32_t etid = threadIdx.x - 128;     // 0..255 over the epilogue warps
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
@@ -502,7 +558,14 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
       const int flags = __ldg(&p.line_flags[j]);
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
-      const int row = t * C::BM + static_cast<int>(q * 32 + lane);
+      uint8_t* stg = staging + (it & 1) * C::OUT_TILE;
+      if constexpr (OUT_ELT > 0) {
+        // the TMA store issued two items ago from this buffer must have read it
+        if (etid == 0) bulk_wait_group_read<1>();
+        named_bar_sync(1, kEpiWarps * 32);
+      }
+      const int trow = static_cast<int>(q * 32 + lane);
+      const int row = t * C::BM + trow;
       const bool row_ok = row < p.m;
       const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
 #pragma unroll 1
@@ -517,12 +580,26 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
 #pragma unroll
           for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
         }
-        epilogue_chunk<EPI, OutT>(p, v0, tbase + B + c * 16, flags, row_ok, col, valid, off,
-                                  vec_ok);
+        epilogue_chunk<EPI, OutT, C::OUT_SW>(p, v0, tbase + B + c * 16, flags, row_ok, col, valid,
+                                             off, vec_ok, stg, trow, c * 16);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[as]);
+      if constexpr (OUT_ELT > 0) {
+        fence_proxy_async_smem();
+        named_bar_sync(1, kEpiWarps * 32);
+        if (etid == 0) {
+#pragma unroll
+          for (int a = 0; a < C::OUT_NATOM; ++a)
+            tma_store_2d(&mapO, stg + a * (C::BM * C::OUT_SW), j * B + a * (C::OUT_SW / OUT_ELT),
+                         t * C::BM);
+          bulk_commit_group();
+        }
+      }
+    }
+    if constexpr (OUT_ELT > 0) {
+      if (etid == 0) bulk_wait_group<0>();
     }
   }
 
