@@ -24,7 +24,7 @@ FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
     "--expt-relaxed-constexpr", "-I", str(INCLUDE), "-I", str(CSRC),
     "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("BLAST_NVCC_FLAGS", "").split()
 
 
 def _sources() -> list[Path]:

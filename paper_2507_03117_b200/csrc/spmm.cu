@@ -73,6 +73,14 @@ static void dbg_end(const char* name, cudaStream_t st, int ctas) {
 static SpmmParams make_params(const EngineCall& c) {
   SpmmParams p{};
   p.dbg = dbg_buffer();
+  {
+    static int skip = -1;
+    if (skip < 0) {
+      const char* e = getenv("BLAST_SKIP_EPILOGUE");
+      skip = e ? atoi(e) : 0;
+    }
+    p.skip_epilogue = skip;
+  }
   p.m = static_cast<int32_t>(c.m);
   p.n_lines = static_cast<int32_t>(c.n_lines);
   p.n_valid = static_cast<int32_t>(c.n_valid);
@@ -191,7 +199,7 @@ constexpr bool staged_fits() {
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
   constexpr int staging = 2 * ((128 * B * 2 + 1023) / 1024 * 1024);
-  return (216 * 1024 - staging) / stage >= 3;
+  return (232448 - 1024 - 512 - staging) / stage >= 3;
 }
 template <int B, int ELT, int NPASS, int NMAT, bool SUM>
 static bool use_staged(const EngineCall& c) {

@@ -356,8 +356,9 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
 #pragma unroll
             for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
           }
-          epilogue_chunk<EPI, OutT>(p, v0, tbase + B + c * 16, flags, row_ok, col, valid, off,
-                                    vec_ok);
+          float v1[16];
+          if (EPI == EPI_GATED_FWD) tmem_ld16(tbase + B + c * 16, v1);
+          epilogue_chunk<EPI, OutT>(p, v0, v1, flags, row_ok, col, valid, off, vec_ok);
         }
         tc_fence_before();
         __syncwarp();

@@ -47,6 +47,7 @@ struct SpmmParams {
   int64_t ld_out;   // row stride (elements) of every out*/in* array
   unsigned long long* dbg;  // optional per-role wait-cycle counters (BLAST_DEBUG_COUNTERS)
   const float* bias;        // EPI_STORE: optional per-output-column bias, added before act
+  int32_t skip_epilogue;    // diagnosis only (BLAST_SKIP_EPILOGUE=1): release accumulators unread
 };
 
 // v[i] += bias[col + i] for the valid columns of a 16-column chunk
@@ -131,7 +132,8 @@ struct TcCfg {
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
   static constexpr int OUT_TILE = OUT_ELT ? round1k(BM * OUT_ROWB) : 0;
   static constexpr int STAGING = 2 * OUT_TILE;
-  static constexpr int SMEM_BUDGET = OUT_ELT ? 216 * 1024 - STAGING : 200 * 1024;
+  // 227 KB opt-in maximum minus barriers, alignment slack and the output staging
+  static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 512 - STAGING : 200 * 1024;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int NACC = SUMACC ? 1 : NMAT;
@@ -145,7 +147,7 @@ struct TcCfg {
   static constexpr uint32_t IDESC =
       make_idesc(BM, B, ELT == 2 ? 1u : 2u, 0u, B_KMAJOR ? 0u : 1u);
   // barriers + tmem slot live after the stages
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE + STAGING + BAR_BYTES + 1024;  // +1024 alignment slack
   static_assert(STAGES >= 2, "stage does not fit twice in shared memory");
   static_assert(B % 16 == 0 && B >= 16 && B <= 256, "tensor-core block size");
@@ -224,7 +226,9 @@ __device__ __forceinline__ void store_chunk16(OutT* dst, const float (&v)[16], i
       }
     }
   } else {
-    for (int i = 0; i < 16 && i < valid; ++i) dst[i] = from_f32<OutT>(v[i]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < valid) dst[i] = from_f32<OutT>(v[i]);
   }
 }
 template <typename T>
@@ -268,7 +272,7 @@ __device__ __forceinline__ void load_chunk16(const T* src, float (&v)[16], int v
 // instead of global memory; rows / columns outside the tensor are clipped by the TMA store.
 template <int EPI, typename OutT, int STG_SW = 0>
 __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[16],
-                                               uint32_t acc1_addr, int flags, bool row_ok,
+                                               float (&v1)[16], int flags, bool row_ok,
                                                int col, int valid, int64_t off, bool vec_ok,
                                                uint8_t* stg = nullptr, int trow = 0,
                                                int tcol = 0) {
@@ -291,8 +295,6 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
       store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
     }
   } else if constexpr (EPI == EPI_GATED_FWD) {
-    float v1[16];
-    tmem_ld16(acc1_addr, v1);
     if (!(flags & 2)) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v1[i] = 0.0f;
@@ -304,9 +306,19 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
     if (live || STG_SW > 0) {
       float g[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) g[i] = gated_fwd(v0[i], v1[i]);
-      if constexpr (STG_SW > 0)
-        stage_chunk16<OutT, STG_SW>(stg, trow, tcol, g);
+      for (int i = 0; i < 16; ++i) {
+        if constexpr (sizeof(OutT) == 2)
+          g[i] = gated_fwd_fast(v0[i], v1[i]);
+        else
+          g[i] = gated_fwd(v0[i], v1[i]);
+      }
+      if constexpr (STG_SW > 0) {
+        if (p.skip_epilogue >= 6) {  // diagnosis: no staging writes
+          if (g[0] == 1234.5f && g[7] == 1.5f) p.dbg[1] = 1;
+        } else {
+          stage_chunk16<OutT, STG_SW>(stg, trow, tcol, g);
+        }
+      }
       else
         store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
     }
@@ -329,6 +341,13 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
     }
   }
 }
+
+// per-stage MMA recipe bits (producer -> MMA warp through shared memory)
+constexpr uint32_t kMetaHas0 = 1u;        // block of matrix 0 in this stage
+constexpr uint32_t kMetaHas1 = 2u;        // block of matrix 1 in this stage
+constexpr uint32_t kMetaMerged = 4u;      // one N = 2B MMA covers both (gate | up)
+constexpr uint32_t kMetaAccFirst = 8u;    // first MMA group accumulates (else overwrites)
+constexpr uint32_t kMetaAccSecond = 16u;  // second MMA group accumulates
 
 // 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (two warps per TMEM lane quarter, splitting the 16-column chunks).
@@ -354,6 +373,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
   uint64_t* tmem_full = empty + C::STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  // per-stage MMA recipe written by the producer before its expect_tx arrive (release) and
+  // read by the MMA warp after the full-barrier wait (acquire): see kMeta* below
+  uint32_t* stage_meta = tmem_slot + 4;
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -384,23 +406,67 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   WaitClock wc;
+#ifdef BLAST_WAIT_COUNTERS
   const bool dbg_on = p.dbg != nullptr;
+#else
+  constexpr bool dbg_on = false;  // keep the role loops free of diagnosis code
+#endif
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    // The whole warp walks the schedule (warp-uniform control flow keeps the loop
-    // state in uniform registers); one elected lane issues the copies.
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------------------ TMA producers
+    // Two warps walk the same schedule (warp-uniform control flow keeps the loop
+    // state in uniform registers); warp 0 issues the copies of even steps, warp 3
+    // those of odd steps, so the per-step issue latency is overlapped. One elected
+    // lane issues each copy.
     const uint64_t pol_w = policy_evict_last();
-    uint32_t stage = 0, phase = 0;
+    const uint32_t mine = warp == 0 ? 0u : 1u;
+    uint32_t stage = 0, phase = 0, n = 0;
+    // merged gate+up: one N = 2B MMA over [W_gate | W_up] (adjacent MN-major atoms)
+    constexpr bool kMerge = (NMAT == 2) && !SUMACC && !B_KMAJOR && (2 * B <= 256) &&
+                            (C::NATOM == 1 || C::B_TILE == C::NATOM * B * C::SW);
+    // The next item's step range and first 32 steps are fetched one item ahead, so
+    // the item boundary does not stall the ring on two dependent global loads.
+    int nx_s0 = 0, nx_s1 = 0;
+    int4 nx_first = make_int4(0, -1, -1, 0);
+    auto prefetch = [&](int item) {
+      if (item >= n_items) return;
+      const int jn = item % p.n_lines;
+      nx_s0 = __ldg(&p.step_ptr[jn]);
+      nx_s1 = __ldg(&p.step_ptr[jn + 1]);
+      const int idx = nx_s0 + static_cast<int>(lane);
+      nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
+    };
+    prefetch(blockIdx.x);
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int t = item / p.n_lines;
-      const int j = item - t * p.n_lines;
-      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      const int s0 = nx_s0, s1 = nx_s1;
       StepCursor cur;
-      cur.start(p.steps, s0, s1);
+      cur.steps = p.steps;
+      cur.end = s1;
+      cur.base = s0;
+      cur.mine = nx_first;
+      prefetch(item + gridDim.x);
+      uint32_t init0 = 0, init1 = 0;  // accumulator i already holds a partial sum
       for (int s = s0; s < s1; ++s) {
         const int4 st = cur.get(s);
         const int kb[2] = {st.y, st.z};
+        const bool has0 = st.y >= 0, has1 = NMAT > 1 && st.z >= 0;
+        // MMA recipe of this step (the MMA warp only decodes it)
+        uint32_t meta = (has0 ? kMetaHas0 : 0u) | (has1 ? kMetaHas1 : 0u);
+        if (kMerge && has0 && has1 && init0 == init1) {
+          meta |= kMetaMerged | (init0 ? kMetaAccFirst : 0u);
+          init0 = init1 = 1;
+        } else {
+          if (has0) { meta |= init0 ? kMetaAccFirst : 0u; init0 = 1; }
+          if (has1) {
+            if (SUMACC) { meta |= init0 ? kMetaAccSecond : 0u; init0 = 1; }
+            else { meta |= init1 ? kMetaAccSecond : 0u; init1 = 1; }
+          }
+        }
+        if ((n++ & 1u) != mine) {
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          continue;
+        }
         wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
         if (elect_one()) {
           uint32_t bytes = 0;
@@ -410,6 +476,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm)
             if (kb[mm] >= 0) bytes += C::NCOPY * (B * C::ROWB);
+          stage_meta[stage] = meta;
           mbar_expect_tx(&full[stage], bytes);
           uint8_t* sbase = smem + stage * C::STAGE;
 #pragma unroll
@@ -475,37 +542,37 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       return (static_cast<uint32_t>(ks) * C::MMA_K * C::SW) >> 4;
     };
     uint32_t stage = 0, phase = 0, it = 0;
+    auto steps_of = [&](int item) -> int {
+      if (item >= n_items) return 0;
+      const int jn = item % p.n_lines;
+      return __ldg(&p.step_ptr[jn + 1]) - __ldg(&p.step_ptr[jn]);
+    };
+    int nx_steps = steps_of(blockIdx.x);  // one item ahead (see the producer)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int t = item / p.n_lines;
-      const int j = item - t * p.n_lines;
-      (void)t;
       const uint32_t as = it & 1, use = it >> 1;
+      const int n_steps = nx_steps;
+      nx_steps = steps_of(item + gridDim.x);
       wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
       tc_fence_after();
-      uint32_t init0 = 0, init1 = 0;
-      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
       const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
-      StepCursor cur;
-      cur.start(p.steps, s0, s1);
-      for (int s = s0; s < s1; ++s) {
-        const int4 st = cur.get(s);
-        const bool has0 = st.y >= 0, has1 = NMAT > 1 && st.z >= 0;
+      for (int s = 0; s < n_steps; ++s) {
         wc.wait(2, &full[stage], phase, dbg_on);
-        wc.acc[7] += dbg_on;
         tc_fence_after();
+        const uint32_t meta = *reinterpret_cast<volatile uint32_t*>(&stage_meta[stage]);
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
           const uint64_t ad = a_desc0 + soff;
           const uint64_t bd = b_desc0 + soff;
-          if (kMerge && has0 && has1 && init0 == init1) {
+          if (kMerge && (meta & kMetaMerged)) {
+            const uint32_t acc = (meta & kMetaAccFirst) ? 1u : 0u;
 #pragma unroll
             for (int ks = 0; ks < C::KSL; ++ks)
               mma_f16(d_base, ad + a_koff(ks), b_desc0_merged + soff + b_koff(ks), kIdescMerged,
-                      (init0 | ks) ? 1u : 0u);
+                      (acc | ks) ? 1u : 0u);
           } else {
 #pragma unroll
             for (int mm = 0; mm < NMAT; ++mm) {
-              if (!(mm == 0 ? has0 : has1)) continue;
+              if (!(meta & (mm == 0 ? kMetaHas0 : kMetaHas1))) continue;
               const int acc_i = SUMACC ? 0 : mm;
               const int a_i = SUMACC ? mm : 0;
               const uint32_t d = d_base + acc_i * B;
@@ -513,7 +580,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
               const uint64_t a_lo = a_hi + (C::A_TILE >> 4);
               const uint64_t b_hi = bd + ((mm * C::NCOPY * C::B_TILE) >> 4);
               const uint64_t b_lo = b_hi + (C::B_TILE >> 4);
-              const uint32_t init = acc_i == 0 ? init0 : init1;
+              const uint32_t init = (meta & (mm == 0 ? kMetaAccFirst : kMetaAccSecond)) ? 1u : 0u;
 #pragma unroll
               for (int ks = 0; ks < C::KSL; ++ks) {
                 const uint32_t acc_flag = (init | ks) ? 1u : 0u;
@@ -528,17 +595,11 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
                   mma_f16(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
                 }
               }
-              if (acc_i == 0) init0 = 1; else init1 = 1;
             }
           }
           mma_commit(&empty[stage]);
         }
         __syncwarp();
-        if (kMerge && has0 && has1) { init0 = 1; init1 = 1; }
-        else {
-          if (has0) init0 = 1;
-          if (has1) { if (SUMACC) init0 = 1; else init1 = 1; }
-        }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
       if (elect_one()) mma_commit(&tmem_full[as]);
@@ -549,6 +610,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
     const uint32_t q = warp & 3;                 // TMEM lane quarter
     const int half = static_cast<int>(warp - 4) >> 2;  // which 16-column chunks
     const uint32_t etid = threadIdx.x - 128;     // 0..255 over the epilogue warps
+    // outputs stream through L2 (evict first) so they do not push out the re-read
+    // activation panels and weight blocks
+    const uint64_t pol_out = policy_evict_first();
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
@@ -558,42 +622,91 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       const int flags = __ldg(&p.line_flags[j]);
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
+      if (p.skip_epilogue == 3) {  // diagnosis: TMEM reads + gating math, no stores
+        uint32_t r0[16], r1[16];
+        float accv = 0.0f;
+#pragma unroll 1
+        for (int c = half; c < B / 16; c += 2) {
+          const uint32_t tb = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + c * 16;
+          tmem_ld16_nowait(tb, r0);
+          tmem_ld16_nowait(tb + B, r1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            accv += gated_fwd_fast(__uint_as_float(r0[i]), __uint_as_float(r1[i]));
+        }
+        if (accv == 1234.5f) p.dbg[0] = 1;
+      }
+      if (p.skip_epilogue == 2) {  // diagnosis: TMEM reads only
+        uint32_t r0[16];
+#pragma unroll 1
+        for (int c = half; c < 2 * B / 16; c += 2) {
+          tmem_ld16_nowait(tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + c * 16, r0);
+          tmem_wait_ld();
+          if (r0[0] == 0x7fc00001u && r0[15] == 0x7fc00001u) p.dbg[0] = 1;  // keep the loads
+        }
+      }
+      if (p.skip_epilogue && p.skip_epilogue < 4) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_empty[as]);
+        continue;
+      }
       uint8_t* stg = staging + (it & 1) * C::OUT_TILE;
       if constexpr (OUT_ELT > 0) {
         // the TMA store issued two items ago from this buffer must have read it
         if (etid == 0) bulk_wait_group_read<1>();
-        named_bar_sync(1, kEpiWarps * 32);
+        if (p.skip_epilogue != 7) named_bar_sync(1, kEpiWarps * 32);
       }
       const int trow = static_cast<int>(q * 32 + lane);
       const int row = t * C::BM + trow;
       const bool row_ok = row < p.m;
       const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
+      // this warp's 16-column chunks are c = half, half + 2, ...; the TMEM loads of two
+      // chunks (both accumulators when gated) are issued before one wait
+      constexpr int NCH = B / 16;
+      constexpr bool kTwoAcc = EPI == EPI_GATED_FWD;
+      const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
 #pragma unroll 1
-      for (int c = half; c < B / 16; c += 2) {
-        const int col = j * B + c * 16;
-        const int valid = p.n_valid - col;
-        const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
-        float v0[16];
-        tmem_ld16(tbase + c * 16, v0);
-        const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
-        if (!acc0_init) {
+      for (int c0 = half; c0 < NCH; c0 += 4) {
+        uint32_t r0[2][16], r1[2][16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
+        for (int k = 0; k < 2; ++k) {
+          const int c = c0 + 2 * k;
+          if (c < NCH) {
+            tmem_ld16_nowait(tbase + c * 16, r0[k]);
+            if (kTwoAcc) tmem_ld16_nowait(tbase + B + c * 16, r1[k]);
+          }
         }
-        epilogue_chunk<EPI, OutT, C::OUT_SW>(p, v0, tbase + B + c * 16, flags, row_ok, col, valid,
-                                             off, vec_ok, stg, trow, c * 16);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int c = c0 + 2 * k;
+          if (c >= NCH) break;
+          const int col = j * B + c * 16;
+          const int valid = p.n_valid - col;
+          const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
+          float v0[16], v1[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v0[i] = acc0_init ? __uint_as_float(r0[k][i]) : 0.0f;
+            v1[i] = kTwoAcc ? __uint_as_float(r1[k][i]) : 0.0f;
+          }
+          epilogue_chunk<EPI, OutT, C::OUT_SW>(p, v0, v1, flags, row_ok, col, valid, off, vec_ok,
+                                               stg, trow, c * 16);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[as]);
       if constexpr (OUT_ELT > 0) {
-        fence_proxy_async_smem();
-        named_bar_sync(1, kEpiWarps * 32);
-        if (etid == 0) {
+        if (p.skip_epilogue < 5) fence_proxy_async_smem();  // 5..7: diagnosis, no fence (no store)
+        if (p.skip_epilogue != 7) named_bar_sync(1, kEpiWarps * 32);
+        if (etid == 0 && p.skip_epilogue < 4) {  // 4..6: diagnosis, never stored
 #pragma unroll
           for (int a = 0; a < C::OUT_NATOM; ++a)
-            tma_store_2d(&mapO, stg + a * (C::BM * C::OUT_SW), j * B + a * (C::OUT_SW / OUT_ELT),
-                         t * C::BM);
+            tma_store_2d_hint(&mapO, stg + a * (C::BM * C::OUT_SW), j * B + a * (C::OUT_SW / OUT_ELT),
+                              t * C::BM, pol_out);
           bulk_commit_group();
         }
       }

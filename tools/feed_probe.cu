@@ -23,15 +23,16 @@ using namespace blast;
   } while (0)
 
 constexpr int M = 8192, D = 4096, LINES = 224, STEPS = 12, NBLK = LINES * STEPS;
-constexpr int PANEL = 128 * 128, WBLK = 8192, STAGE = PANEL + WBLK;
+constexpr int PANEL = 128 * 128, WBLK = 8192;
 
-template <int P, int S, int MMA>
+template <int P, int S, int MMA, int ASC = 0, int GU = 0>
 __global__ void __launch_bounds__(256, 1) feed_kernel(const __grid_constant__ CUtensorMap mx,
-                                                      const __grid_constant__ CUtensorMap mw, int n_items) {
+                                                      const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mw2, int n_items) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[16], empty[16];
   __shared__ uint32_t tslot;
+  constexpr int STAGE = PANEL + (GU ? 2 : 1) * WBLK;
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 16; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -49,13 +50,13 @@ __global__ void __launch_bounds__(256, 1) feed_kernel(const __grid_constant__ CU
       for (int s = 0; s < STEPS; ++s, ++n) {
         if ((n % P) != static_cast<uint32_t>(warp)) continue;
         const uint32_t stage = n % S, phase = (n / S) & 1;
-        const int r = (line * 7 + s * 5) & 63, k = line * STEPS + s;
+        const int r = ASC ? (s * 5 + (line & 3)) : ((line * 7 + s * 5) & 63), k = line * STEPS + s;
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
-          mbar_expect_tx(&full[stage], STAGE);
+          mbar_expect_tx(&full[stage], PANEL + WBLK);
           uint8_t* dst = smem + stage * STAGE;
           tma_load_2d(dst, &mx, &full[stage], r * 64, (t & (n_tiles - 1)) * 128);
-          tma_load_2d(dst + PANEL, &mw, &full[stage], 0, k * 64);
+          tma_load_2d(dst + PANEL + (GU ? (s & 1) * WBLK : 0), (ASC == 2 && (s & 1)) ? &mw2 : &mw, &full[stage], 0, k * 64);
         }
         __syncwarp();
       }
@@ -75,7 +76,8 @@ __global__ void __launch_bounds__(256, 1) feed_kernel(const __grid_constant__ CU
             const uint32_t off = (stage * STAGE) >> 4;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              mma_f16(tbase + (n & 1) * 64, ad0 + off + ks * 2, bd0 + off + ks * 2, idesc, (s | ks) ? 1u : 0u);
+              mma_f16(tbase + (GU ? (s & 1) * 64 : (n & 1) * 64), ad0 + off + ks * 2,
+                      bd0 + off + ks * 2 + (GU ? (s & 1) * (WBLK >> 4) : 0), idesc, (s | ks) ? 1u : 0u);
             mma_commit(&empty[stage]);
           } else {
             mbar_arrive(&empty[stage]);
@@ -111,23 +113,24 @@ static CUtensorMap map2d(void* base, uint64_t inner, uint64_t outer, uint32_t bo
   return m;
 }
 
-template <int P, int S, int MMA>
-void run(const CUtensorMap& mx, const CUtensorMap& mw, cudaEvent_t e0, cudaEvent_t e1) {
-  auto k = feed_kernel<P, S, MMA>;
+template <int P, int S, int MMA, int ASC = 0, int GU = 0>
+void run(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mw2, cudaEvent_t e0, cudaEvent_t e1) {
+  auto k = feed_kernel<P, S, MMA, ASC, GU>;
+  constexpr int STAGE = PANEL + (GU ? 2 : 1) * WBLK;
   const int smem = S * STAGE + 2048;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int n_items = (M / 128) * LINES;
-  k<<<148, 256, smem>>>(mx, mw, n_items);
+  k<<<148, 256, smem>>>(mx, mw, mw2, n_items);
   CK(cudaEventRecord(e0));
-  k<<<148, 256, smem>>>(mx, mw, n_items);
+  k<<<148, 256, smem>>>(mx, mw, mw2, n_items);
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   CK(cudaGetLastError());
   float ms;
   CK(cudaEventElapsedTime(&ms, e0, e1));
-  const double bytes = double(n_items) * STEPS * STAGE;
+  const double bytes = double(n_items) * STEPS * (PANEL + WBLK);
   const double steps_per_sm = double(n_items) * STEPS / 148.0;
-  printf("producers=%d stages=%d consumer=%s: %.3f ms  %.0f GB/s  %.0f cyc/step/SM  (MMA-only floor 280)\n", P, S,
+  printf("gu=%d asc=%d producers=%d stages=%d consumer=%s: %.3f ms  %.0f GB/s  %.0f cyc/step/SM  (MMA-only floor 280)\n", GU, ASC, P, S,
          MMA ? "mma" : "release", ms, bytes / (ms * 1e6), ms * 1e-3 * 1.965e9 / steps_per_sm);
 }
 
@@ -142,12 +145,10 @@ int main() {
   CK(cudaEventCreate(&e1));
   const CUtensorMap mx = map2d(x, D, M, 64, 128);
   const CUtensorMap mw = map2d(w, 64, size_t(NBLK) * 64, 64, 64);
-  run<1, 8, 0>(mx, mw, e0, e1);
-  run<2, 8, 0>(mx, mw, e0, e1);
-  run<4, 8, 0>(mx, mw, e0, e1);
-  run<1, 8, 1>(mx, mw, e0, e1);
-  run<2, 8, 1>(mx, mw, e0, e1);
-  run<4, 8, 1>(mx, mw, e0, e1);
-  run<4, 4, 1>(mx, mw, e0, e1);
+  const CUtensorMap mw2 = map2d(w, 64, size_t(NBLK) * 64, 64, 64);
+  run<1, 8, 1>(mx, mw, mw2, e0, e1);
+  run<1, 6, 1>(mx, mw, mw2, e0, e1);
+  run<1, 6, 1, 0, 1>(mx, mw, mw2, e0, e1);
+  run<1, 5, 1, 0, 1>(mx, mw, mw2, e0, e1);
   return 0;
 }
