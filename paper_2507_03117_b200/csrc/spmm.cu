@@ -77,7 +77,7 @@ static SpmmParams make_params(const EngineCall& c) {
     static int skip = -1;
     if (skip < 0) {
       const char* e = getenv("BLAST_SKIP_EPILOGUE");
-      skip = e ? atoi(e) : 0;
+      skip = (e && e[0] == '1') ? 1 : 0;
     }
     p.skip_epilogue = skip;
   }
@@ -255,10 +255,10 @@ static int pair_stages_override() {
   return v;
 }
 
-template <int B, int NMAT, bool SUM, bool BK, int EPI>
+template <int B, int NMAT, bool SUM, bool BK, int EPI, int OUT_ELT = 0>
 static int launch_pair(const EngineCall& c, cudaStream_t st) {
-  using Cfg = PairCfg<B, NMAT, SUM, BK>;
-  auto kern = spmm_pair_kernel<B, NMAT, SUM, BK, EPI, __nv_bfloat16>;
+  using Cfg = PairCfg<B, NMAT, SUM, BK, OUT_ELT>;
+  auto kern = spmm_pair_kernel<B, NMAT, SUM, BK, EPI, __nv_bfloat16, OUT_ELT>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -287,6 +287,11 @@ static int launch_pair(const EngineCall& c, cudaStream_t st) {
   if (ok) ok = mkW(&mW0, c.w0, c.nnzb0);
   mW1 = mW0;
   if (ok && NMAT > 1) ok = mkW(&mW1, c.w1, c.nnzb1);
+  CUtensorMap mO = mA0;
+  if (ok && OUT_ELT > 0)
+    ok = encode_map_2d(&mO, c.out0, BLAST_BF16, static_cast<uint64_t>(c.n_valid),
+                       static_cast<uint64_t>(c.m), static_cast<uint64_t>(c.ld_out) * 2,
+                       Cfg::OUT_SW / 2, Cfg::BM, Cfg::OUT_SW);
   if (!ok) return BLAST_EINVAL;
   PairParams pp{};
   pp.p = make_params(c);
@@ -297,19 +302,22 @@ static int launch_pair(const EngineCall& c, cudaStream_t st) {
   r = std::max<int64_t>(1, std::min<int64_t>(r, pp.n_pair_tiles));
   pp.tiles_per_item = static_cast<int32_t>(r);
   pp.n_chunks = static_cast<int32_t>(cdiv(pp.n_pair_tiles, r));
-  // Pipeline depth vs resident weights: deep enough to cover the L2 latency
-  // (~1.5 us at load), the remaining shared memory holds resident weight halves.
+  // Pipeline depth vs resident weights: room for ~1.6x the mean stored blocks per line
+  // (so nearly every line is fully resident), then as many panel stages as fit (4..8).
+  const int64_t nnzb_all = c.nnzb0 + (NMAT > 1 ? c.nnzb1 : 0);
+  const int64_t want_res = (16 * nnzb_all + 10 * c.n_lines - 1) / (10 * c.n_lines);
   int stages = pair_stages_override();
-  if (stages <= 0) stages = std::min(Cfg::MAX_STAGES, (120 * 1024) / (Cfg::NA * Cfg::A_TILE) + 1);
-  stages = std::max(2, std::min(stages, std::min(Cfg::MAX_STAGES, Cfg::DATA_BYTES / Cfg::STAGE)));
+  if (stages <= 0)
+    stages = static_cast<int>((Cfg::DATA_BYTES - want_res * Cfg::WH) / Cfg::STAGE);
+  stages = std::max(4, std::min(stages, std::min(8, Cfg::DATA_BYTES / Cfg::STAGE)));
   pp.n_stages = stages;
-  pp.res_cap = (Cfg::DATA_BYTES - stages * Cfg::STAGE) / Cfg::WH;
+  pp.res_cap = std::min<int64_t>(254, (Cfg::DATA_BYTES - stages * Cfg::STAGE) / Cfg::WH);
   if (const char* e = getenv("BLAST_PAIR_RESCAP")) pp.res_cap = std::min(pp.res_cap, atoi(e));
   const int64_t items = static_cast<int64_t>(pp.n_chunks) * c.n_lines;
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(2 * std::min<int64_t>(items, n_pairs));
   dbg_begin(st);
-  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mA0, mA1, mW0, mW1, pp);
+  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mA0, mA1, mW0, mW1, pp);
   const int rc = check_launch("spmm_pair");
   dbg_end("spmm_pair", st, grid);
   return rc;
@@ -318,10 +326,14 @@ static int launch_pair(const EngineCall& c, cudaStream_t st) {
 template <int B>
 static int dispatch_pair_b(const EngineCall& c, cudaStream_t st) {
   if (!c.transposed) {
+    const bool staged = !staged_out_disabled() && !c.accumulate && aligned16(c.out0) &&
+                        (c.ld_out * 2) % 16 == 0;
     if (c.nmat == 1 && c.epi == EPI_STORE && c.act == ACT_NONE && !c.accumulate)
-      return launch_pair<B, 1, false, false, EPI_STORE>(c, st);
+      return staged ? launch_pair<B, 1, false, false, EPI_STORE, 2>(c, st)
+                    : launch_pair<B, 1, false, false, EPI_STORE>(c, st);
     if (c.nmat == 2 && c.epi == EPI_GATED_FWD)
-      return launch_pair<B, 2, false, false, EPI_GATED_FWD>(c, st);
+      return staged ? launch_pair<B, 2, false, false, EPI_GATED_FWD, 2>(c, st)
+                    : launch_pair<B, 2, false, false, EPI_GATED_FWD>(c, st);
   } else {
     if (c.nmat == 1 && c.epi == EPI_STORE)
       return launch_pair<B, 1, false, true, EPI_STORE>(c, st);

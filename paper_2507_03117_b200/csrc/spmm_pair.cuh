@@ -22,7 +22,7 @@
 
 namespace blast {
 
-template <int B, int NMAT, bool SUMACC, bool B_KMAJOR>
+template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0>
 struct PairCfg {
   static constexpr int ELT = 2;
   static constexpr int BM = 128;                          // rows per CTA (M = 256 per pair)
@@ -43,9 +43,15 @@ struct PairCfg {
   static constexpr int WH_ROWS = B_KMAJOR ? B / 2 : B;
   static constexpr int MAX_STAGES = 12;
   static constexpr int STAGE = NA * A_TILE + NMAT * WH;
-  // dynamic shared memory: [1 KiB barriers][n_stages x STAGE][res_cap x WH]
-  static constexpr int SMEM_BYTES = 220 * 1024;
-  static constexpr int DATA_BYTES = SMEM_BYTES - 2048;  // minus barriers and alignment slack
+  // staged output tile (TMA store), double-buffered: see TcCfg
+  static constexpr int OUT_ROWB = B * OUT_ELT;
+  static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
+  static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
+  static constexpr int OUT_TILE = OUT_ELT ? (BM * OUT_ROWB + 1023) / 1024 * 1024 : 0;
+  static constexpr int STAGING = 2 * OUT_TILE;
+  // dynamic shared memory: [1 KiB barriers + meta][staging][n_stages x STAGE][res_cap x WH]
+  static constexpr int SMEM_BYTES = 232448;
+  static constexpr int DATA_BYTES = SMEM_BYTES - 2048 - STAGING;  // stages + resident weights
   static constexpr int NACC = SUMACC ? 1 : NMAT;
   static constexpr int ACC_STRIDE = NACC * B;
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE <= 32    ? 32
@@ -78,12 +84,18 @@ __device__ __forceinline__ uint32_t wh_koff(int ks) {
   return (static_cast<uint32_t>(ks) * 16 * C::WH_SW) >> 4;
 }
 
-template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT>
+// Per-stage recipe written by the producer (see kMeta* in spmm_tc.cuh) plus, per matrix, the
+// resident slot of its weight half (bits 8-15 / 16-23; 0xff = streamed with the panel).
+constexpr uint32_t kPairStreamed = 0xffu;
+
+template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT, int OUT_ELT = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
-spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
+                 const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
                  const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW1,
                  const PairParams pp) {
-  using C = PairCfg<B, NMAT, SUMACC, B_KMAJOR>;
+  using C = PairCfg<B, NMAT, SUMACC, B_KMAJOR, OUT_ELT>;
+  static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
   const SpmmParams& p = pp.p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -96,8 +108,10 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
   uint64_t* wfull = tmem_empty + 2;
   uint64_t* wempty = wfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
-  uint8_t* stages = smem + 1024;               // activation panels (+ streamed weights)
-  uint8_t* res = stages + NST * C::STAGE;      // resident weight halves
+  uint32_t* stage_meta = tmem_slot + 4;          // [MAX_STAGES]
+  uint8_t* staging = smem + 1024;                // [2][OUT_TILE]
+  uint8_t* stages = staging + C::STAGING;        // activation panels (+ streamed weights)
+  uint8_t* res = stages + NST * C::STAGE;        // resident weight halves
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -106,6 +120,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
   const int n_items = pp.n_chunks * p.n_lines;
 
   if (warp == 0 && lane == 0) {
+    if (OUT_ELT) tma_prefetch(&mapO);
     tma_prefetch(&mapA0);
     tma_prefetch(&mapW0);
     if (NMAT > 1) tma_prefetch(&mapW1);
@@ -131,10 +146,17 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   WaitClock wc;
+#ifdef BLAST_WAIT_COUNTERS
   const bool dbg_on = p.dbg != nullptr;
+#else
+  constexpr bool dbg_on = false;
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
+    // Per item (line j, R pair tiles): the line's weight halves go to the resident region
+    // once (as many as fit), then every tile streams its activation panels through the
+    // ring. The first 32 steps of the line stay in registers across the tiles.
     const uint64_t pol_w = policy_evict_last();
     // activation panels are re-read by every line of the same token tile: keep them in L2
     const uint64_t pol_a = policy_evict_last();
@@ -147,12 +169,14 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
       const int t0 = chunk * pp.tiles_per_item;
       const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
       const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
-      // resident weight halves of this line (first RES_CAP blocks in step order)
+      StepCursor first;
+      first.start(p.steps, s0, s1);
+      const int4 first_mine = first.mine;
+      // resident weight halves of this line: its first RCAP blocks in step order
       wc.wait(1, wempty, (it & 1) ^ 1, dbg_on);
       int nres = 0;
       {
-        StepCursor cur;
-        cur.start(p.steps, s0, s1);
+        StepCursor cur = first;
         for (int s = s0; s < s1 && nres < RCAP; ++s) {
           const int4 st = cur.get(s);
           nres += (st.y >= 0 ? 1 : 0);
@@ -163,7 +187,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
       __syncwarp();
       {
         StepCursor cur;
-        cur.start(p.steps, s0, s1);
+        cur.steps = p.steps; cur.end = s1; cur.base = s0; cur.mine = first_mine;
         int r = 0;
         for (int s = s0; s < s1 && r < nres; ++s) {
           const int4 st = cur.get(s);
@@ -192,19 +216,30 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
       }
       for (int t = t0; t < t1; ++t) {
         int rcount = 0;
+        uint32_t init0 = 0, init1 = 0;
         StepCursor cur;
-        cur.start(p.steps, s0, s1);
+        cur.steps = p.steps; cur.end = s1; cur.base = s0; cur.mine = first_mine;
         for (int s = s0; s < s1; ++s) {
           const int4 st = cur.get(s);
           const int kb[2] = {st.y, st.z};
-          bool streamed[2] = {false, false};
+          const bool has0 = kb[0] >= 0, has1 = NMAT > 1 && kb[1] >= 0;
+          // recipe: presence, accumulate flags, resident slot or streamed
+          uint32_t meta = (has0 ? kMetaHas0 : 0u) | (has1 ? kMetaHas1 : 0u);
+          uint32_t slot[2] = {kPairStreamed, kPairStreamed};
           int nstream = 0;
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm) {
             if (kb[mm] < 0) continue;
-            if (rcount < nres) ++rcount;
-            else { streamed[mm] = true; ++nstream; }
+            if (rcount < nres) slot[mm] = static_cast<uint32_t>(rcount);
+            else ++nstream;
+            ++rcount;
           }
+          if (has0) { meta |= init0 ? kMetaAccFirst : 0u; init0 = 1; }
+          if (has1) {
+            if (SUMACC) { meta |= init0 ? kMetaAccSecond : 0u; init0 = 1; }
+            else { meta |= init1 ? kMetaAccSecond : 0u; init1 = 1; }
+          }
+          meta |= (slot[0] << 8) | (slot[1] << 16);
           wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
           if (elect_one()) {
             uint32_t bytes = 0;
@@ -212,6 +247,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
             for (int a = 0; a < C::NA; ++a)
               if (!SUMACC || kb[a] >= 0) bytes += C::BM * C::ROWB;
             bytes += nstream * C::WH;
+            stage_meta[stage] = meta;
             if (rank == 0) mbar_expect_tx(&full[stage], 2u * bytes);
             const uint32_t fb = full0 + stage * 8;
             uint8_t* sbase = stages + stage * C::STAGE;
@@ -227,7 +263,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
             }
 #pragma unroll
             for (int mm = 0; mm < NMAT; ++mm) {
-              if (!streamed[mm]) continue;
+              if (kb[mm] < 0 || slot[mm] != kPairStreamed) continue;
               const CUtensorMap* mw = mm == 0 ? &mapW0 : &mapW1;
               uint8_t* dst = sbase + C::NA * C::A_TILE + mm * C::WH;
 #pragma unroll
@@ -242,12 +278,13 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
             }
           }
           __syncwarp();
-          if (++stage == NST) { stage = 0; phase ^= 1; }
+          if (++stage == static_cast<uint32_t>(NST)) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1 && rank == 0) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
+    // Decodes the producer's per-stage recipe; needs no step list of its own.
     const uint32_t smem0 = smem_u32(stages);
     const uint32_t res0 = smem_u32(res);
     const uint64_t a_desc0 = kmajor_desc<C::SW, C::MMA_K, 2>(smem0, C::BM, 0);
@@ -269,7 +306,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
       const int j = item - chunk * p.n_lines;
       const int t0 = chunk * pp.tiles_per_item;
       const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
-      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      const int n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
       wc.wait(4, wfull, it & 1, dbg_on);
       tc_fence_after();
       for (int t = t0; t < t1; ++t, ++tile_it) {
@@ -277,47 +314,32 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
         wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
         tc_fence_after();
         const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
-        uint32_t init0 = 0, init1 = 0;
-        int rcount = 0;
-        StepCursor cur;
-        cur.start(p.steps, s0, s1);
-        for (int s = s0; s < s1; ++s) {
-          const int4 st = cur.get(s);
-          const int kb[2] = {st.y, st.z};
+        for (int s = 0; s < n_steps; ++s) {
           wc.wait(2, &full[stage], phase, dbg_on);
-          wc.acc[7] += dbg_on;
           tc_fence_after();
-          const uint32_t soff = (stage * C::STAGE) >> 4;
-          int ridx[2] = {-1, -1};
-#pragma unroll
-          for (int mm = 0; mm < NMAT; ++mm) {
-            if (kb[mm] < 0) continue;
-            ridx[mm] = rcount < RCAP ? rcount : -1;
-            ++rcount;
-          }
+          const uint32_t meta = *reinterpret_cast<volatile uint32_t*>(&stage_meta[stage]);
           if (elect_one()) {
+            const uint32_t soff = (stage * C::STAGE) >> 4;
 #pragma unroll
             for (int mm = 0; mm < NMAT; ++mm) {
-              if (kb[mm] < 0) continue;
+              if (!(meta & (mm == 0 ? kMetaHas0 : kMetaHas1))) continue;
               const int acc_i = SUMACC ? 0 : mm;
               const int a_i = SUMACC ? mm : 0;
               const uint32_t d = d_base + acc_i * B;
               const uint64_t ad = a_desc0 + soff + ((a_i * C::A_TILE) >> 4);
-              const uint64_t wd = ridx[mm] >= 0 ? wdesc_res0 + ((ridx[mm] * C::WH) >> 4)
-                                                : wdesc_str0 + soff + ((mm * C::WH) >> 4);
-              const uint32_t init = acc_i == 0 ? init0 : init1;
+              const uint32_t slot = (meta >> (mm == 0 ? 8 : 16)) & 0xffu;
+              const uint64_t wd = slot != kPairStreamed ? wdesc_res0 + ((slot * C::WH) >> 4)
+                                                        : wdesc_str0 + soff + ((mm * C::WH) >> 4);
+              const uint32_t init = (meta & (mm == 0 ? kMetaAccFirst : kMetaAccSecond)) ? 1u : 0u;
 #pragma unroll
               for (int ks = 0; ks < C::KSL; ++ks)
                 mma_f16_pair(d, ad + a_koff(ks), wd + wh_koff<B, B_KMAJOR>(ks), C::IDESC,
                              (init | ks) ? 1u : 0u);
-              if (acc_i == 0) init0 = 1; else init1 = 1;
             }
             mma_commit_pair(&empty[stage]);
           }
           __syncwarp();
-          if (kb[0] >= 0) init0 = 1;
-          if (NMAT > 1 && kb[1] >= 0) { if (SUMACC) init0 = 1; else init1 = 1; }
-          if (++stage == NST) { stage = 0; phase ^= 1; }
+          if (++stage == static_cast<uint32_t>(NST)) { stage = 0; phase ^= 1; }
         }
         if (elect_one()) mma_commit_pair(&tmem_full[as]);
         __syncwarp();
@@ -329,6 +351,8 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
     // ------------------------------------------------------------ epilogue (both CTAs)
     const uint32_t q = warp & 3;
     const int half = static_cast<int>(warp - 4) >> 2;
+    const uint32_t etid = threadIdx.x - 128;
+    const uint64_t pol_out = policy_evict_first();
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
     uint32_t tile_it = 0;
     for (int item = pair; item < n_items; item += n_pairs) {
@@ -341,32 +365,22 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constan
         const uint32_t as = tile_it & 1, use = tile_it >> 1;
         wc.wait(5, &tmem_full[as], use & 1, dbg_on);
         tc_fence_after();
-        const int row = t * 256 + static_cast<int>(rank) * C::BM + static_cast<int>(q * 32 + lane);
-        const bool row_ok = row < p.m;
-        const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
-#pragma unroll 1
-        for (int c = half; c < B / 16; c += 2) {
-          const int col = j * B + c * 16;
-          const int valid = p.n_valid - col;
-          const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
-          float v0[16];
-          tmem_ld16(tbase + c * 16, v0);
-          const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
-          if (!acc0_init) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v0[i] = 0.0f;
-          }
-          float v1[16];
-          if (EPI == EPI_GATED_FWD) tmem_ld16(tbase + B + c * 16, v1);
-          epilogue_chunk<EPI, OutT>(p, v0, v1, flags, row_ok, col, valid, off, vec_ok);
-        }
+        const int row0 = t * 256 + static_cast<int>(rank) * C::BM;
+        uint8_t* stg = staging + (tile_it & 1) * C::OUT_TILE;
+        const uint32_t tacc = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
+        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, row0, j * B, flags, stg, half,
+                                                          q, lane, etid, vec_ok);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           if (rank == 0) mbar_arrive(&tmem_empty[as]);
           else mbar_arrive_cluster(&tmem_empty[as], 0);
         }
+        epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT>(&mapO, stg, row0, j * B, etid, pol_out);
       }
+    }
+    if constexpr (OUT_ELT > 0) {
+      if (etid == 0) bulk_wait_group<0>();
     }
   }
 

@@ -312,13 +312,8 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
         else
           g[i] = gated_fwd(v0[i], v1[i]);
       }
-      if constexpr (STG_SW > 0) {
-        if (p.skip_epilogue >= 6) {  // diagnosis: no staging writes
-          if (g[0] == 1234.5f && g[7] == 1.5f) p.dbg[1] = 1;
-        } else {
-          stage_chunk16<OutT, STG_SW>(stg, trow, tcol, g);
-        }
-      }
+      if constexpr (STG_SW > 0)
+        stage_chunk16<OutT, STG_SW>(stg, trow, tcol, g);
       else
         store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
     }
@@ -342,6 +337,81 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
   }
 }
 
+constexpr int kEpiWarpsT = 8;  // epilogue warps of both engines (named barrier 1)
+
+// ---------------------------------------------------------------- epilogue tile
+// One 128-row output tile of one CTA, shared by the single-CTA and CTA-pair engines.
+// Called by the kEpiWarps epilogue warps after the accumulator's tmem_full wait:
+//   epi_tile_compute  TMEM -> registers -> activation / gating -> out1/out2 stores and
+//                     out0 (staged tile when OUT_SW > 0, else direct stores)
+//   (caller: tcgen05.fence::before_thread_sync + arrive on the accumulator's empty barrier)
+//   epi_tile_store    staged tile -> TMA store (one elected thread)
+// `tacc` is the TMEM address of accumulator 0 for this warp's lane quarter; row0 / col0 are
+// the tile's first output row / column. Staging buffers alternate per tile (`stg`); the TMA
+// store issued from a buffer two tiles ago must have finished reading it.
+template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW>
+__device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t tacc, int row0,
+                                                 int col0, int flags, uint8_t* stg, int half,
+                                                 uint32_t q, uint32_t lane, uint32_t etid,
+                                                 bool vec_ok) {
+  if constexpr (OUT_SW > 0) {
+    if (etid == 0) bulk_wait_group_read<1>();
+    named_bar_sync(1, kEpiWarpsT * 32);
+  }
+  const int trow = static_cast<int>(q * 32 + lane);
+  const int row = row0 + trow;
+  const bool row_ok = row < p.m;
+  constexpr int NCH = B / 16;
+  constexpr bool kTwoAcc = EPI == EPI_GATED_FWD;
+  const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
+  // this warp's 16-column chunks are c = half, half + 2, ...; the TMEM loads of two chunks
+  // (both accumulators when gated) are issued before one wait
+#pragma unroll 1
+  for (int c0 = half; c0 < NCH; c0 += 4) {
+    uint32_t r0[2][16], r1[2][16];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int c = c0 + 2 * k;
+      if (c < NCH) {
+        tmem_ld16_nowait(tacc + c * 16, r0[k]);
+        if (kTwoAcc) tmem_ld16_nowait(tacc + B + c * 16, r1[k]);
+      }
+    }
+    tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int c = c0 + 2 * k;
+      if (c >= NCH) break;
+      const int col = col0 + c * 16;
+      const int valid = p.n_valid - col;
+      const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
+      float v0[16], v1[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        v0[i] = acc0_init ? __uint_as_float(r0[k][i]) : 0.0f;
+        v1[i] = kTwoAcc ? __uint_as_float(r1[k][i]) : 0.0f;
+      }
+      epilogue_chunk<EPI, OutT, OUT_SW>(p, v0, v1, flags, row_ok, col, valid, off, vec_ok, stg,
+                                        trow, c * 16);
+    }
+  }
+}
+template <int OUT_SW, int OUT_NATOM, int OUT_ELT>
+__device__ __forceinline__ void epi_tile_store(const CUtensorMap* mapO, uint8_t* stg, int row0,
+                                               int col0, uint32_t etid, uint64_t pol_out) {
+  if constexpr (OUT_SW > 0) {
+    fence_proxy_async_smem();
+    named_bar_sync(1, kEpiWarpsT * 32);
+    if (etid == 0) {
+#pragma unroll
+      for (int a = 0; a < OUT_NATOM; ++a)
+        tma_store_2d_hint(mapO, stg + a * (128 * OUT_SW), col0 + a * (OUT_SW / OUT_ELT), row0,
+                          pol_out);
+      bulk_commit_group();
+    }
+  }
+}
+
 // per-stage MMA recipe bits (producer -> MMA warp through shared memory)
 constexpr uint32_t kMetaHas0 = 1u;        // block of matrix 0 in this stage
 constexpr uint32_t kMetaHas1 = 2u;        // block of matrix 1 in this stage
@@ -352,7 +422,7 @@ constexpr uint32_t kMetaAccSecond = 16u;  // second MMA group accumulates
 // 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (two warps per TMEM lane quarter, splitting the 16-column chunks).
 constexpr int kTcThreads = 384;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = kEpiWarpsT;
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
           int OUT_ELT = 0>
@@ -622,94 +692,20 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       const int flags = __ldg(&p.line_flags[j]);
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
-      if (p.skip_epilogue == 3) {  // diagnosis: TMEM reads + gating math, no stores
-        uint32_t r0[16], r1[16];
-        float accv = 0.0f;
-#pragma unroll 1
-        for (int c = half; c < B / 16; c += 2) {
-          const uint32_t tb = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + c * 16;
-          tmem_ld16_nowait(tb, r0);
-          tmem_ld16_nowait(tb + B, r1);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            accv += gated_fwd_fast(__uint_as_float(r0[i]), __uint_as_float(r1[i]));
-        }
-        if (accv == 1234.5f) p.dbg[0] = 1;
-      }
-      if (p.skip_epilogue == 2) {  // diagnosis: TMEM reads only
-        uint32_t r0[16];
-#pragma unroll 1
-        for (int c = half; c < 2 * B / 16; c += 2) {
-          tmem_ld16_nowait(tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + c * 16, r0);
-          tmem_wait_ld();
-          if (r0[0] == 0x7fc00001u && r0[15] == 0x7fc00001u) p.dbg[0] = 1;  // keep the loads
-        }
-      }
-      if (p.skip_epilogue && p.skip_epilogue < 4) {
+      if (p.skip_epilogue) {  // diagnosis: release the accumulator unread
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[as]);
         continue;
       }
       uint8_t* stg = staging + (it & 1) * C::OUT_TILE;
-      if constexpr (OUT_ELT > 0) {
-        // the TMA store issued two items ago from this buffer must have read it
-        if (etid == 0) bulk_wait_group_read<1>();
-        if (p.skip_epilogue != 7) named_bar_sync(1, kEpiWarps * 32);
-      }
-      const int trow = static_cast<int>(q * 32 + lane);
-      const int row = t * C::BM + trow;
-      const bool row_ok = row < p.m;
-      const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
-      // this warp's 16-column chunks are c = half, half + 2, ...; the TMEM loads of two
-      // chunks (both accumulators when gated) are issued before one wait
-      constexpr int NCH = B / 16;
-      constexpr bool kTwoAcc = EPI == EPI_GATED_FWD;
-      const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
-#pragma unroll 1
-      for (int c0 = half; c0 < NCH; c0 += 4) {
-        uint32_t r0[2][16], r1[2][16];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int c = c0 + 2 * k;
-          if (c < NCH) {
-            tmem_ld16_nowait(tbase + c * 16, r0[k]);
-            if (kTwoAcc) tmem_ld16_nowait(tbase + B + c * 16, r1[k]);
-          }
-        }
-        tmem_wait_ld();
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int c = c0 + 2 * k;
-          if (c >= NCH) break;
-          const int col = j * B + c * 16;
-          const int valid = p.n_valid - col;
-          const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
-          float v0[16], v1[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            v0[i] = acc0_init ? __uint_as_float(r0[k][i]) : 0.0f;
-            v1[i] = kTwoAcc ? __uint_as_float(r1[k][i]) : 0.0f;
-          }
-          epilogue_chunk<EPI, OutT, C::OUT_SW>(p, v0, v1, flags, row_ok, col, valid, off, vec_ok,
-                                               stg, trow, c * 16);
-        }
-      }
+      const uint32_t tacc = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
+      epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, t * C::BM, j * B, flags, stg,
+                                                        half, q, lane, etid, vec_ok);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[as]);
-      if constexpr (OUT_ELT > 0) {
-        if (p.skip_epilogue < 5) fence_proxy_async_smem();  // 5..7: diagnosis, no fence (no store)
-        if (p.skip_epilogue != 7) named_bar_sync(1, kEpiWarps * 32);
-        if (etid == 0 && p.skip_epilogue < 4) {  // 4..6: diagnosis, never stored
-#pragma unroll
-          for (int a = 0; a < C::OUT_NATOM; ++a)
-            tma_store_2d_hint(&mapO, stg + a * (C::BM * C::OUT_SW), j * B + a * (C::OUT_SW / OUT_ELT),
-                              t * C::BM, pol_out);
-          bulk_commit_group();
-        }
-      }
+      epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT>(&mapO, stg, t * C::BM, j * B, etid, pol_out);
     }
     if constexpr (OUT_ELT > 0) {
       if (etid == 0) bulk_wait_group<0>();

@@ -366,6 +366,69 @@ __global__ void __launch_bounds__(128, 1) ldg_sttm_kernel(const uint8_t* gsrc, s
   if (warp == 0) { tc_fence_after(); tmem_dealloc(tbase, 64); }
 }
 
+// ----------------------------------------------------------------------------- P7
+// cta_group::2 SS-MMA issue rate: M=256 (128 rows per CTA), N (B split N/2 per CTA)
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) pair_rate_kernel(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 0) { tmem_alloc_pair(&tslot, 512); tmem_relinquish_pair(); }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  const uint32_t a0 = smem_u32(smem), b0 = a0 + 16384;
+  const uint32_t idesc = make_idesc(256, N, 1u, 0u, 0u);
+  if (warp == 1 && rank == 0) {
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t bd = make_sdesc(b0 + ks * 32, 16, 1024, 2);
+          const uint64_t ad = make_sdesc(a0 + ks * 32, 16, 1024, 2);
+          mma_f16_pair(tbase, ad, bd, idesc, (i | ks) ? 1u : 0u);
+        }
+        if ((i & 63) == 63) mma_commit_pair(&bar);
+      }
+      __syncwarp();
+      if ((i & 63) == 63) mbar_wait(&bar, (i >> 6) & 1);
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) out[blockIdx.x / 2] = t1 - t0;
+  } else if (warp == 1 && rank == 1) {
+    for (int i = 63; i < iters; i += 64) mbar_wait(&bar, (i >> 6) & 1);
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc_pair(tbase, 512); }
+}
+
+template <int N>
+void run_pair_rate(int iters) {
+  auto k = pair_rate_kernel<N>;
+  const int smem = 16384 + 32768 + 2048;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  unsigned long long* d;
+  CK(cudaMalloc(&d, 74 * 8));
+  k<<<148, 128, smem>>>(iters, d);
+  CK(cudaDeviceSynchronize());
+  unsigned long long h[74];
+  CK(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  double avg = 0;
+  for (int i = 0; i < 74; ++i) avg += h[i];
+  avg /= 74;
+  const double per_mma = avg / (iters * 4.0);
+  printf("P7 pair SS M=256 N=%3d: %6.1f cyc/MMA -> per SM %.1f cyc per 128x%dx16 (single-CTA SS N=%d: see P1)\n", N,
+         per_mma, per_mma, N, N);
+  CK(cudaFree(d));
+}
+
 int main() {
   int clk_khz = 0;
   CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
@@ -375,6 +438,9 @@ int main() {
   CK(cudaMalloc(&g, gbytes));
   CK(cudaMemset(g, 1, gbytes));
 
+  run_pair_rate<64>(4000);
+  run_pair_rate<128>(4000);
+  run_pair_rate<256>(2000);
   run_ts_check();
   run_rate<64, 1, 0, false>("P1 SS", 4000, g, gbytes);
   run_rate<64, 2, 0, false>("P1 SS", 4000, g, gbytes);
