@@ -429,6 +429,171 @@ void run_pair_rate(int iters) {
   CK(cudaFree(d));
 }
 
+
+__device__ __forceinline__ bool mbar_test(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_hint(uint32_t addr, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(ok) : "r"(addr), "r"(parity), "r"(ns) : "memory");
+  return ok != 0;
+}
+template <int W>
+__device__ __forceinline__ void wait_v(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (W == 0) { while (!mbar_try_wait(a, parity)) {} }
+  else if (W == 1) { while (!mbar_test(a, parity)) {} }
+  else { while (!mbar_try_hint(a, parity, 20)) {} }
+}
+// ----------------------------------------------------------------------------- P8
+// Per-step synchronisation overhead of the engine's MMA loop without TMA:
+// MODE 0: 4 MMAs (N=64) + commit to a ring of 8 mbarriers per step;
+// MODE 1: MODE 0 + wait on a "full" mbarrier that a helper warp arrives on 8 steps ahead,
+//         and tcgen05.fence::after_thread_sync (the engine's loop shape)
+// MODE 2: MODE 1 but two steps (8 MMAs, 2 commits) per wait
+template <int MODE, int W = 0, int S = 8>
+__global__ void __launch_bounds__(128, 1) sync_rate_kernel(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t emptyb[16], fullb[16];
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 16; ++i) { mbar_init(&emptyb[i], 1); mbar_init(&fullb[i], 1); }
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  const uint32_t a0 = smem_u32(smem), b0 = a0 + 16384;
+  const uint32_t idesc = make_idesc(128, 64, 1u, 0u, 0u);
+  const uint64_t ad0 = make_sdesc(a0, 16, 1024, 2), bd0 = make_sdesc(b0, 16, 1024, 2);
+  if (warp == 1 && MODE == 7) {
+    // single-lane loop; the wait for step k+1 sits between step k's 2nd and 3rd MMA
+    const long long t0 = clock64();
+    if (lane_id() == 0) {
+      uint32_t stage = 0, phase = 0;
+      wait_v<0>(&fullb[0], 0);
+      for (int i = 0; i < iters; ++i) {
+        const uint32_t ns = stage + 1 == S ? 0 : stage + 1;
+        const uint32_t nph = stage + 1 == S ? phase ^ 1 : phase;
+        tc_fence_after();
+        mma_f16(tbase + (i & 1) * 64, ad0, bd0, idesc, 0u);
+        mma_f16(tbase + (i & 1) * 64, ad0 + 2, bd0 + 2, idesc, 1u);
+        if (i + 1 < iters) wait_v<0>(&fullb[ns], nph);
+        mma_f16(tbase + (i & 1) * 64, ad0 + 4, bd0 + 4, idesc, 1u);
+        mma_f16(tbase + (i & 1) * 64, ad0 + 6, bd0 + 6, idesc, 1u);
+        mma_commit(&emptyb[stage]);
+        stage = ns;
+        phase = nph;
+      }
+    }
+    __syncwarp();
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) out[blockIdx.x] = t1 - t0;
+  } else if (warp == 1 && MODE == 5) {
+    // look-ahead: test full[k+1] before issuing step k's MMAs, block only if it failed
+    const long long t0 = clock64();
+    uint32_t stage = 0, phase = 0;
+    wait_v<0>(&fullb[0], 0);
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t ns = stage + 1 == S ? 0 : stage + 1;
+      const uint32_t nph = stage + 1 == S ? phase ^ 1 : phase;
+      const bool ready = i + 1 >= iters || mbar_test(smem_u32(&fullb[ns]), nph);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_f16(tbase + (i & 1) * 64, ad0 + ks * 2, bd0 + ks * 2, idesc, ks ? 1u : 0u);
+        mma_commit(&emptyb[stage]);
+      }
+      __syncwarp();
+      if (!ready) wait_v<0>(&fullb[ns], nph);
+      stage = ns;
+      phase = nph;
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) out[blockIdx.x] = t1 - t0;
+  } else if (warp == 1) {
+    const long long t0 = clock64();
+    uint32_t stage = 0, phase = 0;
+    const int per = MODE == 2 ? 2 : 1;
+    long long tw = 0, tm = 0;
+    for (int i = 0; i < iters; i += per) {
+      const long long a = clock64();
+      if (MODE >= 1 && MODE != 4 && MODE != 6) {
+        wait_v<W>(&fullb[stage], phase);
+        if (MODE == 2) wait_v<W>(&fullb[stage + 1], phase);
+      }
+      if (MODE == 1 || MODE == 2 || MODE == 4) tc_fence_after();
+      const long long b = clock64();
+      if (elect_one()) {
+        for (int k = 0; k < per; ++k) {
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            mma_f16(tbase + ((i + k) & 1) * 64, ad0 + ks * 2, bd0 + ks * 2, idesc, ks ? 1u : 0u);
+          mma_commit(&emptyb[stage + k]);
+        }
+      }
+      __syncwarp();
+      const long long c = clock64();
+      tw += b - a;
+      tm += c - b;
+      stage += per;
+      if (stage == S) { stage = 0; phase ^= 1; }
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) {
+      out[blockIdx.x] = t1 - t0;
+      if (blockIdx.x == 0) printf("   mode %d: per step wait+fence %.1f, mma issue+commit %.1f cycles\n", MODE,
+                                  double(tw) * per / iters, double(tm) * per / iters);
+    }
+  } else if (warp == 2 && MODE == 6) {
+    // observer only: waits on every empty phase, arrives nowhere (MMA warp runs mode 0)
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      wait_v<0>(&emptyb[stage], phase);
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 2 && MODE >= 1 && MODE != 4) {
+    // "producer": arrive full[s] once the MMAs that used stage s (8 steps ago) are done
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      if (i >= S) wait_v<W>(&emptyb[stage], phase ^ 1);
+      if (elect_one()) mbar_arrive(&fullb[stage]);
+      __syncwarp();
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tbase, 512); }
+}
+
+template <int MODE, int W = 0, int S = 8>
+void run_sync_rate(int iters) {
+  auto k = sync_rate_kernel<MODE, W, S>;
+  const int smem = 16384 + 32768 + 2048;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  unsigned long long* d;
+  CK(cudaMalloc(&d, 148 * 8));
+  k<<<148, 128, smem>>>(iters, d);
+  CK(cudaDeviceSynchronize());
+  unsigned long long h[148];
+  CK(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  avg /= 148;
+  printf("P8 sync mode %d wait %d stages %d: %.1f cycles per step (4 x SS N=64 MMAs)\n", MODE, W, S, avg / iters);
+  CK(cudaFree(d));
+}
+
 int main() {
   int clk_khz = 0;
   CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
@@ -437,6 +602,10 @@ int main() {
   uint8_t* g;
   CK(cudaMalloc(&g, gbytes));
   CK(cudaMemset(g, 1, gbytes));
+
+  run_sync_rate<0>(4000);
+  run_sync_rate<1>(4000);
+  run_sync_rate<2>(4000);
 
   run_pair_rate<64>(4000);
   run_pair_rate<128>(4000);
