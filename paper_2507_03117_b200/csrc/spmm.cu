@@ -101,10 +101,10 @@ static SpmmParams make_params(const EngineCall& c) {
 }
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
-          int OUT_ELT = 0>
+          int OUT_ELT = 0, int TM = 1>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
-  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT>;
-  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT>;
+  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM>;
+  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -116,7 +116,7 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   CUtensorMap mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo;
   auto mkA = [&](CUtensorMap* mp, const void* ptr) {
     return encode_map_2d(mp, ptr, dt, static_cast<uint64_t>(c.a_cols), static_cast<uint64_t>(c.m),
-                         static_cast<uint64_t>(c.a_cols) * ELT, Cfg::SWE, Cfg::BM, Cfg::SW);
+                         static_cast<uint64_t>(c.a_cols) * ELT, Cfg::SWE, Cfg::TROWS, Cfg::SW);
   };
   auto mkW = [&](CUtensorMap* mp, const void* ptr, int64_t nnzb) {
     if (ptr == nullptr || nnzb <= 0) {
@@ -154,7 +154,8 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
                        static_cast<uint64_t>(c.ld_out) * OUT_ELT, Cfg::OUT_SW / (OUT_ELT ? OUT_ELT : 1),
                        Cfg::BM, Cfg::OUT_SW);
   if (!ok) return BLAST_EINVAL;
-  const SpmmParams p = make_params(c);
+  SpmmParams p = make_params(c);
+  p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
   const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
@@ -189,17 +190,28 @@ static bool staged_out_disabled() {
   }
   return v == 1;
 }
-// >= 3 pipeline stages next to the double-buffered bf16 output staging (TcCfg arithmetic)
-template <int B, int ELT, int NPASS, int NMAT, bool SUM>
+// >= 3 pipeline stages next to the double-buffered bf16 output staging (TcCfg arithmetic),
+// and (TM = 2) both token halves' accumulators double-buffered in TMEM
+template <int B, int ELT, int NPASS, int NMAT, bool SUM, int TM = 1>
 constexpr bool staged_fits() {
   if (ELT != 2 || NPASS != 1) return false;
+  if (2 * TM * (SUM ? 1 : NMAT) * B > 512) return false;
   constexpr int rowb = B * ELT;
-  constexpr int a_tile = (128 * rowb + 1023) / 1024 * 1024;
+  constexpr int a_tile = (128 * TM * rowb + 1023) / 1024 * 1024;
   constexpr int b_tile = (B * rowb + 1023) / 1024 * 1024;
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
   constexpr int staging = 2 * ((128 * B * 2 + 1023) / 1024 * 1024);
   return (232448 - 1024 - 512 - staging) / stage >= 3;
+}
+// 256-token items (TcCfg TM = 2) for the forward products; BLAST_WIDE_TILES=0 disables.
+static bool wide_tiles() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_WIDE_TILES");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 template <int B, int ELT, int NPASS, int NMAT, bool SUM>
 static bool use_staged(const EngineCall& c) {
@@ -214,6 +226,9 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
   if (!c.transposed) {
     if (c.nmat == 1 && c.epi == EPI_STORE) {
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>()) {
+        if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2>())
+          if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles())
+            return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
           if (use_staged<B, ELT, NPASS, 1, false>(c))
             return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
@@ -221,6 +236,9 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       }
     } else if (c.nmat == 2 && c.epi == EPI_GATED_FWD) {
       if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
+        if constexpr (staged_fits<B, ELT, NPASS, 2, false, 2>())
+          if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
+            return launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 2, false>())
           if (use_staged<B, ELT, NPASS, 2, false>(c))
             return launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO>(c, a0lo, a1lo, st);

@@ -112,9 +112,14 @@ struct StepCursor {
 
 // OUT_ELT > 0: out0 is staged in shared memory (double-buffered, swizzled) and
 // written by TMA stores (whole 128-byte lines) instead of per-thread row-strided stores.
-template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0>
+// TM = 2: an item covers 2 x 128 tokens; every stage carries a 256-row activation panel,
+// its weight block(s) are loaded once for both halves, and each half accumulates into its
+// own TMEM columns (twice the MMAs per pipeline round trip, half the weight traffic).
+template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0,
+          int TM = 1>
 struct TcCfg {
-  static constexpr int BM = 128;
+  static constexpr int BM = 128;                          // rows per MMA / per output tile
+  static constexpr int TROWS = BM * TM;                   // token rows per item
   static constexpr int ROWB = B * ELT;                    // bytes of one block row
   static constexpr int SW = ROWB < 128 ? ROWB : 128;      // swizzle span
   static constexpr int SWE = SW / ELT;                    // elements per swizzle row
@@ -124,7 +129,7 @@ struct TcCfg {
   static constexpr int NCOPY = NPASS == 3 ? 2 : 1;        // hi / lo operand copies
   static constexpr int NA = SUMACC ? NMAT : 1;            // distinct A panels per step
   static constexpr int round1k(int x) { return (x + 1023) / 1024 * 1024; }
-  static constexpr int A_TILE = round1k(BM * ROWB);
+  static constexpr int A_TILE = round1k(TROWS * ROWB);
   static constexpr int B_TILE = round1k(B * ROWB);
   static constexpr int STAGE = NA * NCOPY * A_TILE + NMAT * NCOPY * B_TILE;
   static constexpr int OUT_ROWB = B * OUT_ELT;                          // bytes of an output tile row
@@ -137,7 +142,8 @@ struct TcCfg {
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int NACC = SUMACC ? 1 : NMAT;
-  static constexpr int ACC_STRIDE = NACC * B;             // TMEM columns per accumulator stage
+  static constexpr int HALF_ACC = NACC * B;               // TMEM columns per 128-row half
+  static constexpr int ACC_STRIDE = TM * HALF_ACC;        // TMEM columns per accumulator stage
   static constexpr int TMEM_COLS_RAW = 2 * ACC_STRIDE;
   static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32    ? 32
                                    : TMEM_COLS_RAW <= 64  ? 64
@@ -154,6 +160,7 @@ struct TcCfg {
   static_assert(TMEM_COLS_RAW <= 512, "accumulators exceed TMEM");
   static_assert(ROWB % SW == 0, "row must be whole swizzle atoms");
   static_assert(OUT_ELT == 0 || (OUT_ROWB >= 32 && OUT_ROWB % (OUT_SW ? OUT_SW : 1) == 0), "staged output rows");
+  static_assert(TM == 1 || TM == 2, "token multiplier");
 };
 
 // Write 16 consecutive output values of tile row `row` starting at tile column `col`
@@ -425,7 +432,7 @@ constexpr int kTcThreads = 384;
 constexpr int kEpiWarps = kEpiWarpsT;
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
-          int OUT_ELT = 0>
+          int OUT_ELT = 0, int TM = 1>
 __global__ void __launch_bounds__(kTcThreads, 1)
 spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
                const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
@@ -433,7 +440,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
                const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW0lo,
                const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW1lo,
                const SpmmParams p) {
-  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT>;
+  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM>;
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -542,7 +549,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
           uint32_t bytes = 0;
 #pragma unroll
           for (int a = 0; a < C::NA; ++a)
-            if (!SUMACC || kb[a] >= 0) bytes += C::NCOPY * (C::BM * C::ROWB);
+            if (!SUMACC || kb[a] >= 0) bytes += C::NCOPY * (C::TROWS * C::ROWB);
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm)
             if (kb[mm] >= 0) bytes += C::NCOPY * (B * C::ROWB);
@@ -559,8 +566,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
               uint8_t* dst = sbase + (a * C::NCOPY + c) * C::A_TILE;
 #pragma unroll
               for (int at = 0; at < C::NATOM; ++at)
-                tma_load_2d(dst + at * C::BM * C::SW, c == 0 ? mh : ml, &full[stage],
-                            st.x * B + at * C::SWE, t * C::BM);
+                tma_load_2d(dst + at * C::TROWS * C::SW, c == 0 ? mh : ml, &full[stage],
+                            st.x * B + at * C::SWE, t * C::TROWS);
             }
           }
 #pragma unroll
@@ -587,7 +594,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
     // Descriptors are built once for stage 0 and advanced by adding byte offsets
     // >> 4 to the start-address field (no carry: shared addresses < 2^18).
     const uint32_t smem0 = smem_u32(smem);
-    const uint64_t a_desc0 = kmajor_desc<C::SW, C::MMA_K, ELT>(smem0, C::BM, 0);
+    const uint64_t a_desc0 = kmajor_desc<C::SW, C::MMA_K, ELT>(smem0, C::TROWS, 0);
     const uint32_t b_off = C::NA * C::NCOPY * C::A_TILE;
     const uint64_t b_desc0 = B_KMAJOR ? kmajor_desc<C::SW, C::MMA_K, ELT>(smem0 + b_off, B, 0)
                                       : mnmajor_desc<C::SW, C::MMA_K, B>(smem0 + b_off, 0);
@@ -602,7 +609,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
     // per-K-slice descriptor increments (in 16-byte units)
     auto a_koff = [](int ks) -> uint32_t {
       const uint32_t byte_k = static_cast<uint32_t>(ks) * C::MMA_K * ELT;
-      return ((byte_k / C::SW) * C::BM * C::SW + (byte_k % C::SW)) >> 4;
+      return ((byte_k / C::SW) * C::TROWS * C::SW + (byte_k % C::SW)) >> 4;
     };
     auto b_koff = [](int ks) -> uint32_t {
       if (B_KMAJOR) {
@@ -631,38 +638,44 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
         const uint32_t meta = *reinterpret_cast<volatile uint32_t*>(&stage_meta[stage]);
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
-          const uint64_t ad = a_desc0 + soff;
           const uint64_t bd = b_desc0 + soff;
-          if (kMerge && (meta & kMetaMerged)) {
-            const uint32_t acc = (meta & kMetaAccFirst) ? 1u : 0u;
 #pragma unroll
-            for (int ks = 0; ks < C::KSL; ++ks)
-              mma_f16(d_base, ad + a_koff(ks), b_desc0_merged + soff + b_koff(ks), kIdescMerged,
-                      (acc | ks) ? 1u : 0u);
-          } else {
+          for (int h = 0; h < TM; ++h) {
+            // half h: rows [h*128, h*128+128) of the panel, its own accumulator columns
+            const uint64_t ad = a_desc0 + soff + ((h * C::BM * C::SW) >> 4);
+            const uint32_t dh = d_base + h * C::HALF_ACC;
+            if (kMerge && (meta & kMetaMerged)) {
+              const uint32_t acc = (meta & kMetaAccFirst) ? 1u : 0u;
 #pragma unroll
-            for (int mm = 0; mm < NMAT; ++mm) {
-              if (!(meta & (mm == 0 ? kMetaHas0 : kMetaHas1))) continue;
-              const int acc_i = SUMACC ? 0 : mm;
-              const int a_i = SUMACC ? mm : 0;
-              const uint32_t d = d_base + acc_i * B;
-              const uint64_t a_hi = ad + ((a_i * C::NCOPY * C::A_TILE) >> 4);
-              const uint64_t a_lo = a_hi + (C::A_TILE >> 4);
-              const uint64_t b_hi = bd + ((mm * C::NCOPY * C::B_TILE) >> 4);
-              const uint64_t b_lo = b_hi + (C::B_TILE >> 4);
-              const uint32_t init = (meta & (mm == 0 ? kMetaAccFirst : kMetaAccSecond)) ? 1u : 0u;
+              for (int ks = 0; ks < C::KSL; ++ks)
+                mma_f16(dh, ad + a_koff(ks), b_desc0_merged + soff + b_koff(ks), kIdescMerged,
+                        (acc | ks) ? 1u : 0u);
+            } else {
 #pragma unroll
-              for (int ks = 0; ks < C::KSL; ++ks) {
-                const uint32_t acc_flag = (init | ks) ? 1u : 0u;
-                if constexpr (NPASS == 3) {
-                  // small cross terms first, then the hi*hi product
-                  mma_tf32(d, a_lo + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
-                  mma_tf32(d, a_hi + a_koff(ks), b_lo + b_koff(ks), C::IDESC, 1u);
-                  mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, 1u);
-                } else if constexpr (ELT == 4) {
-                  mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
-                } else {
-                  mma_f16(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
+              for (int mm = 0; mm < NMAT; ++mm) {
+                if (!(meta & (mm == 0 ? kMetaHas0 : kMetaHas1))) continue;
+                const int acc_i = SUMACC ? 0 : mm;
+                const int a_i = SUMACC ? mm : 0;
+                const uint32_t d = dh + acc_i * B;
+                const uint64_t a_hi = ad + ((a_i * C::NCOPY * C::A_TILE) >> 4);
+                const uint64_t a_lo = a_hi + (C::A_TILE >> 4);
+                const uint64_t b_hi = bd + ((mm * C::NCOPY * C::B_TILE) >> 4);
+                const uint64_t b_lo = b_hi + (C::B_TILE >> 4);
+                const uint32_t init =
+                    (meta & (mm == 0 ? kMetaAccFirst : kMetaAccSecond)) ? 1u : 0u;
+#pragma unroll
+                for (int ks = 0; ks < C::KSL; ++ks) {
+                  const uint32_t acc_flag = (init | ks) ? 1u : 0u;
+                  if constexpr (NPASS == 3) {
+                    // small cross terms first, then the hi*hi product
+                    mma_tf32(d, a_lo + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
+                    mma_tf32(d, a_hi + a_koff(ks), b_lo + b_koff(ks), C::IDESC, 1u);
+                    mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, 1u);
+                  } else if constexpr (ELT == 4) {
+                    mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
+                  } else {
+                    mma_f16(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
+                  }
                 }
               }
             }
@@ -698,14 +711,21 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
         if (lane == 0) mbar_arrive(&tmem_empty[as]);
         continue;
       }
-      uint8_t* stg = staging + (it & 1) * C::OUT_TILE;
-      const uint32_t tacc = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
-      epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, t * C::BM, j * B, flags, stg,
-                                                        half, q, lane, etid, vec_ok);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[as]);
-      epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT>(&mapO, stg, t * C::BM, j * B, etid, pol_out);
+#pragma unroll
+      for (int h = 0; h < TM; ++h) {
+        uint8_t* stg = staging + ((it * TM + h) & 1) * C::OUT_TILE;
+        const uint32_t tacc =
+            tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
+        const int row0 = t * C::TROWS + h * C::BM;
+        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, row0, j * B, flags, stg, half,
+                                                          q, lane, etid, vec_ok);
+        if (h == TM - 1) {  // every TMEM read of this accumulator stage is done
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tmem_empty[as]);
+        }
+        epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT>(&mapO, stg, row0, j * B, etid, pol_out);
+      }
     }
     if constexpr (OUT_ELT > 0) {
       if (etid == 0) bulk_wait_group<0>();
