@@ -474,7 +474,65 @@ __global__ void __launch_bounds__(128, 1) sync_rate_kernel(int iters, unsigned l
   const uint32_t a0 = smem_u32(smem), b0 = a0 + 16384;
   const uint32_t idesc = make_idesc(128, 64, 1u, 0u, 0u);
   const uint64_t ad0 = make_sdesc(a0, 16, 1024, 2), bd0 = make_sdesc(b0, 16, 1024, 2);
-  if (warp == 1 && MODE == 7) {
+  __shared__ volatile int ready_count;
+  if (threadIdx.x == 0) ready_count = 0;
+  __syncthreads();
+  if (warp == 1 && MODE == 9) {
+    // the MMA warp never waits on an mbarrier: warp 3 waits on full[] and publishes a
+    // counter in shared memory that the MMA warp polls
+    const long long t0 = clock64();
+    uint32_t stage = 0;
+    for (int i = 0; i < iters; ++i) {
+      while (ready_count <= i) {
+      }
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_f16(tbase + (i & 1) * 64, ad0 + ks * 2, bd0 + ks * 2, idesc, ks ? 1u : 0u);
+        mma_commit(&emptyb[stage]);
+      }
+      __syncwarp();
+      if (++stage == S) stage = 0;
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) out[blockIdx.x] = t1 - t0;
+  } else if (warp == 3 && MODE == 9) {
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      wait_v<0>(&fullb[stage], phase);
+      if (lane_id() == 0) ready_count = i + 1;
+      __syncwarp();
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 1 && MODE == 8) {
+    // warp-uniform; the wait for step k+1 sits before step k's last MMA
+    const long long t0 = clock64();
+    uint32_t stage = 0, phase = 0;
+    wait_v<0>(&fullb[0], 0);
+    tc_fence_after();
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t ns = stage + 1 == S ? 0 : stage + 1;
+      const uint32_t nph = stage + 1 == S ? phase ^ 1 : phase;
+      if (elect_one()) {
+        mma_f16(tbase + (i & 1) * 64, ad0, bd0, idesc, 0u);
+        mma_f16(tbase + (i & 1) * 64, ad0 + 2, bd0 + 2, idesc, 1u);
+        mma_f16(tbase + (i & 1) * 64, ad0 + 4, bd0 + 4, idesc, 1u);
+      }
+      __syncwarp();
+      if (i + 1 < iters) wait_v<0>(&fullb[ns], nph);
+      tc_fence_after();
+      if (elect_one()) {
+        mma_f16(tbase + (i & 1) * 64, ad0 + 6, bd0 + 6, idesc, 1u);
+        mma_commit(&emptyb[stage]);
+      }
+      __syncwarp();
+      stage = ns;
+      phase = nph;
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) out[blockIdx.x] = t1 - t0;
+  } else if (warp == 1 && MODE == 7) {
     // single-lane loop; the wait for step k+1 sits between step k's 2nd and 3rd MMA
     const long long t0 = clock64();
     if (lane_id() == 0) {
@@ -606,6 +664,8 @@ int main() {
   run_sync_rate<0>(4000);
   run_sync_rate<1>(4000);
   run_sync_rate<2>(4000);
+  run_sync_rate<9, 0, 8>(4000);
+  run_sync_rate<9, 0, 4>(4000);
 
   run_pair_rate<64>(4000);
   run_pair_rate<128>(4000);
