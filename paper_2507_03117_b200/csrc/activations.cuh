@@ -67,6 +67,45 @@ __device__ __forceinline__ float apply_act_grad(float x, int act) {
     default: return 1.0f;
   }
 }
+// bf16-output variants (far below bf16 rounding, the 2e-2 bf16 bar): tanh.approx.f32 and
+// ex2.approx instead of the accurate libm forms; the fp32 paths keep the forms above.
+__device__ __forceinline__ float tanh_approx_f32(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float apply_act_fast(float x, int act) {
+  switch (act) {
+    case ACT_RELU: return act_relu(x);
+    case ACT_GELU: {
+      const float u = 0.7978845834732056f * fmaf(0.044714998453855515f * x, x * x, x);
+      const float h = 0.5f * x;
+      return fmaf(h, tanh_approx_f32(u), h);
+    }
+    case ACT_SILU: {
+      const float h = 0.5f * x;
+      return fmaf(h, tanh_approx_f32(h), h);
+    }
+    default: return x;
+  }
+}
+__device__ __forceinline__ float apply_act_grad_fast(float x, int act) {
+  switch (act) {
+    case ACT_RELU: return x > 0.0f ? 1.0f : 0.0f;
+    case ACT_SILU: {
+      const float s = fmaf(0.5f, tanh_approx_f32(0.5f * x), 0.5f);  // sigmoid(x)
+      return s * fmaf(x, 1.0f - s, 1.0f);
+    }
+    case ACT_GELU: {
+      const float c = 0.7978845834732056f, a = 0.044714998453855515f;
+      const float x2 = x * x;
+      const float t = tanh_approx_f32(c * fmaf(a * x, x2, x));
+      const float du = c * fmaf(3.0f * a, x2, 1.0f);
+      return fmaf(0.5f * x * fmaf(-t, t, 1.0f), du, fmaf(0.5f, t, 0.5f));
+    }
+    default: return 1.0f;
+  }
+}
 // g = (a * sigmoid(a)) * b
 __device__ __forceinline__ float gated_fwd(float a, float b) {
   return __fmul_rn(__fmul_rn(a, act_sigmoid(a)), b);

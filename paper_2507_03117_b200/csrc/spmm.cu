@@ -217,7 +217,8 @@ template <int B, int ELT, int NPASS, int NMAT, bool SUM>
 static bool use_staged(const EngineCall& c) {
   if (!staged_fits<B, ELT, NPASS, NMAT, SUM>() || staged_out_disabled()) return false;
   if (c.accumulate || !aligned16(c.out0) || (c.ld_out * 2) % 16 != 0) return false;
-  return c.epi == EPI_STORE || c.epi == EPI_GATED_FWD;
+  // EPI_GATED_BWD: only the single-output form (y = (x W^T) * act'(pre)) is staged
+  return c.epi == EPI_STORE || c.epi == EPI_GATED_FWD || (c.epi == EPI_GATED_BWD && !c.in1);
 }
 
 template <int B, int ELT, int NPASS, typename OutT>
@@ -247,12 +248,21 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
     }
   } else {
     if (c.nmat == 1 && c.epi == EPI_STORE) {
+      if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2>())
+        if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles())
+          return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT, SO, 2>(c, a0lo, a1lo, st);
       if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
         if (use_staged<B, ELT, NPASS, 1, false>(c))
           return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
     } else if (c.nmat == 1 && c.epi == EPI_GATED_BWD) {
+      if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2>())
+        if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles())
+          return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT, SO, 2>(c, a0lo, a1lo, st);
+      if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
+        if (use_staged<B, ELT, NPASS, 1, false>(c))
+          return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT, SO>(c, a0lo, a1lo, st);
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT>(c, a0lo, a1lo, st);
     } else if (c.nmat == 2 && c.sumacc && c.epi == EPI_STORE) {

@@ -289,7 +289,12 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
     if (p.out1 && live)
       store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, v0, valid, vec_ok);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v0[i] = apply_act(v0[i], p.act);
+    for (int i = 0; i < 16; ++i) {
+      if constexpr (sizeof(OutT) == 2)
+        v0[i] = apply_act_fast(v0[i], p.act);
+      else
+        v0[i] = apply_act(v0[i], p.act);
+    }
     if constexpr (STG_SW > 0) {
       stage_chunk16<OutT, STG_SW>(stg, trow, tcol, v0);
     } else if (live) {
@@ -338,8 +343,16 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
       float pre[16];
       load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, pre, valid, vec_ok);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v0[i] = __fmul_rn(v0[i], apply_act_grad(pre[i], p.act));
-      store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
+      for (int i = 0; i < 16; ++i) {
+        if constexpr (sizeof(OutT) == 2)
+          v0[i] = __fmul_rn(v0[i], apply_act_grad_fast(pre[i], p.act));
+        else
+          v0[i] = __fmul_rn(v0[i], apply_act_grad(pre[i], p.act));
+      }
+      if constexpr (STG_SW > 0)
+        stage_chunk16<OutT, STG_SW>(stg, trow, tcol, v0);
+      else
+        store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, v0, valid, vec_ok);
     }
   }
 }

@@ -101,7 +101,9 @@ class _GeluFn(torch.autograd.Function):
         dx = bspmm_rt(dpre, w1)
         dv2 = _wgrad(hid, dy, w2.rows, w2.cols, w2, full=False)
         dv1 = _wgrad(x2d, dpre, w1.rows, w1.cols, w1, full=False)
-        return (dx, None, dpre.float().sum(0), None, dy.float().sum(0),
+        # bias gradients: column sums accumulated in fp32 straight from the bf16 tensors
+        return (dx, None, torch.sum(dpre, 0, dtype=torch.float32), None,
+                torch.sum(dy, 0, dtype=torch.float32),
                 dv1.to(w1.values.dtype), dv2.to(w2.values.dtype))
 
 
@@ -148,7 +150,8 @@ class SparseGeluMLP(nn.Module):
         else:
             hid = bspmm_fused(x2d, self.w1, "gelu", bias=self.b1)
             y = bspmm_fused(hid, self.w2, "none", bias=self.b2)
-        return self.dropout(y.reshape(*shape[:-1], y.shape[-1]).to(x.dtype))
+        y = y.reshape(*shape[:-1], y.shape[-1]).to(x.dtype)
+        return self.dropout(y) if self.dropout.p > 0 else y
 
 
 def sparsify_llama(model: nn.Module, block: int = 64, sparsity: float = 0.95,
