@@ -345,6 +345,16 @@ __device__ __forceinline__ void bulk_wait_group() {
 }
 
 // ---------------------------------------------------------------- misc
+// Shared-memory word read that the compiler cannot hoist above a preceding barrier wait
+// (asm volatile + memory clobber), issued as LDS rather than a generic strong load.
+__device__ __forceinline__ uint32_t ld_shared_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -317,7 +317,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
         for (int s = 0; s < n_steps; ++s) {
           wc.wait(2, &full[stage], phase, dbg_on);
           tc_fence_after();
-          const uint32_t meta = *reinterpret_cast<volatile uint32_t*>(&stage_meta[stage]);
+          const uint32_t meta = ld_shared_u32(&stage_meta[stage]);
           if (elect_one()) {
             const uint32_t soff = (stage * C::STAGE) >> 4;
 #pragma unroll

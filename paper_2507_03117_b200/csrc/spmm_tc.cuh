@@ -439,6 +439,38 @@ constexpr uint32_t kMetaMerged = 4u;      // one N = 2B MMA covers both (gate | 
 constexpr uint32_t kMetaAccFirst = 8u;    // first MMA group accumulates (else overwrites)
 constexpr uint32_t kMetaAccSecond = 16u;  // second MMA group accumulates
 
+// MMA recipe of one step {a_blk, k0, k1}: presence, merge and accumulate flags. init0/init1
+// track which accumulators already hold a partial sum of the current output line.
+template <int NMAT, bool SUMACC, bool MERGE>
+__device__ __forceinline__ uint32_t step_recipe(const int4& st, uint32_t& init0, uint32_t& init1) {
+  const bool has0 = st.y >= 0, has1 = NMAT > 1 && st.z >= 0;
+  uint32_t meta = (has0 ? kMetaHas0 : 0u) | (has1 ? kMetaHas1 : 0u);
+  if (MERGE && has0 && has1 && init0 == init1) {
+    meta |= kMetaMerged | (init0 ? kMetaAccFirst : 0u);
+    init0 = init1 = 1;
+  } else {
+    if (has0) { meta |= init0 ? kMetaAccFirst : 0u; init0 = 1; }
+    if (has1) {
+      if (SUMACC) { meta |= init0 ? kMetaAccSecond : 0u; init0 = 1; }
+      else { meta |= init1 ? kMetaAccSecond : 0u; init1 = 1; }
+    }
+  }
+  return meta;
+}
+
+// Named barriers (ids; 0 = __syncthreads, 1 = epilogue warps). The MMA warp never waits on an
+// mbarrier or reads shared memory itself: both stall its issue until its in-flight MMAs
+// drain (tools/mma_probe.cu P8: 354 vs 205 cycles per 4 x N=64 step). Warp 2 waits on the
+// mbarriers instead and releases the MMA warp through these hardware barriers.
+constexpr uint32_t kBarAcc = 2;    // + accumulator stage (2 ids)
+constexpr uint32_t kBarStage = 4;  // + ring stage (<= 8 ids)
+// Measured on cfg3 (b = 64): the waiter handoff wins for single-matrix products (down
+// projection 124 -> 118 us) but loses for the gate+up product, whose 48 KB stages leave only
+// 4 in flight so the extra handoff latency is exposed (237 -> 247 us); there the MMA warp
+// waits on the mbarriers itself.
+template <int NMAT, int TM>
+constexpr bool use_waiter() { return NMAT == 1; }
+
 // 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (two warps per TMEM lane quarter, splitting the 16-column chunks).
 constexpr int kTcThreads = 384;
@@ -463,8 +495,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
   uint64_t* tmem_full = empty + C::STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-  // per-stage MMA recipe written by the producer before its expect_tx arrive (release) and
-  // read by the MMA warp after the full-barrier wait (acquire): see kMeta* below
+  // per-stage MMA recipe (when the MMA warp waits on the mbarriers itself): written by the
+  // producer before its expect_tx arrive (release), read after the full wait (acquire)
   uint32_t* stage_meta = tmem_slot + 4;
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
@@ -511,9 +543,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
     const uint64_t pol_w = policy_evict_last();
     const uint32_t mine = warp == 0 ? 0u : 1u;
     uint32_t stage = 0, phase = 0, n = 0;
-    // merged gate+up: one N = 2B MMA over [W_gate | W_up] (adjacent MN-major atoms)
-    constexpr bool kMerge = (NMAT == 2) && !SUMACC && !B_KMAJOR && (2 * B <= 256) &&
-                            (C::NATOM == 1 || C::B_TILE == C::NATOM * B * C::SW);
+    constexpr bool kMergeP = (NMAT == 2) && !SUMACC && !B_KMAJOR && (2 * B <= 256) &&
+                             (C::NATOM == 1 || C::B_TILE == C::NATOM * B * C::SW);
     // The next item's step range and first 32 steps are fetched one item ahead, so
     // the item boundary does not stall the ring on two dependent global loads.
     int nx_s0 = 0, nx_s1 = 0;
@@ -540,19 +571,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       for (int s = s0; s < s1; ++s) {
         const int4 st = cur.get(s);
         const int kb[2] = {st.y, st.z};
-        const bool has0 = st.y >= 0, has1 = NMAT > 1 && st.z >= 0;
-        // MMA recipe of this step (the MMA warp only decodes it)
-        uint32_t meta = (has0 ? kMetaHas0 : 0u) | (has1 ? kMetaHas1 : 0u);
-        if (kMerge && has0 && has1 && init0 == init1) {
-          meta |= kMetaMerged | (init0 ? kMetaAccFirst : 0u);
-          init0 = init1 = 1;
-        } else {
-          if (has0) { meta |= init0 ? kMetaAccFirst : 0u; init0 = 1; }
-          if (has1) {
-            if (SUMACC) { meta |= init0 ? kMetaAccSecond : 0u; init0 = 1; }
-            else { meta |= init1 ? kMetaAccSecond : 0u; init1 = 1; }
-          }
-        }
+        const uint32_t meta = step_recipe<NMAT, SUMACC, kMergeP>(st, init0, init1);
         if ((n++ & 1u) != mine) {
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           continue;
@@ -566,7 +585,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm)
             if (kb[mm] >= 0) bytes += C::NCOPY * (B * C::ROWB);
-          stage_meta[stage] = meta;
+          if (!use_waiter<NMAT, TM>()) stage_meta[stage] = meta;
           mbar_expect_tx(&full[stage], bytes);
           uint8_t* sbase = smem + stage * C::STAGE;
 #pragma unroll
@@ -631,24 +650,71 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       }
       return (static_cast<uint32_t>(ks) * C::MMA_K * C::SW) >> 4;
     };
+    constexpr bool kWaiter = use_waiter<NMAT, TM>();
     uint32_t stage = 0, phase = 0, it = 0;
-    auto steps_of = [&](int item) -> int {
-      if (item >= n_items) return 0;
+    // kWaiter: the step list is walked here (next item's first 32 steps fetched one item
+    // ahead; recipes from two presence ballots per 32 steps), so the per-step loop issues no
+    // shared-memory reads or shuffles between MMAs. Otherwise only the step count is needed
+    // and the recipe comes from the producer through shared memory.
+    int nx_s0 = 0, nx_s1 = 0;
+    int4 nx_first = make_int4(0, -1, -1, 0);
+    auto prefetch = [&](int item) {
+      if (item >= n_items) return;
       const int jn = item % p.n_lines;
-      return __ldg(&p.step_ptr[jn + 1]) - __ldg(&p.step_ptr[jn]);
+      nx_s0 = __ldg(&p.step_ptr[jn]);
+      nx_s1 = __ldg(&p.step_ptr[jn + 1]);
+      if constexpr (kWaiter) {
+        const int idx = nx_s0 + static_cast<int>(lane);
+        nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
+      }
     };
-    int nx_steps = steps_of(blockIdx.x);  // one item ahead (see the producer)
+    prefetch(blockIdx.x);
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const uint32_t as = it & 1, use = it >> 1;
-      const int n_steps = nx_steps;
-      nx_steps = steps_of(item + gridDim.x);
-      wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
+      const uint32_t as = it & 1;
+      const int s0 = nx_s0, s1 = nx_s1;
+      int4 mine = nx_first;
+      prefetch(item + gridDim.x);
+      uint32_t m0 = 0, m1 = 0, seen0 = 0, seen1 = 0;
+      if constexpr (kWaiter)
+        named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
+      else
+        wc.wait(3, &tmem_empty[as], ((it >> 1) & 1) ^ 1, dbg_on);
       tc_fence_after();
       const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
-      for (int s = 0; s < n_steps; ++s) {
-        wc.wait(2, &full[stage], phase, dbg_on);
-        tc_fence_after();
-        const uint32_t meta = *reinterpret_cast<volatile uint32_t*>(&stage_meta[stage]);
+      for (int s = s0; s < s1; ++s) {
+        uint32_t meta = 0;
+        if constexpr (kWaiter) {
+          const int i = (s - s0) & 31;
+          if (i == 0) {
+            if (s != s0) {  // next 32 steps of a long line
+              const int idx = s + static_cast<int>(lane);
+              mine = idx < s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
+            }
+            seen0 |= m0;
+            seen1 |= m1;
+            m0 = __ballot_sync(0xffffffffu, mine.y >= 0);
+            m1 = __ballot_sync(0xffffffffu, NMAT > 1 && mine.z >= 0);
+          }
+          const uint32_t below = (1u << i) - 1u;
+          const bool has0 = (m0 >> i) & 1u, has1 = NMAT > 1 && ((m1 >> i) & 1u);
+          const bool init0 = SUMACC ? (((m0 | m1) & below) | seen0 | seen1) != 0
+                                    : ((m0 & below) | seen0) != 0;
+          const bool init1 = ((m1 & below) | seen1) != 0;
+          meta = (has0 ? kMetaHas0 : 0u) | (has1 ? kMetaHas1 : 0u);
+          if (kMerge && has0 && has1 && init0 == init1) {
+            meta |= kMetaMerged | (init0 ? kMetaAccFirst : 0u);
+          } else {
+            meta |= init0 ? kMetaAccFirst : 0u;
+            if (SUMACC) meta |= (init0 || has0) ? kMetaAccSecond : 0u;
+            else meta |= init1 ? kMetaAccSecond : 0u;
+          }
+          named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
+          tc_fence_after();
+        } else {
+          wc.wait(2, &full[stage], phase, dbg_on);
+          tc_fence_after();
+          meta = ld_shared_u32(&stage_meta[stage]);  // the producer's recipe
+        }
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
           const uint64_t bd = b_desc0 + soff;
@@ -701,6 +767,23 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       if (elect_one()) mma_commit(&tmem_full[as]);
       __syncwarp();
     }
+  } else if (warp == 2 && use_waiter<NMAT, TM>()) {
+    // ------------------------------------------------------------ barrier waiter
+    // Mirrors the MMA warp's item / step sequence: waits on the accumulator-free and
+    // stage-full mbarriers and releases the MMA warp through named barriers.
+    uint32_t stage = 0, phase = 0, it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      const uint32_t as = it & 1, use = it >> 1;
+      const int j = item % p.n_lines;
+      const int n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
+      wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
+      named_bar_arrive(kBarAcc + as, 64);
+      for (int s = 0; s < n_steps; ++s) {
+        wc.wait(2, &full[stage], phase, dbg_on);
+        named_bar_arrive(kBarStage + stage, 64);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;                 // TMEM lane quarter
@@ -745,7 +828,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
     }
   }
 
-  if (warp == 0 || warp == 1 || warp == 4) wc.flush(p.dbg);
+  if (warp == 0 || warp == 2 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
