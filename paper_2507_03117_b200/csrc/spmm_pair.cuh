@@ -87,6 +87,7 @@ __device__ __forceinline__ uint32_t wh_koff(int ks) {
 // Per-stage recipe written by the producer (see kMeta* in spmm_tc.cuh) plus, per matrix, the
 // resident slot of its weight half (bits 8-15 / 16-23; 0xff = streamed with the panel).
 constexpr uint32_t kPairStreamed = 0xffu;
+constexpr uint32_t kBarW = 12;  // named barrier: resident weights of the item landed
 
 template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT, int OUT_ELT = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
@@ -108,7 +109,6 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
   uint64_t* wfull = tmem_empty + 2;
   uint64_t* wempty = wfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + 1);
-  uint32_t* stage_meta = tmem_slot + 4;          // [MAX_STAGES]
   uint8_t* staging = smem + 1024;                // [2][OUT_TILE]
   uint8_t* stages = staging + C::STAGING;        // activation panels (+ streamed weights)
   uint8_t* res = stages + NST * C::STAGE;        // resident weight halves
@@ -152,17 +152,19 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
   constexpr bool dbg_on = false;
 #endif
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (both CTAs)
-    // Per item (line j, R pair tiles): the line's weight halves go to the resident region
-    // once (as many as fit), then every tile streams its activation panels through the
-    // ring. The first 32 steps of the line stay in registers across the tiles.
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------------------ TMA producers (both CTAs)
+    // Per item (line j, R pair tiles): warp 0 puts the line's weight halves into the resident
+    // region once (as many as fit), then every tile streams its activation panels through
+    // the ring; warps 0 and 3 issue the even / odd steps. The first 32 steps of the line stay
+    // in registers across the tiles.
     const uint64_t pol_w = policy_evict_last();
     // activation panels are re-read by every line of the same token tile: keep them in L2
     const uint64_t pol_a = policy_evict_last();
     const uint32_t full0 = mapa_shared(&full[0], 0);
     const uint32_t wfull0 = mapa_shared(wfull, 0);
-    uint32_t stage = 0, phase = 0, it = 0;
+    const uint32_t mine_p = warp == 0 ? 0u : 1u;
+    uint32_t stage = 0, phase = 0, it = 0, n = 0;
     for (int item = pair; item < n_items; item += n_pairs, ++it) {
       const int chunk = item / p.n_lines;
       const int j = item - chunk * p.n_lines;
@@ -172,20 +174,20 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
       StepCursor first;
       first.start(p.steps, s0, s1);
       const int4 first_mine = first.mine;
-      // resident weight halves of this line: its first RCAP blocks in step order
-      wc.wait(1, wempty, (it & 1) ^ 1, dbg_on);
-      int nres = 0;
-      {
-        StepCursor cur = first;
-        for (int s = s0; s < s1 && nres < RCAP; ++s) {
-          const int4 st = cur.get(s);
-          nres += (st.y >= 0 ? 1 : 0);
-          if (NMAT > 1 && nres < RCAP) nres += (st.z >= 0 ? 1 : 0);
+      if (warp == 0) {
+        // resident weight halves of this line: its first RCAP blocks in step order
+        wc.wait(1, wempty, (it & 1) ^ 1, dbg_on);
+        int nres = 0;
+        {
+          StepCursor cur = first;
+          for (int s = s0; s < s1 && nres < RCAP; ++s) {
+            const int4 st = cur.get(s);
+            nres += (st.y >= 0 ? 1 : 0);
+            if (NMAT > 1 && nres < RCAP) nres += (st.z >= 0 ? 1 : 0);
+          }
         }
-      }
-      if (rank == 0 && elect_one()) mbar_expect_tx(wfull, 2u * nres * C::WH);
-      __syncwarp();
-      {
+        if (rank == 0 && elect_one()) mbar_expect_tx(wfull, 2u * nres * C::WH);
+        __syncwarp();
         StepCursor cur;
         cur.steps = p.steps; cur.end = s1; cur.base = s0; cur.mine = first_mine;
         int r = 0;
@@ -215,55 +217,47 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
         }
       }
       for (int t = t0; t < t1; ++t) {
-        int rcount = 0;
-        uint32_t init0 = 0, init1 = 0;
+        int rcount = 0;  // blocks of the line so far (resident while < RCAP)
         StepCursor cur;
         cur.steps = p.steps; cur.end = s1; cur.base = s0; cur.mine = first_mine;
+        const int row0 = t * 256 + static_cast<int>(rank) * C::BM;
         for (int s = s0; s < s1; ++s) {
           const int4 st = cur.get(s);
           const int kb[2] = {st.y, st.z};
-          const bool has0 = kb[0] >= 0, has1 = NMAT > 1 && kb[1] >= 0;
-          // recipe: presence, accumulate flags, resident slot or streamed
-          uint32_t meta = (has0 ? kMetaHas0 : 0u) | (has1 ? kMetaHas1 : 0u);
-          uint32_t slot[2] = {kPairStreamed, kPairStreamed};
+          bool streamed[2] = {false, false};
           int nstream = 0;
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm) {
             if (kb[mm] < 0) continue;
-            if (rcount < nres) slot[mm] = static_cast<uint32_t>(rcount);
-            else ++nstream;
+            if (rcount >= RCAP) { streamed[mm] = true; ++nstream; }
             ++rcount;
           }
-          if (has0) { meta |= init0 ? kMetaAccFirst : 0u; init0 = 1; }
-          if (has1) {
-            if (SUMACC) { meta |= init0 ? kMetaAccSecond : 0u; init0 = 1; }
-            else { meta |= init1 ? kMetaAccSecond : 0u; init1 = 1; }
+          if ((n++ & 1u) != mine_p) {
+            if (++stage == static_cast<uint32_t>(NST)) { stage = 0; phase ^= 1; }
+            continue;
           }
-          meta |= (slot[0] << 8) | (slot[1] << 16);
           wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
           if (elect_one()) {
             uint32_t bytes = 0;
 #pragma unroll
-            for (int a = 0; a < C::NA; ++a)
-              if (!SUMACC || kb[a] >= 0) bytes += C::BM * C::ROWB;
+            for (int a2 = 0; a2 < C::NA; ++a2)
+              if (!SUMACC || kb[a2] >= 0) bytes += C::BM * C::ROWB;
             bytes += nstream * C::WH;
-            stage_meta[stage] = meta;
             if (rank == 0) mbar_expect_tx(&full[stage], 2u * bytes);
             const uint32_t fb = full0 + stage * 8;
             uint8_t* sbase = stages + stage * C::STAGE;
-            const int row0 = t * 256 + static_cast<int>(rank) * C::BM;
 #pragma unroll
-            for (int a = 0; a < C::NA; ++a) {
-              if (SUMACC && kb[a] < 0) continue;
-              const CUtensorMap* ma = a == 0 ? &mapA0 : &mapA1;
+            for (int a2 = 0; a2 < C::NA; ++a2) {
+              if (SUMACC && kb[a2] < 0) continue;
+              const CUtensorMap* ma = a2 == 0 ? &mapA0 : &mapA1;
 #pragma unroll
               for (int at = 0; at < C::NATOM; ++at)
-                tma_load_2d_pair(sbase + a * C::A_TILE + at * C::BM * C::SW, ma, fb,
+                tma_load_2d_pair(sbase + a2 * C::A_TILE + at * C::BM * C::SW, ma, fb,
                                  st.x * B + at * C::SWE, row0, pol_a);
             }
 #pragma unroll
             for (int mm = 0; mm < NMAT; ++mm) {
-              if (kb[mm] < 0 || slot[mm] != kPairStreamed) continue;
+              if (!streamed[mm]) continue;
               const CUtensorMap* mw = mm == 0 ? &mapW0 : &mapW1;
               uint8_t* dst = sbase + C::NA * C::A_TILE + mm * C::WH;
 #pragma unroll
@@ -284,7 +278,9 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
     }
   } else if (warp == 1 && rank == 0) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
-    // Decodes the producer's per-stage recipe; needs no step list of its own.
+    // Walks the line's step list itself (presence ballots, 32 steps per load) and is
+    // released by warp 2 through named barriers, so nothing between its MMAs reads shared
+    // memory or waits on an mbarrier (see kBarAcc in spmm_tc.cuh).
     const uint32_t smem0 = smem_u32(stages);
     const uint32_t res0 = smem_u32(res);
     const uint64_t a_desc0 = kmajor_desc<C::SW, C::MMA_K, 2>(smem0, C::BM, 0);
@@ -300,37 +296,62 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
       const uint32_t byte_k = static_cast<uint32_t>(ks) * 32;
       return ((byte_k / C::SW) * C::BM * C::SW + (byte_k % C::SW)) >> 4;
     };
-    uint32_t stage = 0, phase = 0, it = 0, tile_it = 0;
-    for (int item = pair; item < n_items; item += n_pairs, ++it) {
+    uint32_t stage = 0, tile_it = 0;
+    for (int item = pair; item < n_items; item += n_pairs) {
       const int chunk = item / p.n_lines;
       const int j = item - chunk * p.n_lines;
       const int t0 = chunk * pp.tiles_per_item;
       const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
-      const int n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
-      wc.wait(4, wfull, it & 1, dbg_on);
+      const int s0 = __ldg(&p.step_ptr[j]), s1 = __ldg(&p.step_ptr[j + 1]);
+      const int idx0 = s0 + static_cast<int>(lane);
+      const int4 first = idx0 < s1 ? __ldg(&p.steps[idx0]) : make_int4(0, -1, -1, 0);
+      named_bar_sync(kBarW, 64);  // warp 2 saw wfull: this line's resident halves landed
       tc_fence_after();
       for (int t = t0; t < t1; ++t, ++tile_it) {
-        const uint32_t as = tile_it & 1, use = tile_it >> 1;
-        wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
+        const uint32_t as = tile_it & 1;
+        named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
         tc_fence_after();
         const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
-        for (int s = 0; s < n_steps; ++s) {
-          wc.wait(2, &full[stage], phase, dbg_on);
+        int4 mine = first;
+        uint32_t m0 = 0, m1 = 0, seen0 = 0, seen1 = 0;
+        int base_blocks = 0;  // stored blocks of this line before the current 32-step chunk
+        for (int s = s0; s < s1; ++s) {
+          const int i = (s - s0) & 31;
+          if (i == 0) {
+            if (s != s0) {
+              base_blocks += __popc(m0) + __popc(m1);
+              const int idx = s + static_cast<int>(lane);
+              mine = idx < s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
+            }
+            seen0 |= m0;
+            seen1 |= m1;
+            m0 = __ballot_sync(0xffffffffu, mine.y >= 0);
+            m1 = __ballot_sync(0xffffffffu, NMAT > 1 && mine.z >= 0);
+          }
+          const uint32_t below = (1u << i) - 1u;
+          const bool has0 = (m0 >> i) & 1u, has1 = NMAT > 1 && ((m1 >> i) & 1u);
+          const bool init0 = SUMACC ? (((m0 | m1) & below) | seen0 | seen1) != 0
+                                    : ((m0 & below) | seen0) != 0;
+          const bool init1 = ((m1 & below) | seen1) != 0;
+          // block order in the line: step order, matrix 0 before matrix 1 (the producer's)
+          const int b0 = base_blocks + __popc(m0 & below) + __popc(m1 & below);
+          const int bidx[2] = {b0, b0 + (has0 ? 1 : 0)};
+          named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
           tc_fence_after();
-          const uint32_t meta = ld_shared_u32(&stage_meta[stage]);
           if (elect_one()) {
             const uint32_t soff = (stage * C::STAGE) >> 4;
 #pragma unroll
             for (int mm = 0; mm < NMAT; ++mm) {
-              if (!(meta & (mm == 0 ? kMetaHas0 : kMetaHas1))) continue;
+              if (!(mm == 0 ? has0 : has1)) continue;
               const int acc_i = SUMACC ? 0 : mm;
               const int a_i = SUMACC ? mm : 0;
               const uint32_t d = d_base + acc_i * B;
               const uint64_t ad = a_desc0 + soff + ((a_i * C::A_TILE) >> 4);
-              const uint32_t slot = (meta >> (mm == 0 ? 8 : 16)) & 0xffu;
-              const uint64_t wd = slot != kPairStreamed ? wdesc_res0 + ((slot * C::WH) >> 4)
-                                                        : wdesc_str0 + soff + ((mm * C::WH) >> 4);
-              const uint32_t init = (meta & (mm == 0 ? kMetaAccFirst : kMetaAccSecond)) ? 1u : 0u;
+              const uint64_t wd = bidx[mm] < RCAP
+                                      ? wdesc_res0 + ((static_cast<uint32_t>(bidx[mm]) * C::WH) >> 4)
+                                      : wdesc_str0 + soff + ((mm * C::WH) >> 4);
+              const uint32_t init = mm == 0 ? (init0 ? 1u : 0u)
+                                            : (SUMACC ? ((init0 || has0) ? 1u : 0u) : (init1 ? 1u : 0u));
 #pragma unroll
               for (int ks = 0; ks < C::KSL; ++ks)
                 mma_f16_pair(d, ad + a_koff(ks), wd + wh_koff<B, B_KMAJOR>(ks), C::IDESC,
@@ -339,13 +360,35 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
             mma_commit_pair(&empty[stage]);
           }
           __syncwarp();
-          if (++stage == static_cast<uint32_t>(NST)) { stage = 0; phase ^= 1; }
+          if (++stage == static_cast<uint32_t>(NST)) stage = 0;
         }
         if (elect_one()) mma_commit_pair(&tmem_full[as]);
         __syncwarp();
       }
       if (elect_one()) mma_commit_pair(wempty);
       __syncwarp();
+    }
+  } else if (warp == 2 && rank == 0) {
+    // ------------------------------------------------------------ barrier waiter (leader)
+    uint32_t stage = 0, phase = 0, it = 0, tile_it = 0;
+    for (int item = pair; item < n_items; item += n_pairs, ++it) {
+      const int chunk = item / p.n_lines;
+      const int j = item - chunk * p.n_lines;
+      const int t0 = chunk * pp.tiles_per_item;
+      const int t1 = min(t0 + pp.tiles_per_item, pp.n_pair_tiles);
+      const int n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
+      wc.wait(4, wfull, it & 1, dbg_on);
+      named_bar_arrive(kBarW, 64);
+      for (int t = t0; t < t1; ++t, ++tile_it) {
+        const uint32_t as = tile_it & 1, use = tile_it >> 1;
+        wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
+        named_bar_arrive(kBarAcc + as, 64);
+        for (int s = 0; s < n_steps; ++s) {
+          wc.wait(2, &full[stage], phase, dbg_on);
+          named_bar_arrive(kBarStage + stage, 64);
+          if (++stage == static_cast<uint32_t>(NST)) { stage = 0; phase ^= 1; }
+        }
+      }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
@@ -384,7 +427,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
     }
   }
 
-  if (warp == 0 || warp == 1 || warp == 4) wc.flush(p.dbg);
+  if (warp == 0 || warp == 2 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {

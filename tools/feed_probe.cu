@@ -13,6 +13,14 @@
 
 using namespace blast;
 
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 #define CK(x)                                                                        \
   do {                                                                               \
     cudaError_t e_ = (x);                                                            \
@@ -25,9 +33,10 @@ using namespace blast;
 constexpr int M = 8192, D = 4096, LINES = 224, STEPS = 12, NBLK = LINES * STEPS;
 constexpr int PANEL = 128 * 128, WBLK = 8192;
 
-template <int P, int S, int MMA, int ASC = 0, int GU = 0>
+template <int P, int S, int MMA, int ASC = 0, int GU = 0, int BULK = 0>
 __global__ void __launch_bounds__(256, 1) feed_kernel(const __grid_constant__ CUtensorMap mx,
-                                                      const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mw2, int n_items) {
+                                                      const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mw2, int n_items,
+                                                      const uint8_t* xg, const uint8_t* wg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[16], empty[16];
@@ -55,8 +64,14 @@ __global__ void __launch_bounds__(256, 1) feed_kernel(const __grid_constant__ CU
         if (elect_one()) {
           mbar_expect_tx(&full[stage], PANEL + WBLK);
           uint8_t* dst = smem + stage * STAGE;
-          tma_load_2d(dst, &mx, &full[stage], r * 64, (t & (n_tiles - 1)) * 128);
-          tma_load_2d(dst + PANEL + (GU ? (s & 1) * WBLK : 0), (ASC == 2 && (s & 1)) ? &mw2 : &mw, &full[stage], 0, k * 64);
+          if (BULK) {
+            // block-major activation layout: panel (t, r) is one contiguous 16 KB run
+            bulk_g2s(dst, xg + (static_cast<size_t>(r) * n_tiles + (t & (n_tiles - 1))) * PANEL, PANEL, &full[stage]);
+            bulk_g2s(dst + PANEL, wg + static_cast<size_t>(k) * WBLK, WBLK, &full[stage]);
+          } else {
+            tma_load_2d(dst, &mx, &full[stage], r * 64, (t & (n_tiles - 1)) * 128);
+            tma_load_2d(dst + PANEL + (GU ? (s & 1) * WBLK : 0), (ASC == 2 && (s & 1)) ? &mw2 : &mw, &full[stage], 0, k * 64);
+          }
         }
         __syncwarp();
       }
@@ -113,16 +128,17 @@ static CUtensorMap map2d(void* base, uint64_t inner, uint64_t outer, uint32_t bo
   return m;
 }
 
-template <int P, int S, int MMA, int ASC = 0, int GU = 0>
-void run(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mw2, cudaEvent_t e0, cudaEvent_t e1) {
-  auto k = feed_kernel<P, S, MMA, ASC, GU>;
+template <int P, int S, int MMA, int ASC = 0, int GU = 0, int BULK = 0>
+void run(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mw2, cudaEvent_t e0, cudaEvent_t e1,
+         const void* xg = nullptr, const void* wg = nullptr) {
+  auto k = feed_kernel<P, S, MMA, ASC, GU, BULK>;
   constexpr int STAGE = PANEL + (GU ? 2 : 1) * WBLK;
   const int smem = S * STAGE + 2048;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int n_items = (M / 128) * LINES;
-  k<<<148, 256, smem>>>(mx, mw, mw2, n_items);
+  k<<<148, 256, smem>>>(mx, mw, mw2, n_items, (const uint8_t*)xg, (const uint8_t*)wg);
   CK(cudaEventRecord(e0));
-  k<<<148, 256, smem>>>(mx, mw, mw2, n_items);
+  k<<<148, 256, smem>>>(mx, mw, mw2, n_items, (const uint8_t*)xg, (const uint8_t*)wg);
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   CK(cudaGetLastError());
@@ -130,7 +146,7 @@ void run(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mw2, c
   CK(cudaEventElapsedTime(&ms, e0, e1));
   const double bytes = double(n_items) * STEPS * (PANEL + WBLK);
   const double steps_per_sm = double(n_items) * STEPS / 148.0;
-  printf("gu=%d asc=%d producers=%d stages=%d consumer=%s: %.3f ms  %.0f GB/s  %.0f cyc/step/SM  (MMA-only floor 280)\n", GU, ASC, P, S,
+  printf("bulk=%d gu=%d asc=%d producers=%d stages=%d consumer=%s: %.3f ms  %.0f GB/s  %.0f cyc/step/SM  (MMA-only floor 280)\n", BULK, GU, ASC, P, S,
          MMA ? "mma" : "release", ms, bytes / (ms * 1e6), ms * 1e-3 * 1.965e9 / steps_per_sm);
 }
 
@@ -146,9 +162,10 @@ int main() {
   const CUtensorMap mx = map2d(x, D, M, 64, 128);
   const CUtensorMap mw = map2d(w, 64, size_t(NBLK) * 64, 64, 64);
   const CUtensorMap mw2 = map2d(w, 64, size_t(NBLK) * 64, 64, 64);
+  run<1, 8, 0>(mx, mw, mw2, e0, e1);
   run<1, 8, 1>(mx, mw, mw2, e0, e1);
-  run<1, 6, 1>(mx, mw, mw2, e0, e1);
-  run<1, 6, 1, 0, 1>(mx, mw, mw2, e0, e1);
-  run<1, 5, 1, 0, 1>(mx, mw, mw2, e0, e1);
+  run<1, 8, 0, 0, 0, 1>(mx, mw, mw2, e0, e1, x, w);
+  run<1, 8, 1, 0, 0, 1>(mx, mw, mw2, e0, e1, x, w);
+  run<2, 8, 0, 0, 0, 1>(mx, mw, mw2, e0, e1, x, w);
   return 0;
 }

@@ -477,7 +477,33 @@ __global__ void __launch_bounds__(128, 1) sync_rate_kernel(int iters, unsigned l
   __shared__ volatile int ready_count;
   if (threadIdx.x == 0) ready_count = 0;
   __syncthreads();
-  if (warp == 1 && MODE == 9) {
+  if (warp == 1 && MODE == 10) {
+    // the MMA warp never touches shared memory: warp 3 waits on full[] and releases the
+    // MMA warp through a named barrier (bar.sync / bar.arrive, ids 1..8 by stage)
+    const long long t0 = clock64();
+    uint32_t stage = 0;
+    for (int i = 0; i < iters; ++i) {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + stage));
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_f16(tbase + (i & 1) * 64, ad0 + ks * 2, bd0 + ks * 2, idesc, ks ? 1u : 0u);
+        mma_commit(&emptyb[stage]);
+      }
+      __syncwarp();
+      if (++stage == S) stage = 0;
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) out[blockIdx.x] = t1 - t0;
+  } else if (warp == 3 && MODE == 10) {
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      wait_v<0>(&fullb[stage], phase);
+      asm volatile("bar.arrive %0, 64;" ::"r"(1 + stage));
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 1 && MODE == 9) {
     // the MMA warp never waits on an mbarrier: warp 3 waits on full[] and publishes a
     // counter in shared memory that the MMA warp polls
     const long long t0 = clock64();
@@ -665,7 +691,7 @@ int main() {
   run_sync_rate<1>(4000);
   run_sync_rate<2>(4000);
   run_sync_rate<9, 0, 8>(4000);
-  run_sync_rate<9, 0, 4>(4000);
+  run_sync_rate<10, 0, 8>(4000);
 
   run_pair_rate<64>(4000);
   run_pair_rate<128>(4000);
