@@ -283,10 +283,10 @@ static int pair_stages_override() {
   return v;
 }
 
-template <int B, int NMAT, bool SUM, bool BK, int EPI, int OUT_ELT = 0>
+template <int B, int NMAT, bool SUM, bool BK, int EPI, int OUT_ELT = 0, int TM = 1>
 static int launch_pair(const EngineCall& c, cudaStream_t st) {
-  using Cfg = PairCfg<B, NMAT, SUM, BK, OUT_ELT>;
-  auto kern = spmm_pair_kernel<B, NMAT, SUM, BK, EPI, __nv_bfloat16, OUT_ELT>;
+  using Cfg = PairCfg<B, NMAT, SUM, BK, OUT_ELT, TM>;
+  auto kern = spmm_pair_kernel<B, NMAT, SUM, BK, EPI, __nv_bfloat16, OUT_ELT, TM>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -323,7 +323,7 @@ static int launch_pair(const EngineCall& c, cudaStream_t st) {
   if (!ok) return BLAST_EINVAL;
   PairParams pp{};
   pp.p = make_params(c);
-  pp.n_pair_tiles = static_cast<int32_t>(cdiv(c.m, 256));
+  pp.n_pair_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::PT));
   const int64_t n_pairs = num_sms() / 2;
   int64_t r = (c.n_lines * pp.n_pair_tiles) / (12 * n_pairs);
   if (const char* e = getenv("BLAST_PAIR_R")) r = atoi(e);
@@ -356,12 +356,15 @@ static int dispatch_pair_b(const EngineCall& c, cudaStream_t st) {
   if (!c.transposed) {
     const bool staged = !staged_out_disabled() && !c.accumulate && aligned16(c.out0) &&
                         (c.ld_out * 2) % 16 == 0;
+    const bool wide = staged && c.m >= 512 && wide_tiles();
     if (c.nmat == 1 && c.epi == EPI_STORE && c.act == ACT_NONE && !c.accumulate)
-      return staged ? launch_pair<B, 1, false, false, EPI_STORE, 2>(c, st)
-                    : launch_pair<B, 1, false, false, EPI_STORE>(c, st);
+      return wide ? launch_pair<B, 1, false, false, EPI_STORE, 2, 2>(c, st)
+             : staged ? launch_pair<B, 1, false, false, EPI_STORE, 2>(c, st)
+                      : launch_pair<B, 1, false, false, EPI_STORE>(c, st);
     if (c.nmat == 2 && c.epi == EPI_GATED_FWD)
-      return staged ? launch_pair<B, 2, false, false, EPI_GATED_FWD, 2>(c, st)
-                    : launch_pair<B, 2, false, false, EPI_GATED_FWD>(c, st);
+      return wide ? launch_pair<B, 2, false, false, EPI_GATED_FWD, 2, 2>(c, st)
+             : staged ? launch_pair<B, 2, false, false, EPI_GATED_FWD, 2>(c, st)
+                      : launch_pair<B, 2, false, false, EPI_GATED_FWD>(c, st);
   } else {
     if (c.nmat == 1 && c.epi == EPI_STORE)
       return launch_pair<B, 1, false, true, EPI_STORE>(c, st);

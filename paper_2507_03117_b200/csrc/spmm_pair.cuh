@@ -22,10 +22,14 @@
 
 namespace blast {
 
-template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0>
+// TM = 2: a pair tile is 512 tokens; each CTA stages two 128-row halves per step (rows
+// t*512 + h*256 + rank*128), and every half accumulates into its own TMEM columns: 8 pair
+// MMAs per pipeline round trip instead of 4.
+template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0, int TM = 1>
 struct PairCfg {
   static constexpr int ELT = 2;
-  static constexpr int BM = 128;                          // rows per CTA (M = 256 per pair)
+  static constexpr int BM = 128;                          // rows per CTA per half (M = 256 per pair)
+  static constexpr int PT = 256 * TM;                     // tokens per pair tile
   static constexpr int ROWB = B * ELT;                    // bytes of an activation panel row
   static constexpr int SW = ROWB < 128 ? ROWB : 128;
   static constexpr int SWE = SW / ELT;
@@ -33,7 +37,8 @@ struct PairCfg {
   static constexpr int MMA_K = 16;
   static constexpr int KSL = B / MMA_K;
   static constexpr int NA = SUMACC ? NMAT : 1;
-  static constexpr int A_TILE = (BM * ROWB + 1023) / 1024 * 1024;
+  static constexpr int A_HALF = (BM * ROWB + 1023) / 1024 * 1024;  // one 128-row half
+  static constexpr int A_TILE = TM * A_HALF;
   // weight half: MN-major (forward) = [B k-rows x B/2 n-cols]; K-major (transposed
   // product) = [B/2 n-rows x B k-cols]. Either way B*B/2 elements.
   static constexpr int WH = B * (B / 2) * ELT;
@@ -53,7 +58,8 @@ struct PairCfg {
   static constexpr int SMEM_BYTES = 232448;
   static constexpr int DATA_BYTES = SMEM_BYTES - 2048 - STAGING;  // stages + resident weights
   static constexpr int NACC = SUMACC ? 1 : NMAT;
-  static constexpr int ACC_STRIDE = NACC * B;
+  static constexpr int HALF_ACC = NACC * B;
+  static constexpr int ACC_STRIDE = TM * HALF_ACC;
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE <= 32    ? 32
                                    : 2 * ACC_STRIDE <= 64  ? 64
                                    : 2 * ACC_STRIDE <= 128 ? 128
@@ -89,13 +95,14 @@ __device__ __forceinline__ uint32_t wh_koff(int ks) {
 constexpr uint32_t kPairStreamed = 0xffu;
 constexpr uint32_t kBarW = 12;  // named barrier: resident weights of the item landed
 
-template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT, int OUT_ELT = 0>
+template <int B, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT, int OUT_ELT = 0,
+          int TM = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
                  const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
                  const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW1,
                  const PairParams pp) {
-  using C = PairCfg<B, NMAT, SUMACC, B_KMAJOR, OUT_ELT>;
+  using C = PairCfg<B, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM>;
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
   const SpmmParams& p = pp.p;
   extern __shared__ uint8_t smem_raw[];
@@ -220,7 +227,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
         int rcount = 0;  // blocks of the line so far (resident while < RCAP)
         StepCursor cur;
         cur.steps = p.steps; cur.end = s1; cur.base = s0; cur.mine = first_mine;
-        const int row0 = t * 256 + static_cast<int>(rank) * C::BM;
+        const int row0 = t * C::PT + static_cast<int>(rank) * C::BM;
         for (int s = s0; s < s1; ++s) {
           const int4 st = cur.get(s);
           const int kb[2] = {st.y, st.z};
@@ -241,7 +248,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
             uint32_t bytes = 0;
 #pragma unroll
             for (int a2 = 0; a2 < C::NA; ++a2)
-              if (!SUMACC || kb[a2] >= 0) bytes += C::BM * C::ROWB;
+              if (!SUMACC || kb[a2] >= 0) bytes += TM * C::BM * C::ROWB;
             bytes += nstream * C::WH;
             if (rank == 0) mbar_expect_tx(&full[stage], 2u * bytes);
             const uint32_t fb = full0 + stage * 8;
@@ -251,9 +258,11 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
               if (SUMACC && kb[a2] < 0) continue;
               const CUtensorMap* ma = a2 == 0 ? &mapA0 : &mapA1;
 #pragma unroll
-              for (int at = 0; at < C::NATOM; ++at)
-                tma_load_2d_pair(sbase + a2 * C::A_TILE + at * C::BM * C::SW, ma, fb,
-                                 st.x * B + at * C::SWE, row0, pol_a);
+              for (int h = 0; h < TM; ++h)
+#pragma unroll
+                for (int at = 0; at < C::NATOM; ++at)
+                  tma_load_2d_pair(sbase + a2 * C::A_TILE + h * C::A_HALF + at * C::BM * C::SW,
+                                   ma, fb, st.x * B + at * C::SWE, row0 + h * 256, pol_a);
             }
 #pragma unroll
             for (int mm = 0; mm < NMAT; ++mm) {
@@ -341,12 +350,13 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
           if (elect_one()) {
             const uint32_t soff = (stage * C::STAGE) >> 4;
 #pragma unroll
-            for (int mm = 0; mm < NMAT; ++mm) {
+            for (int hm = 0; hm < TM * NMAT; ++hm) {
+              const int h = hm / NMAT, mm = hm % NMAT;  // half-major: one B operand per half
               if (!(mm == 0 ? has0 : has1)) continue;
               const int acc_i = SUMACC ? 0 : mm;
               const int a_i = SUMACC ? mm : 0;
-              const uint32_t d = d_base + acc_i * B;
-              const uint64_t ad = a_desc0 + soff + ((a_i * C::A_TILE) >> 4);
+              const uint32_t d = d_base + h * C::HALF_ACC + acc_i * B;
+              const uint64_t ad = a_desc0 + soff + ((a_i * C::A_TILE + h * C::A_HALF) >> 4);
               const uint64_t wd = bidx[mm] < RCAP
                                       ? wdesc_res0 + ((static_cast<uint32_t>(bidx[mm]) * C::WH) >> 4)
                                       : wdesc_str0 + soff + ((mm * C::WH) >> 4);
@@ -408,18 +418,24 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
         const uint32_t as = tile_it & 1, use = tile_it >> 1;
         wc.wait(5, &tmem_full[as], use & 1, dbg_on);
         tc_fence_after();
-        const int row0 = t * 256 + static_cast<int>(rank) * C::BM;
-        uint8_t* stg = staging + (tile_it & 1) * C::OUT_TILE;
-        const uint32_t tacc = tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE;
-        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, row0, j * B, flags, stg, half,
-                                                          q, lane, etid, vec_ok);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (rank == 0) mbar_arrive(&tmem_empty[as]);
-          else mbar_arrive_cluster(&tmem_empty[as], 0);
+#pragma unroll
+        for (int h = 0; h < TM; ++h) {
+          const int row0 = t * C::PT + h * 256 + static_cast<int>(rank) * C::BM;
+          uint8_t* stg = staging + ((tile_it * TM + h) & 1) * C::OUT_TILE;
+          const uint32_t tacc =
+              tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
+          epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, row0, j * B, flags, stg,
+                                                            half, q, lane, etid, vec_ok);
+          if (h == TM - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (rank == 0) mbar_arrive(&tmem_empty[as]);
+              else mbar_arrive_cluster(&tmem_empty[as], 0);
+            }
+          }
+          epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT>(&mapO, stg, row0, j * B, etid, pol_out);
         }
-        epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT>(&mapO, stg, row0, j * B, etid, pol_out);
       }
     }
     if constexpr (OUT_ELT > 0) {
