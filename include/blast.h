@@ -42,7 +42,8 @@ enum {
   BLAST_EMISMATCH = 2,  /* dimension mismatch (kernels.py:70-72 "mismatch") */
   BLAST_EGRID = 3,      /* mask grid does not match matrix grid (pruner.py:178-182) */
   BLAST_ECUDA = 4,      /* CUDA runtime / launch error */
-  BLAST_ENOMEM = 5
+  BLAST_ENOMEM = 5,
+  BLAST_EUNSUPPORTED = 6  /* configuration not covered by this entry point (nothing launched) */
 };
 
 /* Device-resident BCSC matrix (bcsc.py:35 BlockSparseMatrix) plus the cached
@@ -127,6 +128,16 @@ int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
                       const blast_bcsc_t* up, const blast_bcsc_t* down,
                       const blast_mlp_plan_t* plan, void* y, void* gate_pre, void* up_out,
                       void* gated, void* stream);
+/* Fused inference forward y = (silu(x Wg) * (x Wu)) Wd in one persistent kernel, the
+ * intermediate G kept in a 4-tile (4 x 256 tokens) ring that stays in L2 instead of an
+ * [m, h] tensor in HBM (mlp.py:102-115 without the saved activations). bf16, b = 64,
+ * m >= 256, d and h multiples of 64; otherwise returns BLAST_EUNSUPPORTED without launching.
+ * Results equal the two-launch path bit for bit. blast_mlp_forward takes this path only when
+ * BLAST_FUSED_MLP=1: on cfg3 it is slower (0.435 vs 0.352 ms per 8192 tokens) and the ring
+ * is written back to HBM anyway. */
+int blast_mlp_forward_fused(const void* x, int64_t m, const blast_bcsc_t* gate,
+                            const blast_bcsc_t* up, const blast_bcsc_t* down,
+                            const blast_mlp_plan_t* plan, void* y, void* stream);
 /* blast_mlp_forward on HOST buffers, the reference's boundary (mlp.py:102 takes and returns
  * ndarrays): x_host [m, e] and y_host [m, e] in the network dtype. The tokens are cut into
  * chunks of chunk_tokens rows (0: automatic) and the host->device copy of chunk c+1, the

@@ -60,6 +60,8 @@ _PROTOS = {
     "blast_mlp_forward": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                     C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp, vp, vp,
                                     vp]),
+    "blast_mlp_forward_fused": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
+                                          C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp]),
     "blast_mlp_forward_host": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                          C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, i64,
                                          vp]),

@@ -6,6 +6,10 @@
 #include "spmm_pair.cuh"
 #include "spmm_tc.cuh"
 
+int blast_mlp_forward_fused_if_enabled(const void* x, int64_t m, const blast_bcsc_t* gate,
+                                       const blast_bcsc_t* up, const blast_bcsc_t* down,
+                                       const blast_mlp_plan_t* plan, void* y, void* stream);
+
 namespace blast {
 
 struct EngineCall {
@@ -622,6 +626,10 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
     return BLAST_EMISMATCH;
   }
   if (m <= 0) return BLAST_OK;
+  if (!gated && !gate_pre && !up_out) {
+    const int rf = blast_mlp_forward_fused_if_enabled(x, m, gate, up, down, plan, y, stream);
+    if (rf != BLAST_EUNSUPPORTED) return rf;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t elt = bytes_of(gate->dtype);
   Scratch sg;
