@@ -44,6 +44,7 @@ struct EngineCall {
   const void* in1 = nullptr;
   int64_t ld_out = 0;
   const float* bias = nullptr;
+  bool reverse_tiles = false;  // last token tile first (see SpmmParams::reverse_tiles)
 };
 
 // BLAST_DEBUG_COUNTERS=1: per-role wait cycles of every tensor-core launch to stderr
@@ -101,6 +102,7 @@ static SpmmParams make_params(const EngineCall& c) {
   p.in1 = c.in1;
   p.ld_out = c.ld_out;
   p.bias = c.bias;
+  p.reverse_tiles = c.reverse_tiles ? 1 : 0;
   return p;
 }
 
@@ -513,8 +515,16 @@ extern "C" int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int 
   return blast_bspmm_ex(x, m, w, nullptr, act, y, nullptr, stream);
 }
 
+static int bspmm_impl(const void* x, int64_t m, const blast_bcsc_t* w, const float* bias, int act,
+                      void* y, void* pre, bool reverse_tiles, void* stream);
+
 extern "C" int blast_bspmm_ex(const void* x, int64_t m, const blast_bcsc_t* w, const float* bias,
                               int act, void* y, void* pre, void* stream) {
+  return bspmm_impl(x, m, w, bias, act, y, pre, false, stream);
+}
+
+static int bspmm_impl(const void* x, int64_t m, const blast_bcsc_t* w, const float* bias, int act,
+                      void* y, void* pre, bool reverse_tiles, void* stream) {
   if (!check_w(w)) return BLAST_EINVAL;
   if (act < 0 || act > 3) {
     set_error("unknown nonlinearity code %d", act);
@@ -540,6 +550,7 @@ extern "C" int blast_bspmm_ex(const void* x, int64_t m, const blast_bcsc_t* w, c
   c.out0 = y;
   c.out1 = pre;
   c.ld_out = w->cols;
+  c.reverse_tiles = reverse_tiles;
   return run_engine(c, static_cast<cudaStream_t>(stream));
 }
 
@@ -639,7 +650,9 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
   }
   int r = blast_mlp_gate_up(x, m, gate, up, plan, gated, gate_pre, up_out, stream);
   if (r) return r;
-  return blast_bspmm(gated, m, down, BLAST_ACT_NONE, y, stream);
+  // gate+up wrote G tile by tile in order: read it back last tile first, while the most
+  // recently written rows are still in L2
+  return bspmm_impl(gated, m, down, nullptr, BLAST_ACT_NONE, y, nullptr, true, stream);
 }
 
 extern "C" int blast_mlp_gate_up(const void* x, int64_t m, const blast_bcsc_t* gate,

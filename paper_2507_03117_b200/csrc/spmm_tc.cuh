@@ -48,7 +48,15 @@ struct SpmmParams {
   unsigned long long* dbg;  // optional per-role wait-cycle counters (BLAST_DEBUG_COUNTERS)
   const float* bias;        // EPI_STORE: optional per-output-column bias, added before act
   int32_t skip_epilogue;    // diagnosis only (BLAST_SKIP_EPILOGUE=1): release accumulators unread
+  int32_t reverse_tiles;    // process token tiles last-to-first (reads the most recently
+                            // written rows of the activations first, while they are in L2)
 };
+
+// token tile of a work item (items are t-major: item = t * n_lines + j)
+__device__ __forceinline__ int item_tile(const SpmmParams& p, int item) {
+  const int t = item / p.n_lines;
+  return p.reverse_tiles ? p.n_tok_tiles - 1 - t : t;
+}
 
 // v[i] += bias[col + i] for the valid columns of a 16-column chunk
 __device__ __forceinline__ void add_bias16(float (&v)[16], const float* bias, int col, int valid) {
@@ -559,7 +567,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
     };
     prefetch(blockIdx.x);
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int t = item / p.n_lines;
+      const int t = item_tile(p, item);
       const int s0 = nx_s0, s1 = nx_s1;
       StepCursor cur;
       cur.steps = p.steps;
@@ -795,8 +803,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int t = item / p.n_lines;
-      const int j = item - t * p.n_lines;
+      const int t = item_tile(p, item);
+      const int j = item % p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
       const int flags = __ldg(&p.line_flags[j]);
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
