@@ -109,7 +109,8 @@ static SpmmParams make_params(const EngineCall& c) {
 template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
           int OUT_ELT = 0, int TM = 1>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
-  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM>;
+  constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
+  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM, IN_ST>;
   auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM>;
   static bool configured = false;
   if (!configured) {
@@ -159,6 +160,12 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
                        static_cast<uint64_t>(c.n_valid), static_cast<uint64_t>(c.m),
                        static_cast<uint64_t>(c.ld_out) * OUT_ELT, Cfg::OUT_SW / (OUT_ELT ? OUT_ELT : 1),
                        Cfg::BM, Cfg::OUT_SW);
+  // staged in0 tiles (activation-derivative epilogue): same geometry as the output
+  CUtensorMap mI = mO;
+  if (ok && IN_ST)
+    ok = encode_map_2d(&mI, c.in0, BLAST_BF16, static_cast<uint64_t>(c.n_valid),
+                       static_cast<uint64_t>(c.m), static_cast<uint64_t>(c.ld_out) * 2,
+                       Cfg::OUT_SW / 2, Cfg::BM, Cfg::OUT_SW);
   if (!ok) return BLAST_EINVAL;
   SpmmParams p = make_params(c);
   p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
@@ -166,8 +173,8 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
   dbg_begin(st);
-  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1,
-                                                  mW1lo, p);
+  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo,
+                                                  mW1, mW1lo, p);
   const int rc = check_launch("spmm_tc");
   dbg_end("spmm_tc", st, grid);
   return rc;
@@ -198,7 +205,7 @@ static bool staged_out_disabled() {
 }
 // >= 3 pipeline stages next to the double-buffered bf16 output staging (TcCfg arithmetic),
 // and (TM = 2) both token halves' accumulators double-buffered in TMEM
-template <int B, int ELT, int NPASS, int NMAT, bool SUM, int TM = 1>
+template <int B, int ELT, int NPASS, int NMAT, bool SUM, int TM = 1, int IN_ST = 0>
 constexpr bool staged_fits() {
   if (ELT != 2 || NPASS != 1) return false;
   if (2 * TM * (SUM ? 1 : NMAT) * B > 512) return false;
@@ -207,7 +214,7 @@ constexpr bool staged_fits() {
   constexpr int b_tile = (B * rowb + 1023) / 1024 * 1024;
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
-  constexpr int staging = 2 * ((128 * B * 2 + 1023) / 1024 * 1024);
+  constexpr int staging = (2 + IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
   return (232448 - 1024 - 512 - staging) / stage >= 3;
 }
 // 256-token items (TcCfg TM = 2) for the forward products; BLAST_WIDE_TILES=0 disables.
@@ -263,11 +270,12 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
     } else if (c.nmat == 1 && c.epi == EPI_GATED_BWD) {
-      if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2>())
-        if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles())
+      if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2, 1>())
+        if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles() &&
+            aligned16(c.in0))
           return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT, SO, 2>(c, a0lo, a1lo, st);
-      if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
-        if (use_staged<B, ELT, NPASS, 1, false>(c))
+      if constexpr (staged_fits<B, ELT, NPASS, 1, false, 1, 1>())
+        if (use_staged<B, ELT, NPASS, 1, false>(c) && aligned16(c.in0))
           return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT, SO>(c, a0lo, a1lo, st);
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT>(c, a0lo, a1lo, st);

@@ -123,8 +123,11 @@ struct StepCursor {
 // TM = 2: an item covers 2 x 128 tokens; every stage carries a 256-row activation panel,
 // its weight block(s) are loaded once for both halves, and each half accumulates into its
 // own TMEM columns (twice the MMAs per pipeline round trip, half the weight traffic).
+// IN_ST = 1 (staged single-input activation-derivative epilogue): the epilogue also stages the
+// item's `in0` tiles (TM x 128 rows x B) in shared memory with one TMA load per tile, issued
+// before it waits for the accumulator, instead of row-strided per-thread loads.
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0,
-          int TM = 1>
+          int TM = 1, int IN_ST = 0>
 struct TcCfg {
   static constexpr int BM = 128;                          // rows per MMA / per output tile
   static constexpr int TROWS = BM * TM;                   // token rows per item
@@ -144,7 +147,8 @@ struct TcCfg {
   static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
   static constexpr int OUT_TILE = OUT_ELT ? round1k(BM * OUT_ROWB) : 0;
-  static constexpr int STAGING = 2 * OUT_TILE;
+  static constexpr int IN_STAGING = IN_ST ? TM * OUT_TILE : 0;
+  static constexpr int STAGING = 2 * OUT_TILE + IN_STAGING;
   // 227 KB opt-in maximum minus barriers, alignment slack and the output staging
   static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 512 - STAGING : 200 * 1024;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
@@ -175,6 +179,33 @@ struct TcCfg {
 // into a staged output tile laid out as OUT_NATOM swizzle atoms of [128 rows x SW bytes]
 // (the layout a SWIZZLE_<SW> TMA store reads): 16-byte unit u of a row lands at
 // u ^ ((row * SW / 128) mod (SW / 16)).
+// Inverse of stage_chunk16: 16 consecutive values of a staged (TMA-loaded, swizzled) tile.
+template <typename OutT, int SW>
+__device__ __forceinline__ void unstage_chunk16(const uint8_t* tile, int row, int col,
+                                                float (&v)[16]) {
+  constexpr int E = sizeof(OutT);
+  constexpr int UNITS = 16 * E / 16;
+  const int byte0 = col * E;
+  const uint8_t* atom = tile + (byte0 / SW) * (128 * SW) + row * SW;
+  const int u0 = (byte0 % SW) / 16;
+  const int x = ((row * SW) >> 7) & (SW / 16 - 1);
+#pragma unroll
+  for (int k = 0; k < UNITS; ++k) {
+    const uint4 w = *reinterpret_cast<const uint4*>(atom + (((u0 + k) ^ x) * 16));
+    if constexpr (E == 4) {
+      v[4 * k] = __uint_as_float(w.x); v[4 * k + 1] = __uint_as_float(w.y);
+      v[4 * k + 2] = __uint_as_float(w.z); v[4 * k + 3] = __uint_as_float(w.w);
+    } else {
+      const uint32_t h[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h[i]));
+        v[8 * k + 2 * i] = f.x;
+        v[8 * k + 2 * i + 1] = f.y;
+      }
+    }
+  }
+}
 template <typename OutT, int SW>
 __device__ __forceinline__ void stage_chunk16(uint8_t* tile, int row, int col, const float (&v)[16]) {
   constexpr int E = sizeof(OutT);
@@ -290,7 +321,7 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
                                                float (&v1)[16], int flags, bool row_ok,
                                                int col, int valid, int64_t off, bool vec_ok,
                                                uint8_t* stg = nullptr, int trow = 0,
-                                               int tcol = 0) {
+                                               int tcol = 0, const uint8_t* in_stg = nullptr) {
   const bool live = row_ok && valid > 0;
   if constexpr (EPI == EPI_STORE) {
     add_bias16(v0, p.bias, col, valid);
@@ -349,7 +380,12 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
       store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, db, valid, vec_ok);
     } else {
       float pre[16];
-      load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, pre, valid, vec_ok);
+      if constexpr (STG_SW > 0) {
+        if (in_stg) unstage_chunk16<OutT, STG_SW>(in_stg, trow, tcol, pre);
+        else load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, pre, valid, vec_ok);
+      } else {
+        load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, pre, valid, vec_ok);
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         if constexpr (sizeof(OutT) == 2)
@@ -381,7 +417,7 @@ template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW>
 __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t tacc, int row0,
                                                  int col0, int flags, uint8_t* stg, int half,
                                                  uint32_t q, uint32_t lane, uint32_t etid,
-                                                 bool vec_ok) {
+                                                 bool vec_ok, const uint8_t* in_stg = nullptr) {
   if constexpr (OUT_SW > 0) {
     if (etid == 0) bulk_wait_group_read<1>();
     named_bar_sync(1, kEpiWarpsT * 32);
@@ -420,7 +456,7 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
         v1[i] = kTwoAcc ? __uint_as_float(r1[k][i]) : 0.0f;
       }
       epilogue_chunk<EPI, OutT, OUT_SW>(p, v0, v1, flags, row_ok, col, valid, off, vec_ok, stg,
-                                        trow, c * 16);
+                                        trow, c * 16, in_stg);
     }
   }
 }
@@ -484,16 +520,20 @@ constexpr bool use_waiter() { return NMAT == 1; }
 constexpr int kTcThreads = 384;
 constexpr int kEpiWarps = kEpiWarpsT;
 
+template <int EPI, int OUT_ELT>
+constexpr int in_staged() { return (EPI == EPI_GATED_BWD && OUT_ELT > 0) ? 1 : 0; }
+
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
           int OUT_ELT = 0, int TM = 1>
 __global__ void __launch_bounds__(kTcThreads, 1)
-spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
+spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapI,
                const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
                const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA1lo,
                const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW0lo,
                const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW1lo,
                const SpmmParams p) {
-  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM>;
+  constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
+  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST>;
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -506,6 +546,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
   // per-stage MMA recipe (when the MMA warp waits on the mbarriers itself): written by the
   // producer before its expect_tx arrive (release), read after the full wait (acquire)
   uint32_t* stage_meta = tmem_slot + 4;
+  uint64_t* in_full = reinterpret_cast<uint64_t*>(stage_meta + 8);  // staged in0 tiles landed
+  uint8_t* in_staging = staging + 2 * C::OUT_TILE;                  // [TM][OUT_TILE] (IN_ST)
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -525,6 +567,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], kEpiWarps);
     }
+    mbar_init(in_full, 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -807,8 +850,21 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
       const int j = item % p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
       const int flags = __ldg(&p.line_flags[j]);
+      if constexpr (IN_ST) {
+        // this item's in0 tiles (the previous item's were consumed before its last barrier)
+        if (etid == 0) {
+          mbar_expect_tx(in_full, TM * C::BM * C::OUT_ROWB);
+#pragma unroll
+          for (int h = 0; h < TM; ++h)
+#pragma unroll
+            for (int a = 0; a < C::OUT_NATOM; ++a)
+              tma_load_2d(in_staging + h * C::OUT_TILE + a * (C::BM * C::OUT_SW), &mapI, in_full,
+                          j * B + a * (C::OUT_SW / OUT_ELT), t * C::TROWS + h * C::BM);
+        }
+      }
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
+      if constexpr (IN_ST) mbar_wait(in_full, it & 1);
       if (p.skip_epilogue) {  // diagnosis: release the accumulator unread
         tc_fence_before();
         __syncwarp();
@@ -821,8 +877,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO,
         const uint32_t tacc =
             tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
         const int row0 = t * C::TROWS + h * C::BM;
-        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, row0, j * B, flags, stg, half,
-                                                          q, lane, etid, vec_ok);
+        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(
+            p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
+            IN_ST ? in_staging + h * C::OUT_TILE : nullptr);
         if (h == TM - 1) {  // every TMEM read of this accumulator stage is done
           tc_fence_before();
           __syncwarp();
