@@ -107,11 +107,11 @@ static SpmmParams make_params(const EngineCall& c) {
 }
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
-          int OUT_ELT = 0, int TM = 1>
+          int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
-  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM, IN_ST>;
-  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM>;
+  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM, IN_ST, SPLIT>;
+  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM, SPLIT>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -217,6 +217,17 @@ constexpr bool staged_fits() {
   constexpr int staging = (2 + IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
   return (232448 - 1024 - 512 - staging) / stage >= 3;
 }
+// gate+up with one weight block per stage and single-buffered output staging (TcCfg SPLIT):
+// 5 pipeline stages instead of 4. Measured equal on cfg3 (236.6 vs 236.5 us: the kernel is
+// bound by L2->SM bytes, not by stages in flight), so opt-in: BLAST_SPLIT_STAGES=1.
+static bool split_stages() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_SPLIT_STAGES");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 // 256-token items (TcCfg TM = 2) for the forward products; BLAST_WIDE_TILES=0 disables.
 static bool wide_tiles() {
   static int v = -1;
@@ -252,7 +263,9 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
         if constexpr (staged_fits<B, ELT, NPASS, 2, false, 2>())
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
-            return launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2>(c, a0lo, a1lo, st);
+            return split_stages()
+                       ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 1>(c, a0lo, a1lo, st)
+                       : launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 2, false>())
           if (use_staged<B, ELT, NPASS, 2, false>(c))
             return launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO>(c, a0lo, a1lo, st);

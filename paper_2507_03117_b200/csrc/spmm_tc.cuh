@@ -126,8 +126,12 @@ struct StepCursor {
 // IN_ST = 1 (staged single-input activation-derivative epilogue): the epilogue also stages the
 // item's `in0` tiles (TM x 128 rows x B) in shared memory with one TMA load per tile, issued
 // before it waits for the accumulator, instead of row-strided per-thread loads.
+// SPLIT = 1 (gate+up): a stage carries ONE weight block; a step with both a gate and an up
+// block becomes two stages (the panel is loaded twice, ~5 % of steps at 90 % sparsity), and
+// the output is staged single-buffered. The 16 + 16 KB saved buy a fifth pipeline stage,
+// which the TMA latency under load needs.
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0,
-          int TM = 1, int IN_ST = 0>
+          int TM = 1, int IN_ST = 0, int SPLIT = 0>
 struct TcCfg {
   static constexpr int BM = 128;                          // rows per MMA / per output tile
   static constexpr int TROWS = BM * TM;                   // token rows per item
@@ -142,13 +146,15 @@ struct TcCfg {
   static constexpr int round1k(int x) { return (x + 1023) / 1024 * 1024; }
   static constexpr int A_TILE = round1k(TROWS * ROWB);
   static constexpr int B_TILE = round1k(B * ROWB);
-  static constexpr int STAGE = NA * NCOPY * A_TILE + NMAT * NCOPY * B_TILE;
+  static constexpr int WSLOTS = SPLIT ? 1 : NMAT;           // weight blocks per stage
+  static constexpr int STAGE = NA * NCOPY * A_TILE + WSLOTS * NCOPY * B_TILE;
+  static constexpr int OUT_BUFS = SPLIT ? 1 : 2;
   static constexpr int OUT_ROWB = B * OUT_ELT;                          // bytes of an output tile row
   static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
   static constexpr int OUT_TILE = OUT_ELT ? round1k(BM * OUT_ROWB) : 0;
   static constexpr int IN_STAGING = IN_ST ? TM * OUT_TILE : 0;
-  static constexpr int STAGING = 2 * OUT_TILE + IN_STAGING;
+  static constexpr int STAGING = OUT_BUFS * OUT_TILE + IN_STAGING;
   // 227 KB opt-in maximum minus barriers, alignment slack and the output staging
   static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 512 - STAGING : 200 * 1024;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
@@ -413,13 +419,13 @@ constexpr int kEpiWarpsT = 8;  // epilogue warps of both engines (named barrier 
 // `tacc` is the TMEM address of accumulator 0 for this warp's lane quarter; row0 / col0 are
 // the tile's first output row / column. Staging buffers alternate per tile (`stg`); the TMA
 // store issued from a buffer two tiles ago must have finished reading it.
-template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW>
+template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW, int NBUF = 2>
 __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t tacc, int row0,
                                                  int col0, int flags, uint8_t* stg, int half,
                                                  uint32_t q, uint32_t lane, uint32_t etid,
                                                  bool vec_ok, const uint8_t* in_stg = nullptr) {
   if constexpr (OUT_SW > 0) {
-    if (etid == 0) bulk_wait_group_read<1>();
+    if (etid == 0) bulk_wait_group_read<NBUF - 1>();
     named_bar_sync(1, kEpiWarpsT * 32);
   }
   const int trow = static_cast<int>(q * 32 + lane);
@@ -482,6 +488,7 @@ constexpr uint32_t kMetaHas1 = 2u;        // block of matrix 1 in this stage
 constexpr uint32_t kMetaMerged = 4u;      // one N = 2B MMA covers both (gate | up)
 constexpr uint32_t kMetaAccFirst = 8u;    // first MMA group accumulates (else overwrites)
 constexpr uint32_t kMetaAccSecond = 16u;  // second MMA group accumulates
+constexpr uint32_t kMetaLast = 32u;       // SPLIT: last stage of the item
 
 // MMA recipe of one step {a_blk, k0, k1}: presence, merge and accumulate flags. init0/init1
 // track which accumulators already hold a partial sum of the current output line.
@@ -524,7 +531,7 @@ template <int EPI, int OUT_ELT>
 constexpr int in_staged() { return (EPI == EPI_GATED_BWD && OUT_ELT > 0) ? 1 : 0; }
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
-          int OUT_ELT = 0, int TM = 1>
+          int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
 __global__ void __launch_bounds__(kTcThreads, 1)
 spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapI,
                const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
@@ -533,7 +540,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
                const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW1lo,
                const SpmmParams p) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
-  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST>;
+  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST, SPLIT>;
+  static_assert(!SPLIT || (NMAT == 2 && !SUMACC && NPASS == 1 && !use_waiter<NMAT, TM>()),
+                "split stages: gate+up products only");
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -547,7 +556,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   // producer before its expect_tx arrive (release), read after the full wait (acquire)
   uint32_t* stage_meta = tmem_slot + 4;
   uint64_t* in_full = reinterpret_cast<uint64_t*>(stage_meta + 8);  // staged in0 tiles landed
-  uint8_t* in_staging = staging + 2 * C::OUT_TILE;                  // [TM][OUT_TILE] (IN_ST)
+  uint8_t* in_staging = staging + C::OUT_BUFS * C::OUT_TILE;        // [TM][OUT_TILE] (IN_ST)
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -621,8 +630,15 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       uint32_t init0 = 0, init1 = 0;  // accumulator i already holds a partial sum
       for (int s = s0; s < s1; ++s) {
         const int4 st = cur.get(s);
-        const int kb[2] = {st.y, st.z};
-        const uint32_t meta = step_recipe<NMAT, SUMACC, kMergeP>(st, init0, init1);
+        // SPLIT: a step holding both a gate and an up block becomes two stages
+        const bool both = SPLIT && st.y >= 0 && st.z >= 0;
+        const int nparts = both ? 2 : 1;
+#pragma unroll 1
+        for (int part = 0; part < nparts; ++part) {
+        const int kb[2] = {(both && part == 1) ? -1 : st.y, (both && part == 0) ? -1 : st.z};
+        uint32_t meta = step_recipe<NMAT, SUMACC, kMergeP && !SPLIT>(make_int4(st.x, kb[0], kb[1], 0),
+                                                                     init0, init1);
+        if (SPLIT && s + 1 == s1 && part + 1 == nparts) meta |= kMetaLast;
         if ((n++ & 1u) != mine) {
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           continue;
@@ -658,9 +674,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             if (kb[mm] < 0) continue;
             const CUtensorMap* mh = (mm == 0) ? &mapW0 : &mapW1;
             const CUtensorMap* ml = (mm == 0) ? &mapW0lo : &mapW1lo;
+            const int slot = SPLIT ? 0 : mm;
 #pragma unroll
             for (int c = 0; c < C::NCOPY; ++c) {
-              uint8_t* dst = sbase + C::NA * C::NCOPY * C::A_TILE + (mm * C::NCOPY + c) * C::B_TILE;
+              uint8_t* dst = sbase + C::NA * C::NCOPY * C::A_TILE + (slot * C::NCOPY + c) * C::B_TILE;
 #pragma unroll
               for (int at = 0; at < C::NATOM; ++at)
                 tma_load_2d_hint(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
@@ -670,6 +687,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         }
         __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -732,7 +750,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         wc.wait(3, &tmem_empty[as], ((it >> 1) & 1) ^ 1, dbg_on);
       tc_fence_after();
       const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
-      for (int s = s0; s < s1; ++s) {
+      bool done = s0 >= s1;  // SPLIT: an item's stages end at the producer's kMetaLast
+      for (int s = s0; SPLIT ? !done : s < s1; ++s) {
         uint32_t meta = 0;
         if constexpr (kWaiter) {
           const int i = (s - s0) & 31;
@@ -765,6 +784,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           wc.wait(2, &full[stage], phase, dbg_on);
           tc_fence_after();
           meta = ld_shared_u32(&stage_meta[stage]);  // the producer's recipe
+          if (SPLIT) done = (meta & kMetaLast) != 0;
         }
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
@@ -789,7 +809,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
                 const uint32_t d = dh + acc_i * B;
                 const uint64_t a_hi = ad + ((a_i * C::NCOPY * C::A_TILE) >> 4);
                 const uint64_t a_lo = a_hi + (C::A_TILE >> 4);
-                const uint64_t b_hi = bd + ((mm * C::NCOPY * C::B_TILE) >> 4);
+                const uint64_t b_hi = bd + (((SPLIT ? 0 : mm) * C::NCOPY * C::B_TILE) >> 4);
                 const uint64_t b_lo = b_hi + (C::B_TILE >> 4);
                 const uint32_t init =
                     (meta & (mm == 0 ? kMetaAccFirst : kMetaAccSecond)) ? 1u : 0u;
@@ -873,11 +893,11 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       }
 #pragma unroll
       for (int h = 0; h < TM; ++h) {
-        uint8_t* stg = staging + ((it * TM + h) & 1) * C::OUT_TILE;
+        uint8_t* stg = staging + ((it * TM + h) % C::OUT_BUFS) * C::OUT_TILE;
         const uint32_t tacc =
             tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
         const int row0 = t * C::TROWS + h * C::BM;
-        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(
+        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS>(
             p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
             IN_ST ? in_staging + h * C::OUT_TILE : nullptr);
         if (h == TM - 1) {  // every TMEM read of this accumulator stage is done
