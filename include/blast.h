@@ -138,6 +138,9 @@ int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
 int blast_mlp_forward_fused(const void* x, int64_t m, const blast_bcsc_t* gate,
                             const blast_bcsc_t* up, const blast_bcsc_t* down,
                             const blast_mlp_plan_t* plan, void* y, void* stream);
+/* out[c] = sum_r x[r, c] (fp32) of a row-major [m, n] bf16 / f32 matrix: bias gradients of
+ * layers with bias (GPT2MLP integration). Deterministic (fixed row splits, fixed order). */
+int blast_column_sums(const void* x, int dtype, int64_t m, int64_t n, float* out, void* stream);
 /* blast_mlp_forward on HOST buffers, the reference's boundary (mlp.py:102 takes and returns
  * ndarrays): x_host [m, e] and y_host [m, e] in the network dtype. The tokens are cut into
  * chunks of chunk_tokens rows (0: automatic) and the host->device copy of chunk c+1, the
@@ -171,6 +174,15 @@ int blast_mlp_backward_dgrad(const void* dy, int64_t m, const void* gate_pre,
 int blast_block_wgrad(const void* a, const void* d, int64_t m, int64_t rows, int64_t cols,
                       int32_t block, int dtype, const int64_t* col_ptr, const int32_t* row_idx,
                       int64_t nnzb, float* out_blocks, float* dense_out, void* stream);
+/* The stored-block mode's work list depends only on the structure: build it once
+ * (items: int4[nnzb], counts: int64[grid_cols + 1]; b = 64 or 128) and reuse it with
+ * blast_block_wgrad_planned until the mask changes. Same results as blast_block_wgrad. */
+int blast_wgrad_plan(const int64_t* col_ptr, int64_t grid_rows, int64_t grid_cols, int32_t block,
+                     int32_t* items, int64_t* counts, void* stream);
+int blast_block_wgrad_planned(const void* a, const void* d, int64_t m, int64_t rows,
+                              int64_t cols, int32_t block, int dtype, const int64_t* col_ptr,
+                              const int32_t* row_idx, int64_t nnzb, const int32_t* items,
+                              const int64_t* counts, float* out_blocks, void* stream);
 
 /* ---------------------------------------------------------------- prune-and-grow */
 /* Frobenius norm per b x b block in float64 (pruner.py:88-98); zero-padded edges.

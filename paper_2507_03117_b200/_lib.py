@@ -60,6 +60,7 @@ _PROTOS = {
     "blast_mlp_forward": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                     C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp, vp, vp,
                                     vp]),
+    "blast_column_sums": (C.c_int, [vp, C.c_int, i64, i64, vp, vp]),
     "blast_mlp_forward_fused": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                           C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp]),
     "blast_mlp_forward_host": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
@@ -72,6 +73,9 @@ _PROTOS = {
                                            C.POINTER(MlpPlanDesc), vp, vp, vp, vp]),
     "blast_block_wgrad": (C.c_int, [vp, vp, i64, i64, i64, i32, C.c_int, vp, vp, i64, vp, vp,
                                     vp]),
+    "blast_wgrad_plan": (C.c_int, [vp, i64, i64, i32, vp, vp, vp]),
+    "blast_block_wgrad_planned": (C.c_int, [vp, vp, i64, i64, i64, i32, C.c_int, vp, vp, i64,
+                                            vp, vp, vp, vp]),
     "blast_block_norms": (C.c_int, [vp, vp, i64, i64, i32, C.c_int, vp, vp, vp]),
     "blast_topk_mask": (C.c_int, [vp, i64, i64, i64, vp, vp]),
     "blast_topk_mask2": (C.c_int, [vp, vp, i64, i64, i64, vp, vp, vp]),

@@ -95,6 +95,20 @@ class BlockSparseMatrix:
                                           by_rows)
         return self._cache[key]
 
+    def wgrad_plan(self):
+        """(items, counts) of the stored-block weight-gradient work list (blast_wgrad_plan),
+        cached with the structure like the product plans; None when b is not 64 / 128."""
+        if self.block not in (64, 128) or self.nnzb == 0:
+            return None
+        if "wgrad" not in self._cache:
+            items = torch.empty(self.nnzb, 4, dtype=torch.int32, device=A.DEVICE)
+            counts = torch.empty(self.grid_cols + 1, dtype=torch.int64, device=A.DEVICE)
+            L.check(L.load().blast_wgrad_plan(self.col_ptr.data_ptr(), self.grid_rows,
+                                              self.grid_cols, self.block, items.data_ptr(),
+                                              counts.data_ptr(), L.stream()), "wgrad_plan")
+            self._cache["wgrad"] = (items, counts)
+        return self._cache["wgrad"]
+
     def _tf32(self):
         if "tf32" not in self._cache:
             v = self.values

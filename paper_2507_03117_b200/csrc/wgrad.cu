@@ -362,10 +362,51 @@ static int launch_wgrad_tc(const void* a, const void* d, const WgradParams& p, c
 
 using namespace blast;
 
+static int block_wgrad_impl(const void* a, const void* d, int64_t m, int64_t rows, int64_t cols,
+                            int32_t block, int dtype, const int64_t* col_ptr,
+                            const int32_t* row_idx, int64_t nnzb, float* out_blocks,
+                            float* dense_out, const int32_t* plan_items,
+                            const int64_t* plan_counts, void* stream);
+
 extern "C" int blast_block_wgrad(const void* a, const void* d, int64_t m, int64_t rows,
                                  int64_t cols, int32_t block, int dtype, const int64_t* col_ptr,
                                  const int32_t* row_idx, int64_t nnzb, float* out_blocks,
                                  float* dense_out, void* stream) {
+  return block_wgrad_impl(a, d, m, rows, cols, block, dtype, col_ptr, row_idx, nnzb, out_blocks,
+                          dense_out, nullptr, nullptr, stream);
+}
+
+extern "C" int blast_wgrad_plan(const int64_t* col_ptr, int64_t grid_rows, int64_t grid_cols,
+                                int32_t block, int32_t* items, int64_t* counts, void* stream) {
+  if (!col_ptr || !items || !counts || grid_cols < 1 || (block != 64 && block != 128)) {
+    set_error("wgrad_plan: col_ptr, items, counts required; block 64 or 128");
+    return BLAST_EINVAL;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int per_item = block == 64 ? 2 : 1;
+  const int thr = 256, blk = static_cast<int>(cdiv(grid_cols, thr));
+  wgrad_item_count_kernel<<<blk, thr, 0, st>>>(col_ptr, grid_rows, grid_cols, per_item, counts);
+  offsets_scan_kernel<int64_t><<<1, 1024, 0, st>>>(counts, grid_cols);
+  wgrad_items_kernel<<<blk, thr, 0, st>>>(col_ptr, grid_rows, grid_cols, per_item, counts,
+                                          reinterpret_cast<int4*>(items));
+  return check_launch("wgrad_plan");
+}
+
+extern "C" int blast_block_wgrad_planned(const void* a, const void* d, int64_t m, int64_t rows,
+                                         int64_t cols, int32_t block, int dtype,
+                                         const int64_t* col_ptr, const int32_t* row_idx,
+                                         int64_t nnzb, const int32_t* items,
+                                         const int64_t* counts, float* out_blocks,
+                                         void* stream) {
+  return block_wgrad_impl(a, d, m, rows, cols, block, dtype, col_ptr, row_idx, nnzb, out_blocks,
+                          nullptr, items, counts, stream);
+}
+
+static int block_wgrad_impl(const void* a, const void* d, int64_t m, int64_t rows, int64_t cols,
+                            int32_t block, int dtype, const int64_t* col_ptr,
+                            const int32_t* row_idx, int64_t nnzb, float* out_blocks,
+                            float* dense_out, const int32_t* plan_items,
+                            const int64_t* plan_counts, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rows < 1 || cols < 1 || block < 1 || m < 0) {
     set_error("block_wgrad: invalid shape");
@@ -399,15 +440,20 @@ extern "C" int blast_block_wgrad(const void* a, const void* d, int64_t m, int64_
   if (tc) {
     const int per_item = block == 64 ? 2 : 1;
     Scratch sp, si;
-    if (!sp.alloc(sizeof(int64_t) * (gc + 1), st)) return cuda_status(cudaGetLastError(), "wgrad");
-    if (!si.alloc(sizeof(int4) * nsel, st)) return cuda_status(cudaGetLastError(), "wgrad");
-    const int thr = 256, blk = static_cast<int>(cdiv(gc, thr));
-    wgrad_item_count_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>());
-    offsets_scan_kernel<int64_t><<<1, 1024, 0, st>>>(sp.as<int64_t>(), gc);
-    wgrad_items_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>(), si.as<int4>());
+    if (plan_items && plan_counts && !dense) {  // item list cached with the matrix structure
+      p.n_items_dev = plan_counts + gc;
+      p.items = reinterpret_cast<const int4*>(plan_items);
+    } else {
+      if (!sp.alloc(sizeof(int64_t) * (gc + 1), st)) return cuda_status(cudaGetLastError(), "wgrad");
+      if (!si.alloc(sizeof(int4) * nsel, st)) return cuda_status(cudaGetLastError(), "wgrad");
+      const int thr = 256, blk = static_cast<int>(cdiv(gc, thr));
+      wgrad_item_count_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>());
+      offsets_scan_kernel<int64_t><<<1, 1024, 0, st>>>(sp.as<int64_t>(), gc);
+      wgrad_items_kernel<<<blk, thr, 0, st>>>(cp, gr, gc, per_item, sp.as<int64_t>(), si.as<int4>());
+      p.n_items_dev = sp.as<int64_t>() + gc;
+      p.items = si.as<int4>();
+    }
     p.n_items = static_cast<int32_t>((nsel + gc + per_item - 1) / per_item);
-    p.n_items_dev = sp.as<int64_t>() + gc;
-    p.items = si.as<int4>();
     // split-K when the blocks cannot fill the GPU (e.g. GPT-2 small at 90%: ~60 blocks)
     const int ksteps = static_cast<int>(cdiv(m, 64));
     int n_split = 1;

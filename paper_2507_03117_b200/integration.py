@@ -21,7 +21,7 @@ from torch import nn
 
 from . import bcsc
 from .bcsc import BlockMask, BlockSparseMatrix
-from .kernels import bspmm_act_save, bspmm_fused, bspmm_rt, bspmm_rt_act_grad
+from .kernels import bspmm_act_save, bspmm_fused, bspmm_rt, bspmm_rt_act_grad, column_sums
 from .mlp import SparseMlp, _wgrad, mlp_backward, mlp_forward
 from .pruner import block_norms, prune_s
 
@@ -102,8 +102,7 @@ class _GeluFn(torch.autograd.Function):
         dv2 = _wgrad(hid, dy, w2.rows, w2.cols, w2, full=False)
         dv1 = _wgrad(x2d, dpre, w1.rows, w1.cols, w1, full=False)
         # bias gradients: column sums accumulated in fp32 straight from the bf16 tensors
-        return (dx, None, torch.sum(dpre, 0, dtype=torch.float32), None,
-                torch.sum(dy, 0, dtype=torch.float32),
+        return (dx, None, column_sums(dpre), None, column_sums(dy),
                 dv1.to(w1.values.dtype), dv2.to(w2.values.dtype))
 
 

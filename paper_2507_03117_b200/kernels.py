@@ -127,6 +127,17 @@ def _product(x, w: BlockSparseMatrix, act: int, transposed: bool, bias=None):
     return A.like_input(y, host)
 
 
+def column_sums(x: torch.Tensor) -> torch.Tensor:
+    """fp32 sums over the rows of a [m, n] CUDA tensor (bias gradients), deterministic."""
+    if x.dim() != 2 or not x.is_cuda or x.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("column_sums expects a 2-D bf16/fp32 CUDA tensor")
+    x = x.contiguous()
+    out = torch.empty(x.shape[1], dtype=torch.float32, device=x.device)
+    L.check(L.load().blast_column_sums(x.data_ptr(), L.dtype_code(x.dtype), x.shape[0],
+                                       x.shape[1], out.data_ptr(), L.stream()), "column_sums")
+    return out
+
+
 def bspmm_act_save(x: torch.Tensor, w: BlockSparseMatrix, f: str, bias=None):
     """(f(X @ W + bias), X @ W + bias) in one launch: the activation and the
     pre-activation the backward needs (device tensors)."""

@@ -238,10 +238,17 @@ def _wgrad(a: torch.Tensor, d: torch.Tensor, rows: int, cols: int, w: BlockSpars
         return out
     out = torch.empty(w.nnzb, b, b, dtype=torch.float32, device=A.DEVICE)
     if w.nnzb:
-        L.check(lib.blast_block_wgrad(a.data_ptr(), d.data_ptr(), m, rows, cols, b,
-                                      L.dtype_code(a.dtype), w.col_ptr.data_ptr(),
-                                      w.block_row_idx.data_ptr(), w.nnzb, out.data_ptr(), None,
-                                      L.stream()), "wgrad")
+        plan = w.wgrad_plan() if a.dtype == torch.bfloat16 else None
+        if plan is not None:  # work list cached with the structure
+            L.check(lib.blast_block_wgrad_planned(
+                a.data_ptr(), d.data_ptr(), m, rows, cols, b, L.dtype_code(a.dtype),
+                w.col_ptr.data_ptr(), w.block_row_idx.data_ptr(), w.nnzb, plan[0].data_ptr(),
+                plan[1].data_ptr(), out.data_ptr(), L.stream()), "wgrad")
+        else:
+            L.check(lib.blast_block_wgrad(a.data_ptr(), d.data_ptr(), m, rows, cols, b,
+                                          L.dtype_code(a.dtype), w.col_ptr.data_ptr(),
+                                          w.block_row_idx.data_ptr(), w.nnzb, out.data_ptr(), None,
+                                          L.stream()), "wgrad")
     return out
 
 

@@ -89,3 +89,17 @@ def test_sparsify_llama_model_runs_and_matches_masked_dense():
         logits = model(ids).logits
     assert torch.isfinite(logits).all()
     assert sum(isinstance(l.mlp, integration.SparseGatedMLP) for l in model.model.layers) == 2
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("m,n", [(1, 1), (7, 3), (300, 769), (8192, 3072), (4096, 768)])
+def test_column_sums(dtype, m, n):
+    """Bias-gradient column sums: fp32 accumulation, deterministic, against an fp64 reference."""
+    from paper_2507_03117_b200.kernels import column_sums
+    torch.manual_seed(m * 31 + n)
+    x = torch.randn(m, n, device="cuda").to(dtype)
+    got = column_sums(x)
+    ref = x.double().sum(0)
+    scale = x.double().abs().sum(0).clamp_min(1e-30)
+    assert ((got.double() - ref).abs() / scale).max().item() <= 1e-5
+    assert torch.equal(got, column_sums(x))  # run-to-run bitwise
