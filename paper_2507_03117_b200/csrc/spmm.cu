@@ -107,11 +107,11 @@ static SpmmParams make_params(const EngineCall& c) {
 }
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
-          int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
+          int OUT_ELT = 0, int TM = 1, int SPLIT = 0, int CL = 1>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
   using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM, IN_ST, SPLIT>;
-  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM, SPLIT>;
+  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM, SPLIT, CL>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -169,14 +169,41 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   if (!ok) return BLAST_EINVAL;
   SpmmParams p = make_params(c);
   p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
-  const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
+  const int64_t items = cdiv(p.n_tok_tiles, CL) * p.n_lines;  // per cluster
   if (items <= 0) return BLAST_OK;
-  const int grid = static_cast<int>(items < num_sms() ? items : num_sms());
+  int64_t clusters = std::min<int64_t>(items, num_sms() / CL);
   dbg_begin(st);
-  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo,
-                                                  mW1, mW1lo, p);
+  if constexpr (CL > 1) {
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // persistent clusters: no more than can be resident at once (GPCs may not split evenly)
+    static int max_clusters = 0;
+    if (max_clusters == 0) {
+      cfg.gridDim = dim3(static_cast<unsigned>(num_sms() / CL * CL));
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess ||
+          max_clusters <= 0)
+        max_clusters = num_sms() / CL;
+      cudaGetLastError();
+    }
+    clusters = std::min<int64_t>(clusters, max_clusters);
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
+    cudaLaunchKernelEx(&cfg, kern, mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
+  } else {
+    const int grid = static_cast<int>(clusters);
+    kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo,
+                                                    mW1, mW1lo, p);
+  }
   const int rc = check_launch("spmm_tc");
-  dbg_end("spmm_tc", st, grid);
+  dbg_end("spmm_tc", st, static_cast<int>(clusters * CL));
   return rc;
 }
 
@@ -228,6 +255,18 @@ static bool split_stages() {
   }
   return v == 1;
 }
+// Clusters of two CTAs sharing weight blocks through TMA multicast (spmm_tc_kernel CL = 2) for
+// the 256-token forward products. Measured slower on cfg3 (gate+up 243 vs 232 us, down 123 vs
+// 119 us: the lockstep coupling of the pair costs more than the 10 % fewer L2 -> SM bytes), so
+// opt-in: BLAST_CLUSTER_W=1.
+static bool cluster_weights() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_CLUSTER_W");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 // 256-token items (TcCfg TM = 2) for the forward products; BLAST_WIDE_TILES=0 disables.
 static bool wide_tiles() {
   static int v = -1;
@@ -253,7 +292,9 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>()) {
         if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2>())
           if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles())
-            return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO, 2>(c, a0lo, a1lo, st);
+            return (c.m >= 512 && cluster_weights())
+                       ? launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO, 2, 0, 2>(c, a0lo, a1lo, st)
+                       : launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
           if (use_staged<B, ELT, NPASS, 1, false>(c))
             return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
@@ -265,6 +306,8 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
             return split_stages()
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 1>(c, a0lo, a1lo, st)
+                   : (c.m >= 512 && cluster_weights())
+                       ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 0, 2>(c, a0lo, a1lo, st)
                        : launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 2, false>())
           if (use_staged<B, ELT, NPASS, 2, false>(c))

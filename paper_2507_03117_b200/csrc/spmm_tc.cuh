@@ -530,8 +530,12 @@ constexpr int kEpiWarps = kEpiWarpsT;
 template <int EPI, int OUT_ELT>
 constexpr int in_staged() { return (EPI == EPI_GATED_BWD && OUT_ELT > 0) ? 1 : 0; }
 
+// CL = 2: launched as clusters of two CTAs that work on the same output line for two
+// consecutive token tiles in lockstep; each weight block is read from L2 once and multicast
+// into both CTAs' stages (halving the weight share of the L2 -> SM bytes), and every MMA
+// commit releases the stage in both CTAs (empty barriers count 2 arrivals).
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
-          int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
+          int OUT_ELT = 0, int TM = 1, int SPLIT = 0, int CL = 1>
 __global__ void __launch_bounds__(kTcThreads, 1)
 spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapI,
                const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
@@ -560,7 +564,18 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
-  const int n_items = p.n_tok_tiles * p.n_lines;
+  // items: CL = 1: (token tile, line); CL = 2: (pair of token tiles, line), this CTA's tile is
+  // 2 * pair + rank (a tile past the end runs on zero-filled rows, stores clipped)
+  const uint32_t crank = CL > 1 ? cluster_ctarank() : 0u;
+  const int n_items = ((p.n_tok_tiles + CL - 1) / CL) * p.n_lines;
+  const int i0 = static_cast<int>(blockIdx.x) / CL, istep = static_cast<int>(gridDim.x) / CL;
+  auto tile_of = [&](int item) -> int {
+    if (CL == 1) return item_tile(p, item);
+    const int np = (p.n_tok_tiles + CL - 1) / CL;
+    int pt = item / p.n_lines;
+    if (p.reverse_tiles) pt = np - 1 - pt;
+    return pt * CL + static_cast<int>(crank);
+  };
 
   if (warp == 0 && lane == 0) {
     if (OUT_ELT) tma_prefetch(&mapO);
@@ -570,7 +585,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     if (SUMACC) tma_prefetch(&mapA1);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
@@ -584,7 +599,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     tmem_relinquish();
   }
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   WaitClock wc;
@@ -617,16 +635,16 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       const int idx = nx_s0 + static_cast<int>(lane);
       nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
     };
-    prefetch(blockIdx.x);
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int t = item_tile(p, item);
+    prefetch(i0);
+    for (int item = i0; item < n_items; item += istep) {
+      const int t = tile_of(item);
       const int s0 = nx_s0, s1 = nx_s1;
       StepCursor cur;
       cur.steps = p.steps;
       cur.end = s1;
       cur.base = s0;
       cur.mine = nx_first;
-      prefetch(item + gridDim.x);
+      prefetch(item + istep);
       uint32_t init0 = 0, init1 = 0;  // accumulator i already holds a partial sum
       for (int s = s0; s < s1; ++s) {
         const int4 st = cur.get(s);
@@ -679,9 +697,17 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             for (int c = 0; c < C::NCOPY; ++c) {
               uint8_t* dst = sbase + C::NA * C::NCOPY * C::A_TILE + (slot * C::NCOPY + c) * C::B_TILE;
 #pragma unroll
-              for (int at = 0; at < C::NATOM; ++at)
-                tma_load_2d_hint(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
-                                 at * C::SWE, kb[mm] * B, pol_w);
+              for (int at = 0; at < C::NATOM; ++at) {
+                if constexpr (CL > 1) {
+                  if (crank == 0)
+                    tma_load_2d_mc(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
+                                   at * C::SWE, kb[mm] * B, static_cast<uint16_t>((1u << CL) - 1u),
+                                   pol_w);
+                } else {
+                  tma_load_2d_hint(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
+                                   at * C::SWE, kb[mm] * B, pol_w);
+                }
+              }
             }
           }
         }
@@ -737,12 +763,12 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
       }
     };
-    prefetch(blockIdx.x);
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    prefetch(i0);
+    for (int item = i0; item < n_items; item += istep, ++it) {
       const uint32_t as = it & 1;
       const int s0 = nx_s0, s1 = nx_s1;
       int4 mine = nx_first;
-      prefetch(item + gridDim.x);
+      prefetch(item + istep);
       uint32_t m0 = 0, m1 = 0, seen0 = 0, seen1 = 0;
       if constexpr (kWaiter)
         named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
@@ -830,7 +856,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
               }
             }
           }
-          mma_commit(&empty[stage]);
+          if constexpr (CL > 1)
+            mma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << CL) - 1u));
+          else
+            mma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -843,7 +872,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     // Mirrors the MMA warp's item / step sequence: waits on the accumulator-free and
     // stage-full mbarriers and releases the MMA warp through named barriers.
     uint32_t stage = 0, phase = 0, it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    for (int item = i0; item < n_items; item += istep, ++it) {
       const uint32_t as = it & 1, use = it >> 1;
       const int j = item % p.n_lines;
       const int n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
@@ -865,8 +894,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     const uint64_t pol_out = policy_evict_first();
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int t = item_tile(p, item);
+    for (int item = i0; item < n_items; item += istep, ++it) {
+      const int t = tile_of(item);
       const int j = item % p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
       const int flags = __ldg(&p.line_flags[j]);
@@ -915,7 +944,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 
   if (warp == 0 || warp == 2 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync();  // no CTA leaves while its peer may still multicast into it
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
