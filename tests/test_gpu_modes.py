@@ -1,0 +1,64 @@
+"""Opt-in engine modes (read once per process from the environment) give bitwise the same
+MLP forward as the default engine: split stages, cluster weight multicast, the CTA-pair engine,
+the fused gate+up->down kernel, and the narrow-tile / direct-store fallbacks. Each mode runs in
+a subprocess."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import oracle
+import paper_2507_03117_b200 as bs
+rng = np.random.default_rng(5)
+mats = []
+for rows, cols in ((1024, 3072), (1024, 3072), (3072, 1024)):
+    w = oracle.random_bcsc(rows, cols, 64, 0.85, rng)
+    w = w._replace(values=(w.values / np.sqrt(rows)).astype(np.float32))
+    mats.append(bs.from_host(w, torch.bfloat16))
+net = bs.SparseMlp.from_caches(*mats)
+x = torch.from_numpy(rng.standard_normal(({m}, 1024)).astype(np.float32)).cuda().bfloat16()
+y, _ = bs.mlp_forward(x, net, save_activations=False)
+y2, acts = bs.mlp_forward(x, net, save_activations=True)
+torch.cuda.synchronize()
+np.save({out!r}, torch.stack([y.float(), y2.float()]).cpu().numpy())
+"""
+
+MODES = {
+    "default": {},
+    "split": {"BLAST_SPLIT_STAGES": "1"},
+    "cluster": {"BLAST_CLUSTER_W": "1"},
+    "pair": {"BLAST_PAIR_ENGINE": "1"},
+    "fused": {"BLAST_FUSED_MLP": "1"},
+    "narrow": {"BLAST_WIDE_TILES": "0"},
+    "direct": {"BLAST_DIRECT_STORES": "1"},
+}
+
+
+def run_mode(env_extra, m, tmp_path, name):
+    out = str(tmp_path / f"{name}_{m}.npy")
+    env = dict(os.environ, **env_extra)
+    code = SCRIPT.format(root=str(ROOT), m=m, out=out)
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    return np.load(out)
+
+
+@pytest.mark.parametrize("m", [1000, 4096])
+def test_modes_bitwise_equal(m, tmp_path):
+    ref = run_mode(MODES["default"], m, tmp_path, "default")
+    for name, env in MODES.items():
+        if name == "default":
+            continue
+        got = run_mode(env, m, tmp_path, name)
+        assert np.array_equal(got, ref), name
