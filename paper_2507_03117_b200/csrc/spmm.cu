@@ -241,7 +241,7 @@ constexpr bool staged_fits() {
   constexpr int b_tile = (B * rowb + 1023) / 1024 * 1024;
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
-  constexpr int staging = (2 + IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
+  constexpr int staging = (2 + 2 * IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
   return (232448 - 1024 - 512 - staging) / stage >= 3;
 }
 // gate+up with one weight block per stage and single-buffered output staging (TcCfg SPLIT):

@@ -124,8 +124,8 @@ struct StepCursor {
 // its weight block(s) are loaded once for both halves, and each half accumulates into its
 // own TMEM columns (twice the MMAs per pipeline round trip, half the weight traffic).
 // IN_ST = 1 (staged single-input activation-derivative epilogue): the epilogue also stages the
-// item's `in0` tiles (TM x 128 rows x B) in shared memory with one TMA load per tile, issued
-// before it waits for the accumulator, instead of row-strided per-thread loads.
+// items' `in0` tiles (TM x 128 rows x B) in shared memory with one TMA load per tile, one item
+// ahead (double-buffered), instead of row-strided per-thread loads.
 // SPLIT = 1 (gate+up): a stage carries ONE weight block; a step with both a gate and an up
 // block becomes two stages (the panel is loaded twice, ~5 % of steps at 90 % sparsity), and
 // the output is staged single-buffered. The 16 + 16 KB saved buy a fifth pipeline stage,
@@ -153,7 +153,7 @@ struct TcCfg {
   static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
   static constexpr int OUT_TILE = OUT_ELT ? round1k(BM * OUT_ROWB) : 0;
-  static constexpr int IN_STAGING = IN_ST ? TM * OUT_TILE : 0;
+  static constexpr int IN_STAGING = IN_ST ? 2 * TM * OUT_TILE : 0;  // double-buffered by item
   static constexpr int STAGING = OUT_BUFS * OUT_TILE + IN_STAGING;
   // 227 KB opt-in maximum minus barriers, alignment slack and the output staging
   static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 512 - STAGING : 200 * 1024;
@@ -559,8 +559,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   // per-stage MMA recipe (when the MMA warp waits on the mbarriers itself): written by the
   // producer before its expect_tx arrive (release), read after the full wait (acquire)
   uint32_t* stage_meta = tmem_slot + 4;
-  uint64_t* in_full = reinterpret_cast<uint64_t*>(stage_meta + 8);  // staged in0 tiles landed
-  uint8_t* in_staging = staging + C::OUT_BUFS * C::OUT_TILE;        // [TM][OUT_TILE] (IN_ST)
+  uint64_t* in_full = reinterpret_cast<uint64_t*>(stage_meta + 8);  // [2] staged in0 landed
+  uint8_t* in_staging = staging + C::OUT_BUFS * C::OUT_TILE;        // [2][TM][OUT_TILE] (IN_ST)
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -591,7 +591,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], kEpiWarps);
     }
-    mbar_init(in_full, 1);
+    mbar_init(&in_full[0], 1);
+    mbar_init(&in_full[1], 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -900,20 +901,28 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       const uint32_t as = it & 1, use = it >> 1;
       const int flags = __ldg(&p.line_flags[j]);
       if constexpr (IN_ST) {
-        // this item's in0 tiles (the previous item's were consumed before its last barrier)
-        if (etid == 0) {
-          mbar_expect_tx(in_full, TM * C::BM * C::OUT_ROWB);
+        // in0 tiles one item ahead: this item's were requested during the previous item (or
+        // here for the first); the buffer of the next one was last read by the previous item,
+        // whose reads all precede its final barrier
+        auto load_in = [&](int itm, uint32_t buf) {
+          const int tt = tile_of(itm), jj = itm % p.n_lines;
+          mbar_expect_tx(&in_full[buf], TM * C::BM * C::OUT_ROWB);
 #pragma unroll
           for (int h = 0; h < TM; ++h)
 #pragma unroll
             for (int a = 0; a < C::OUT_NATOM; ++a)
-              tma_load_2d(in_staging + h * C::OUT_TILE + a * (C::BM * C::OUT_SW), &mapI, in_full,
-                          j * B + a * (C::OUT_SW / OUT_ELT), t * C::TROWS + h * C::BM);
+              tma_load_2d(in_staging + (buf * TM + h) * C::OUT_TILE + a * (C::BM * C::OUT_SW),
+                          &mapI, &in_full[buf], jj * B + a * (C::OUT_SW / OUT_ELT),
+                          tt * C::TROWS + h * C::BM);
+        };
+        if (etid == 0) {
+          if (it == 0) load_in(item, 0);
+          if (item + istep < n_items) load_in(item + istep, (it + 1) & 1);
         }
       }
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
-      if constexpr (IN_ST) mbar_wait(in_full, it & 1);
+      if constexpr (IN_ST) mbar_wait(&in_full[it & 1], (it >> 1) & 1);
       if (p.skip_epilogue) {  // diagnosis: release the accumulator unread
         tc_fence_before();
         __syncwarp();
@@ -928,7 +937,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         const int row0 = t * C::TROWS + h * C::BM;
         epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS>(
             p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
-            IN_ST ? in_staging + h * C::OUT_TILE : nullptr);
+            IN_ST ? in_staging + ((it & 1) * TM + h) * C::OUT_TILE : nullptr);
         if (h == TM - 1) {  // every TMEM read of this accumulator stage is done
           tc_fence_before();
           __syncwarp();
