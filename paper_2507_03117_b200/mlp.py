@@ -288,3 +288,39 @@ def mlp_backward(dy, acts: MlpActivations, mlp: SparseMlp, grad_mode: str = "ful
     if host:
         return tuple(A.to_host(t) for t in (dx, d_gate, d_up, d_down))
     return dx, d_gate, d_up, d_down
+
+
+class GraphedMlpForward:
+    """Inference forward captured once in a CUDA graph for a fixed token count (serving /
+    decode): every kernel of mlp_forward(save_activations=False) replays without host launch
+    work. Results are bitwise those of the eager call. The structure of ``mlp`` must not
+    change after capture (a mask refresh needs a new instance); weight values may.
+
+    Measured on one B200 (tools/graph_probe.py, Llama-3-8B MLP at 95 %): 128 tokens 36 -> 18.5
+    us per forward, 8192 tokens 218 -> 216 us."""
+
+    def __init__(self, mlp: SparseMlp, tokens: int):
+        if tokens <= 0:
+            raise ValueError("tokens must be positive")
+        self.mlp = mlp
+        self.x = torch.zeros(tokens, mlp.embed_dim, dtype=mlp.dtype, device=A.DEVICE)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # build plans, configure kernels, warm the pools
+            for _ in range(2):
+                mlp_forward(self.x, mlp, save_activations=False)
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.y, _ = mlp_forward(self.x, mlp, save_activations=False)
+
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        """y = mlp(x) for x of shape [tokens, embed_dim]; returns the graph's output buffer
+        (overwritten by the next call)."""
+        if tuple(x.shape) != tuple(self.x.shape):
+            raise ValueError(f"graphed forward was captured for {tuple(self.x.shape)}, "
+                             f"got {tuple(x.shape)}")
+        self.x.copy_(x)
+        self.graph.replay()
+        return self.y
+

@@ -258,3 +258,25 @@ class TestBackward:
         g2 = bs.mlp_backward(dy, acts, net)
         for a, b in zip(g1, g2):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("m", [128, 300, 1024])
+def test_graphed_forward_equals_eager(m):
+    """CUDA-graph capture of the inference forward: bitwise the eager result, reusable."""
+    rng = np.random.default_rng(m)
+    mats = []
+    for rows, cols in ((512, 1536), (512, 1536), (1536, 512)):
+        w = oracle.random_bcsc(rows, cols, 64, 0.9, rng)
+        w = w._replace(values=(w.values / np.sqrt(rows)).astype(np.float32))
+        mats.append(bs.from_host(w, torch.bfloat16))
+    net = bs.SparseMlp.from_caches(*mats)
+    fwd = bs.GraphedMlpForward(net, m)
+    for seed in (1, 2):
+        x = torch.from_numpy(np.random.default_rng(seed).standard_normal((m, 512))
+                             .astype(np.float32)).cuda().bfloat16()
+        y_eager, _ = bs.mlp_forward(x, net, save_activations=False)
+        y_graph = fwd(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y_graph, y_eager)
+    with pytest.raises(ValueError, match="captured for"):
+        fwd(torch.zeros(m + 1, 512, device="cuda", dtype=torch.bfloat16))
