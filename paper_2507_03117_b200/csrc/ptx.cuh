@@ -364,6 +364,11 @@ __device__ __forceinline__ void bulk_wait_group() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Blocks until the grid this one depends on (launched with programmatic stream serialization)
+// has completed and its memory is visible; a no-op for a normal launch.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- misc
 // Shared-memory word read that the compiler cannot hoist above a preceding barrier wait
 // (asm volatile + memory clobber), issued as LDS rather than a generic strong load.

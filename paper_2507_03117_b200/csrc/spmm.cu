@@ -106,6 +106,16 @@ static SpmmParams make_params(const EngineCall& c) {
   return p;
 }
 
+// Programmatic dependent launch for the tensor-core engine; BLAST_PDL=0 disables.
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
           int OUT_ELT = 0, int TM = 1, int SPLIT = 0, int CL = 1>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
@@ -198,9 +208,19 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
     cudaLaunchKernelEx(&cfg, kern, mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
   } else {
-    const int grid = static_cast<int>(clusters);
-    kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo,
-                                                    mW1, mW1lo, p);
+    // programmatic dependent launch: this grid's CTAs start their setup on SMs freed by the
+    // previous kernel's tail and wait in-kernel (griddep_wait) for its completion
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters));
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
   }
   const int rc = check_launch("spmm_tc");
   dbg_end("spmm_tc", st, static_cast<int>(clusters * CL));

@@ -606,6 +606,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Everything above (barriers, TMEM, descriptor prefetch) may overlap the previous kernel's
+  // tail under programmatic dependent launch; nothing below runs before it has completed.
+  griddep_wait();
   WaitClock wc;
 #ifdef BLAST_WAIT_COUNTERS
   const bool dbg_on = p.dbg != nullptr;
