@@ -51,9 +51,17 @@ def _compile(src: Path) -> Path:
 
 
 def build(force: bool = False, verbose: bool = True) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    stamp = BUILD / "flags.txt"
+    flags = " ".join(ARCH + FLAGS)
+    if stamp.exists() and stamp.read_text() != flags:  # new flags: rebuild everything
+        force = True
+    if force:
+        for o in BUILD.glob("*.o"):
+            o.unlink()
+    stamp.write_text(flags)
     if not force and LIB.exists() and LIB.stat().st_mtime >= _newest_input():
         return LIB
-    BUILD.mkdir(exist_ok=True)
     srcs = _sources()
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(_compile, srcs))

@@ -100,7 +100,7 @@ __global__ void plan_fill_kernel(const int32_t* kmap0, const int32_t* kmap1, int
   const int lane = threadIdx.x & 31;
   if (line >= lines) return;
   int out = step_ptr[line];
-  int f = 0;
+  int f = 0, seen = 0;  // seen: warp-uniform, matrices with a block in earlier chunks
   for (int64_t base = 0; base < inner; base += 32) {
     const int64_t i = base + lane;
     int k0 = -1, k1 = -1;
@@ -111,9 +111,19 @@ __global__ void plan_fill_kernel(const int32_t* kmap0, const int32_t* kmap1, int
     }
     const bool present = k0 >= 0 || k1 >= 0;
     const unsigned bal = __ballot_sync(0xffffffffu, present);
+    // .w: presence and first-occurrence bits, so the MMA issuer reads a step's recipe
+    // with one shuffle: bit 0/1 block of matrix 0/1, bit 2/3 its first block in the line
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned bal0 = __ballot_sync(0xffffffffu, k0 >= 0);
+    const unsigned bal1 = __ballot_sync(0xffffffffu, k1 >= 0);
+    const bool first0 = k0 >= 0 && !(seen & 1) && !(bal0 & lt);
+    const bool first1 = k1 >= 0 && !(seen & 2) && !(bal1 & lt);
+    seen |= (bal0 ? 1 : 0) | (bal1 ? 2 : 0);
     if (present) {
-      const int pos = out + __popc(bal & ((1u << lane) - 1u));
-      steps[pos] = make_int4(static_cast<int>(i), k0, k1, 0);
+      const int pos = out + __popc(bal & lt);
+      steps[pos] = make_int4(static_cast<int>(i), k0, k1,
+                             (k0 >= 0 ? 1 : 0) | (k1 >= 0 ? 2 : 0) | (first0 ? 4 : 0) |
+                                 (first1 ? 8 : 0));
     }
     f |= (k0 >= 0 ? 1 : 0) | (k1 >= 0 ? 2 : 0);
     out += __popc(bal);

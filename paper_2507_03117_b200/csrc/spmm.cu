@@ -71,8 +71,9 @@ static void dbg_end(const char* name, cudaStream_t st, int ctas) {
   const double n = ctas > 0 ? ctas : 1;
   fprintf(stderr,
           "[blast dbg] %s ctas=%d per-CTA cycles: prod.wait_empty=%.0f prod.wait_wempty=%.0f "
-          "mma.wait_full=%.0f mma.wait_acc=%.0f mma.wait_w=%.0f epi.wait_acc=%.0f steps=%.0f\n",
-          name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[7] / n);
+          "mma.wait_full=%.0f mma.wait_acc=%.0f mma.loop=%.0f epi.wait_acc=%.0f mma.issue=%.0f "
+          "mma.steps=%.0f\n",
+          name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n);
 }
 
 static SpmmParams make_params(const EngineCall& c) {
@@ -82,7 +83,7 @@ static SpmmParams make_params(const EngineCall& c) {
     static int skip = -1;
     if (skip < 0) {
       const char* e = getenv("BLAST_SKIP_EPILOGUE");
-      skip = (e && e[0] == '1') ? 1 : 0;
+      skip = e ? atoi(e) & 3 : 0;  // 1: skip epilogues, 2: skip operand loads (timing only)
     }
     p.skip_epilogue = skip;
   }

@@ -47,7 +47,8 @@ struct SpmmParams {
   int64_t ld_out;   // row stride (elements) of every out*/in* array
   unsigned long long* dbg;  // optional per-role wait-cycle counters (BLAST_DEBUG_COUNTERS)
   const float* bias;        // EPI_STORE: optional per-output-column bias, added before act
-  int32_t skip_epilogue;    // diagnosis only (BLAST_SKIP_EPILOGUE=1): release accumulators unread
+  int32_t skip_epilogue;    // diagnosis only (BLAST_SKIP_EPILOGUE): 1 release accumulators unread,
+                            // 2 mark stages full without loading operands
   int32_t reverse_tiles;    // process token tiles last-to-first (reads the most recently
                             // written rows of the activations first, while they are in L2)
 };
@@ -519,8 +520,14 @@ constexpr uint32_t kBarStage = 4;  // + ring stage (<= 8 ids)
 // projection 124 -> 118 us) but loses for the gate+up product, whose 48 KB stages leave only
 // 4 in flight so the extra handoff latency is exposed (237 -> 247 us); there the MMA warp
 // waits on the mbarriers itself.
-template <int NMAT, int TM>
-constexpr bool use_waiter() { return NMAT == 1; }
+#ifndef BLAST_WAITER_GU
+#define BLAST_WAITER_GU 0
+#endif
+#ifndef BLAST_BALLOT_GU
+#define BLAST_BALLOT_GU 0
+#endif
+template <int NMAT, int TM, bool SPLIT = false>
+constexpr bool use_waiter() { return !SPLIT && (NMAT == 1 || BLAST_WAITER_GU); }
 
 // 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (two warps per TMEM lane quarter, splitting the 16-column chunks).
@@ -545,7 +552,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
                const SpmmParams p) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
   using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST, SPLIT>;
-  static_assert(!SPLIT || (NMAT == 2 && !SUMACC && NPASS == 1 && !use_waiter<NMAT, TM>()),
+  static_assert(!SPLIT || (NMAT == 2 && !SUMACC && NPASS == 1 && !use_waiter<NMAT, TM, SPLIT>()),
                 "split stages: gate+up products only");
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
   extern __shared__ uint8_t smem_raw[];
@@ -674,11 +681,17 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm)
             if (kb[mm] >= 0) bytes += C::NCOPY * (B * C::ROWB);
-          if (!use_waiter<NMAT, TM>()) stage_meta[stage] = meta;
-          mbar_expect_tx(&full[stage], bytes);
+          if (!use_waiter<NMAT, TM, SPLIT>()) stage_meta[stage] = meta;
+          if (p.skip_epilogue & 2) {  // diagnosis: MMAs run on stale shared memory
+            mbar_arrive(&full[stage]);
+            bytes = 0;
+          } else {
+            mbar_expect_tx(&full[stage], bytes);
+          }
           uint8_t* sbase = smem + stage * C::STAGE;
 #pragma unroll
           for (int a = 0; a < C::NA; ++a) {
+            if (bytes == 0) break;
             if (SUMACC && kb[a] < 0) continue;
             const CUtensorMap* mh = (a == 0) ? &mapA0 : &mapA1;
             const CUtensorMap* ml = (a == 0) ? &mapA0lo : &mapA1lo;
@@ -693,7 +706,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           }
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm) {
-            if (kb[mm] < 0) continue;
+            if (kb[mm] < 0 || bytes == 0) continue;
             const CUtensorMap* mh = (mm == 0) ? &mapW0 : &mapW1;
             const CUtensorMap* ml = (mm == 0) ? &mapW0lo : &mapW1lo;
             const int slot = SPLIT ? 0 : mm;
@@ -749,7 +762,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       }
       return (static_cast<uint32_t>(ks) * C::MMA_K * C::SW) >> 4;
     };
-    constexpr bool kWaiter = use_waiter<NMAT, TM>();
+    constexpr bool kWaiter = use_waiter<NMAT, TM, SPLIT>();
     uint32_t stage = 0, phase = 0, it = 0;
     // kWaiter: the step list is walked here (next item's first 32 steps fetched one item
     // ahead; recipes from two presence ballots per 32 steps), so the per-step loop issues no
@@ -757,23 +770,27 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     // and the recipe comes from the producer through shared memory.
     int nx_s0 = 0, nx_s1 = 0;
     int4 nx_first = make_int4(0, -1, -1, 0);
+    // kBallot: the MMA warp derives each step's recipe from the step list itself (no
+    // shared-memory read queued behind the in-flight MMAs' operand reads)
+    // (single-matrix plans hold only present blocks: every step is one block of matrix 0)
+    constexpr bool kBallot = NMAT > 1 && (kWaiter || (!SPLIT && BLAST_BALLOT_GU));
     auto prefetch = [&](int item) {
       if (item >= n_items) return;
       const int jn = item % p.n_lines;
       nx_s0 = __ldg(&p.step_ptr[jn]);
       nx_s1 = __ldg(&p.step_ptr[jn + 1]);
-      if constexpr (kWaiter) {
+      if constexpr (kBallot) {
         const int idx = nx_s0 + static_cast<int>(lane);
         nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
       }
     };
     prefetch(i0);
+    const long long t_loop = dbg_on ? clock64() : 0;
     for (int item = i0; item < n_items; item += istep, ++it) {
       const uint32_t as = it & 1;
       const int s0 = nx_s0, s1 = nx_s1;
       int4 mine = nx_first;
       prefetch(item + istep);
-      uint32_t m0 = 0, m1 = 0, seen0 = 0, seen1 = 0;
       if constexpr (kWaiter)
         named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
       else
@@ -783,23 +800,20 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       bool done = s0 >= s1;  // SPLIT: an item's stages end at the producer's kMetaLast
       for (int s = s0; SPLIT ? !done : s < s1; ++s) {
         uint32_t meta = 0;
-        if constexpr (kWaiter) {
+        if constexpr (NMAT == 1) {
+          meta = kMetaHas0 | (s != s0 ? kMetaAccFirst : 0u);
+        } else if constexpr (kBallot) {
+          // the plan's per-step bits (plan.cu): presence and first block of each matrix
           const int i = (s - s0) & 31;
-          if (i == 0) {
-            if (s != s0) {  // next 32 steps of a long line
-              const int idx = s + static_cast<int>(lane);
-              mine = idx < s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
-            }
-            seen0 |= m0;
-            seen1 |= m1;
-            m0 = __ballot_sync(0xffffffffu, mine.y >= 0);
-            m1 = __ballot_sync(0xffffffffu, NMAT > 1 && mine.z >= 0);
+          if (i == 0 && s != s0) {  // next 32 steps of a long line
+            const int idx = s + static_cast<int>(lane);
+            mine = idx < s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
           }
-          const uint32_t below = (1u << i) - 1u;
-          const bool has0 = (m0 >> i) & 1u, has1 = NMAT > 1 && ((m1 >> i) & 1u);
-          const bool init0 = SUMACC ? (((m0 | m1) & below) | seen0 | seen1) != 0
-                                    : ((m0 & below) | seen0) != 0;
-          const bool init1 = ((m1 & below) | seen1) != 0;
+          const uint32_t w = static_cast<uint32_t>(__shfl_sync(0xffffffffu, mine.w, i));
+          const bool has0 = w & 1u, has1 = (w & 2u) != 0;
+          // accumulator already holds a partial sum before this step
+          const bool init0 = SUMACC ? s != s0 : !(w & 4u);
+          const bool init1 = !(w & 8u);
           meta = (has0 ? kMetaHas0 : 0u) | (has1 ? kMetaHas1 : 0u);
           if (kMerge && has0 && has1 && init0 == init1) {
             meta |= kMetaMerged | (init0 ? kMetaAccFirst : 0u);
@@ -808,7 +822,15 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             if (SUMACC) meta |= (init0 || has0) ? kMetaAccSecond : 0u;
             else meta |= init1 ? kMetaAccSecond : 0u;
           }
-          named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
+        }
+        if constexpr (NMAT == 1 || kBallot) {
+          if constexpr (kWaiter) {
+            const long long tw0 = dbg_on ? clock64() : 0;
+            named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
+            if (dbg_on) wc.acc[2] += static_cast<unsigned long long>(clock64() - tw0);
+          } else {
+            wc.wait(2, &full[stage], phase, dbg_on);
+          }
           tc_fence_after();
         } else {
           wc.wait(2, &full[stage], phase, dbg_on);
@@ -816,6 +838,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           meta = ld_shared_u32(&stage_meta[stage]);  // the producer's recipe
           if (SPLIT) done = (meta & kMetaLast) != 0;
         }
+        const long long ti0 = dbg_on ? clock64() : 0;
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
           const uint64_t bd = b_desc0 + soff;
@@ -866,12 +889,17 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             mma_commit(&empty[stage]);
         }
         __syncwarp();
+        if (dbg_on) {
+          wc.acc[6] += static_cast<unsigned long long>(clock64() - ti0);
+          wc.acc[7] += 1;
+        }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
       if (elect_one()) mma_commit(&tmem_full[as]);
       __syncwarp();
     }
-  } else if (warp == 2 && use_waiter<NMAT, TM>()) {
+    if (dbg_on) wc.acc[4] += static_cast<unsigned long long>(clock64() - t_loop);
+  } else if (warp == 2 && use_waiter<NMAT, TM, SPLIT>()) {
     // ------------------------------------------------------------ barrier waiter
     // Mirrors the MMA warp's item / step sequence: waits on the accumulator-free and
     // stage-full mbarriers and releases the MMA warp through named barriers.
@@ -926,7 +954,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
       if constexpr (IN_ST) mbar_wait(&in_full[it & 1], (it >> 1) & 1);
-      if (p.skip_epilogue) {  // diagnosis: release the accumulator unread
+      if (p.skip_epilogue & 1) {  // diagnosis: release the accumulator unread
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[as]);
@@ -954,7 +982,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     }
   }
 
-  if (warp == 0 || warp == 2 || warp == 4) wc.flush(p.dbg);
+  if (warp <= 2 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
   if (CL > 1)
     cluster_sync();  // no CTA leaves while its peer may still multicast into it

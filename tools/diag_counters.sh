@@ -1,0 +1,3 @@
+for e in 0 3; do
+  echo "== skip=$e"; BLAST_DEBUG_COUNTERS=1 BLAST_SKIP_EPILOGUE=$e timeout 120 python tools/diag_time.py 2>&1 | grep "blast dbg" | tail -2
+done

@@ -58,7 +58,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // ----------------------------------------------------------------------------- P1/P2/P4
 // MODE 0: SS, MODE 1: TS. NACC accumulators rotate per 4-MMA block. STREAM: warps 4..7 keep
 // bulk-copying 16 KB chunks from global into a separate smem ring (P4).
-template <int N, int NACC, int MODE, bool STREAM>
+template <int N, int NACC, int MODE, bool STREAM, int M = 128, int BMN = 0>
 __global__ void __launch_bounds__(256, 1) rate_kernel(int iters, const uint8_t* gsrc, size_t gbytes,
                                                       unsigned long long* out, unsigned long long* out2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256, 1) rate_kernel(int iters, const uint8_t* 
   tc_fence_after();
   const uint32_t tbase = tslot;
   const uint32_t a0 = smem_u32(smem), b0 = a0 + 16384;
-  const uint32_t idesc = make_idesc(128, N, 1u, 0u, 0u);  // A, B K-major
+  const uint32_t idesc = make_idesc(M, N, 1u, 0u, BMN ? 1u : 0u);  // A K-major, B K- or MN-major
   uint8_t* ring = smem + 16384 + 32768;
   if (warp == 1) {
     const long long t0 = clock64();
@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(256, 1) rate_kernel(int iters, const uint8_t* 
         const uint32_t d = tbase + 256 * (MODE == 1) + (NACC > 1 ? (i % NACC) * N : 0);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t bd = make_sdesc(b0 + ks * 32, 16, 1024, 2);
+          const uint64_t bd = BMN ? make_sdesc(b0 + ks * 16 * 128, N * 128, 1024, 2)
+                                  : make_sdesc(b0 + ks * 32, 16, 1024, 2);
           if (MODE == 0) {
             const uint64_t ad = make_sdesc(a0 + ks * 32, 16, 1024, 2);
             mma_f16(d, ad, bd, idesc, (i | ks) ? 1u : 0u);
@@ -141,9 +142,9 @@ __global__ void __launch_bounds__(256, 1) rate_kernel(int iters, const uint8_t* 
   if (warp == 0) { tc_fence_after(); tmem_dealloc(tbase, 512); }
 }
 
-template <int N, int NACC, int MODE, bool STREAM>
+template <int N, int NACC, int MODE, bool STREAM, int M = 128, int BMN = 0>
 void run_rate(const char* name, int iters, const uint8_t* gsrc, size_t gbytes) {
-  auto k = rate_kernel<N, NACC, MODE, STREAM>;
+  auto k = rate_kernel<N, NACC, MODE, STREAM, M, BMN>;
   const int smem = 16384 + 32768 + 65536 + 2048;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   unsigned long long *d, *d2;
@@ -160,9 +161,9 @@ void run_rate(const char* name, int iters, const uint8_t* gsrc, size_t gbytes) {
   avg /= 148;
   avg2 /= 148;
   const double per_mma = avg / (iters * 4.0);
-  const double ideal = 128.0 * N / 256.0;
-  printf("%-34s N=%3d nacc=%d: %6.1f cyc/MMA (floor %3.0f) -> %5.1f%% of peak", name, N, NACC,
-         per_mma, ideal, 100.0 * ideal / per_mma);
+  const double ideal = M * N / 256.0;
+  printf("%-34s M=%3d N=%3d nacc=%d: %6.1f cyc/MMA (floor %3.0f) -> %5.1f%% of peak", name, M, N,
+         NACC, per_mma, ideal, 100.0 * ideal / per_mma);
   if (STREAM) printf("   concurrent bulk-copy fill %.1f B/cyc/SM", avg2 / 1000.0);
   printf("\n");
   CK(cudaFree(d));
@@ -678,7 +679,71 @@ void run_sync_rate(int iters) {
   CK(cudaFree(d));
 }
 
-int main() {
+// ----------------------------------------------------------------------------- P11
+// Accumulator dependency chains: 8 SS M=128 N=64 MMAs per iteration spread over NCH
+// accumulators, either blocked (all of one accumulator's MMAs back to back, like the
+// engine's TM = 2 step: h0 k0..k3, h1 k0..k3) or interleaved round-robin. All accumulate.
+template <int NCH, bool INTERLEAVE>
+__global__ void __launch_bounds__(128, 1) chain_kernel(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  const uint32_t a0 = smem_u32(smem), b0 = a0 + 32768;
+  const uint32_t idesc = make_idesc(128, 64, 1u, 0u, 0u);
+  if (warp == 1) {
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      if (elect_one()) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int per = 8 / NCH;
+          const int acc = INTERLEAVE ? j % NCH : j / per;
+          const int ks = (INTERLEAVE ? j / NCH : j % per) & 3;
+          const uint64_t ad = make_sdesc(a0 + (acc & 1) * 16384 + ks * 32, 16, 1024, 2);
+          const uint64_t bd = make_sdesc(b0 + ks * 32, 16, 1024, 2);
+          mma_f16(tbase + acc * 64, ad, bd, idesc, 1u);
+        }
+        if ((i & 7) == 7) mma_commit(&bar);
+      }
+      __syncwarp();
+      if ((i & 7) == 7) mbar_wait(&bar, (i >> 3) & 1);
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+template <int NCH, bool INTERLEAVE>
+void run_chain(int iters) {
+  auto k = chain_kernel<NCH, INTERLEAVE>;
+  const int smem = 65536 + 2048;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  unsigned long long* d;
+  CK(cudaMalloc(&d, 148 * 8));
+  k<<<148, 128, smem>>>(iters, d);
+  CK(cudaDeviceSynchronize());
+  unsigned long long h[148];
+  CK(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  avg /= 148;
+  printf("P11 %d accumulators %-11s: %6.1f cyc/MMA (8 MMAs per commit group of 1)\n", NCH,
+         INTERLEAVE ? "interleaved" : "blocked", avg / (iters * 8.0));
+  CK(cudaFree(d));
+}
+
+int main(int argc, char** argv) {
   int clk_khz = 0;
   CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
   printf("SM clock attr %.0f MHz\n", clk_khz / 1000.0);
@@ -686,6 +751,34 @@ int main() {
   uint8_t* g;
   CK(cudaMalloc(&g, gbytes));
   CK(cudaMemset(g, 1, gbytes));
+  if (argc > 1 && argv[1][0] == 'm') {  // P9: M = 64 vs M = 128 issue rate by N
+    run_rate<64, 1, 0, false, 64>("P9 SS", 4000, g, gbytes);
+    run_rate<128, 1, 0, false, 64>("P9 SS", 4000, g, gbytes);
+    run_rate<256, 1, 0, false, 64>("P9 SS", 2000, g, gbytes);
+    run_rate<64, 1, 0, false>("P9 SS", 4000, g, gbytes);
+    run_rate<128, 1, 0, false>("P9 SS", 4000, g, gbytes);
+    run_rate<256, 1, 0, false>("P9 SS", 2000, g, gbytes);
+    run_rate<256, 2, 0, false>("P9 SS", 2000, g, gbytes);
+    return 0;
+  }
+  if (argc > 1 && argv[1][0] == 'c') {
+    run_chain<1, false>(2000);
+    run_chain<2, false>(2000);
+    run_chain<2, true>(2000);
+    run_chain<4, false>(2000);
+    run_chain<4, true>(2000);
+    run_chain<8, true>(2000);
+    return 0;
+  }
+  if (argc > 1 && argv[1][0] == 'b') {  // P10: B operand K-major vs MN-major (weights)
+    run_rate<64, 1, 0, false>("P10 SS B K-major", 4000, g, gbytes);
+    run_rate<64, 2, 0, false>("P10 SS B K-major", 4000, g, gbytes);
+    run_rate<64, 1, 0, false, 128, 1>("P10 SS B MN-major", 4000, g, gbytes);
+    run_rate<64, 2, 0, false, 128, 1>("P10 SS B MN-major", 4000, g, gbytes);
+    run_rate<128, 1, 0, false, 128, 1>("P10 SS B MN-major", 4000, g, gbytes);
+    run_rate<64, 1, 1, false, 128, 1>("P10 TS B MN-major", 4000, g, gbytes);
+    return 0;
+  }
 
   run_sync_rate<0>(4000);
   run_sync_rate<1>(4000);
