@@ -101,6 +101,7 @@ __global__ void plan_fill_kernel(const int32_t* kmap0, const int32_t* kmap1, int
   if (line >= lines) return;
   int out = step_ptr[line];
   int f = 0, seen = 0;  // seen: warp-uniform, matrices with a block in earlier chunks
+  int n0 = 0, n1 = 0;   // blocks of matrix 0 / 1 in the line (warp-uniform)
   for (int64_t base = 0; base < inner; base += 32) {
     const int64_t i = base + lane;
     int k0 = -1, k1 = -1;
@@ -119,6 +120,8 @@ __global__ void plan_fill_kernel(const int32_t* kmap0, const int32_t* kmap1, int
     const bool first0 = k0 >= 0 && !(seen & 1) && !(bal0 & lt);
     const bool first1 = k1 >= 0 && !(seen & 2) && !(bal1 & lt);
     seen |= (bal0 ? 1 : 0) | (bal1 ? 2 : 0);
+    n0 += __popc(bal0);
+    n1 += __popc(bal1);
     if (present) {
       const int pos = out + __popc(bal & lt);
       steps[pos] = make_int4(static_cast<int>(i), k0, k1,
@@ -129,7 +132,8 @@ __global__ void plan_fill_kernel(const int32_t* kmap0, const int32_t* kmap1, int
     out += __popc(bal);
   }
   for (int o = 16; o > 0; o >>= 1) f |= __shfl_xor_sync(0xffffffffu, f, o);
-  if (lane == 0) flags[line] = f;
+  // bits 0/1: matrix 0/1 present; bits 2..16 / 17..31: its block count (inner < 2^15)
+  if (lane == 0) flags[line] = f | (min(n0, 0x7fff) << 2) | (min(n1, 0x7fff) << 17);
 }
 
 __global__ void split_tf32_kernel(const float* x, float* hi, float* lo, int64_t n) {

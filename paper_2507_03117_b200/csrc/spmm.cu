@@ -55,22 +55,46 @@ static unsigned long long* dbg_buffer() {
   if (on < 0) {
     const char* e = getenv("BLAST_DEBUG_COUNTERS");
     on = (e && e[0] == '1') ? 1 : 0;
-    if (on && cudaMalloc(&buf, 8 * sizeof(unsigned long long)) != cudaSuccess) on = 0;
+    // [0, 8): summed role counters; [8, 8 + 2 * 1024): per-CTA start / end globaltimer
+    if (on && cudaMalloc(&buf, (8 + 2048) * sizeof(unsigned long long)) != cudaSuccess) on = 0;
   }
   return on ? buf : nullptr;
 }
 static void dbg_begin(cudaStream_t st) {
-  if (auto* b = dbg_buffer()) cudaMemsetAsync(b, 0, 8 * sizeof(unsigned long long), st);
+  if (auto* b = dbg_buffer()) cudaMemsetAsync(b, 0, (8 + 2048) * sizeof(unsigned long long), st);
 }
 static void dbg_end(const char* name, cudaStream_t st, int ctas) {
   auto* b = dbg_buffer();
   if (!b) return;
-  unsigned long long h[8];
+  static unsigned long long h[8 + 2048];
   cudaMemcpyAsync(h, b, sizeof(h), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   const double n = ctas > 0 ? ctas : 1;
+  if (ctas > 0 && ctas <= 1024 && h[8] != 0) {  // per-CTA spans (globaltimer, ns)
+    unsigned long long t0 = ~0ull, t1 = 0, e0 = ~0ull;
+    double sum = 0, mx = 0;
+    for (int i = 0; i < ctas; ++i) {
+      const unsigned long long a = h[8 + 2 * i], z = h[8 + 2 * i + 1];
+      t0 = std::min(t0, a);
+      t1 = std::max(t1, z);
+      e0 = std::min(e0, z);
+      sum += double(z - a);
+      mx = std::max(mx, double(z - a));
+    }
+    unsigned long long s1 = 0;
+    for (int i = 0; i < ctas; ++i) s1 = std::max(s1, h[8 + 2 * i]);
+    fprintf(stderr,
+            "[blast dbg] %s span %.1f us: CTA starts within %.1f us, ends within %.1f us, "
+            "per-CTA avg %.1f max %.1f us\n",
+            name, (t1 - t0) * 1e-3, (s1 - t0) * 1e-3, (t1 - e0) * 1e-3, sum / ctas * 1e-3, mx * 1e-3);
+    if (getenv("BLAST_DEBUG_CTAS")) {
+      fprintf(stderr, "[blast dbg] per-CTA end (us after first start):");
+      for (int i = 0; i < ctas; ++i) fprintf(stderr, " %.1f", (h[8 + 2 * i + 1] - t0) * 1e-3);
+      fprintf(stderr, "\n");
+    }
+  }
   fprintf(stderr,
-          "[blast dbg] %s ctas=%d per-CTA cycles: prod.wait_empty=%.0f prod.wait_wempty=%.0f "
+          "[blast dbg] %s ctas=%d per-CTA cycles: prod.wait_empty=%.0f cta.total=%.0f "
           "mma.wait_full=%.0f mma.wait_acc=%.0f mma.loop=%.0f epi.wait_acc=%.0f mma.issue=%.0f "
           "mma.steps=%.0f\n",
           name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n);
@@ -268,13 +292,14 @@ constexpr bool staged_fits() {
 // gate+up with one weight block per stage and single-buffered output staging (TcCfg SPLIT):
 // 5 pipeline stages instead of 4. Measured equal on cfg3 (236.6 vs 236.5 us: the kernel is
 // bound by L2->SM bytes, not by stages in flight), so opt-in: BLAST_SPLIT_STAGES=1.
-static bool split_stages() {
+// BLAST_SPLIT_STAGES=2: sequential gate+up (TcCfg SPLIT = 2).
+static int split_stages() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BLAST_SPLIT_STAGES");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
   }
-  return v == 1;
+  return v;
 }
 // Clusters of two CTAs sharing weight blocks through TMA multicast (spmm_tc_kernel CL = 2) for
 // the 256-token forward products. Measured slower on cfg3 (gate+up 243 vs 232 us, down 123 vs
@@ -325,7 +350,9 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
         if constexpr (staged_fits<B, ELT, NPASS, 2, false, 2>())
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
-            return split_stages()
+            return split_stages() == 2
+                       ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 2>(c, a0lo, a1lo, st)
+                   : split_stages() == 1
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 1>(c, a0lo, a1lo, st)
                    : (c.m >= 512 && cluster_weights())
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 0, 2>(c, a0lo, a1lo, st)

@@ -36,7 +36,8 @@ struct SpmmParams {
   int32_t n_tok_tiles;  // ceil(m / 128)
   const int32_t* step_ptr;  // [n_lines + 1]
   const int4* steps;        // {a_blk, k0, k1, 0}
-  const int32_t* line_flags;  // bit i: accumulator i received at least one MMA
+  const int32_t* line_flags;  // bit i: accumulator i received at least one MMA; bits 2..16 /
+                              // 17..31: blocks of matrix 0 / 1 in the line
   int32_t act;
   int32_t accumulate;  // EPI_STORE: out0 += result (second half of a split dX sum)
   void* out0;  // Y | G | dA
@@ -131,6 +132,10 @@ struct StepCursor {
 // block becomes two stages (the panel is loaded twice, ~5 % of steps at 90 % sparsity), and
 // the output is staged single-buffered. The 16 + 16 KB saved buy a fifth pipeline stage,
 // which the TMA latency under load needs.
+// SPLIT = 2 (gate+up, sequential): same stage layout; an item runs all of its line's gate
+// blocks, then all of its up blocks (the plan walked twice), so the MMA issuer's recipe is
+// the stage index against the line's gate-block count (plan flags) and a waiter warp
+// handles the mbarriers, as for single-matrix products.
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0,
           int TM = 1, int IN_ST = 0, int SPLIT = 0>
 struct TcCfg {
@@ -434,7 +439,7 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
   const bool row_ok = row < p.m;
   constexpr int NCH = B / 16;
   constexpr bool kTwoAcc = EPI == EPI_GATED_FWD;
-  const bool acc0_init = SUMACC ? (flags != 0) : ((flags & 1) != 0);
+  const bool acc0_init = SUMACC ? ((flags & 3) != 0) : ((flags & 1) != 0);
   // this warp's 16-column chunks are c = half, half + 2, ...; the TMEM loads of two chunks
   // (both accumulators when gated) are issued before one wait
 #pragma unroll 1
@@ -526,8 +531,9 @@ constexpr uint32_t kBarStage = 4;  // + ring stage (<= 8 ids)
 #ifndef BLAST_BALLOT_GU
 #define BLAST_BALLOT_GU 0
 #endif
-template <int NMAT, int TM, bool SPLIT = false>
-constexpr bool use_waiter() { return !SPLIT && (NMAT == 1 || BLAST_WAITER_GU); }
+// SPLIT = 2 (sequential gate+up) always uses the waiter: its recipe is the stage index.
+template <int NMAT, int TM, int SPLIT = 0>
+constexpr bool use_waiter() { return SPLIT == 2 || (SPLIT == 0 && (NMAT == 1 || BLAST_WAITER_GU)); }
 
 // 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (two warps per TMEM lane quarter, splitting the 16-column chunks).
@@ -552,9 +558,14 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
                const SpmmParams p) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
   using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST, SPLIT>;
-  static_assert(!SPLIT || (NMAT == 2 && !SUMACC && NPASS == 1 && !use_waiter<NMAT, TM, SPLIT>()),
+  static_assert(!SPLIT || (NMAT == 2 && !SUMACC && NPASS == 1 &&
+                           (SPLIT == 2) == use_waiter<NMAT, TM, SPLIT>()),
                 "split stages: gate+up products only");
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
+#ifdef BLAST_WAIT_COUNTERS
+  const long long t_kernel0 = clock64();
+  if (p.dbg && threadIdx.x == 0) p.dbg[8 + 2 * blockIdx.x] = globaltimer_ns();
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* staging = smem + C::STAGES * C::STAGE;  // [2][OUT_TILE] when OUT_ELT > 0
@@ -647,6 +658,53 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
     };
     prefetch(i0);
+    if constexpr (SPLIT == 2) {
+      // sequential gate+up: pass 0 loads the line's gate blocks, pass 1 its up blocks; one
+      // panel + one weight block (slot 0) per stage
+      for (int item = i0; item < n_items; item += istep) {
+        const int t = tile_of(item);
+        const int s0 = nx_s0, s1 = nx_s1;
+        const int4 first = nx_first;
+        prefetch(item + istep);
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          StepCursor cur;
+          cur.steps = p.steps;
+          cur.end = s1;
+          cur.base = s0;
+          cur.mine = first;
+          for (int s = s0; s < s1; ++s) {
+            const int4 st = cur.get(s);
+            const int kb = pass == 0 ? st.y : st.z;
+            if (kb < 0) continue;
+            if ((n++ & 1u) != mine) {
+              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+              continue;
+            }
+            wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
+            if (elect_one()) {
+              uint8_t* sbase = smem + stage * C::STAGE;
+              if (p.skip_epilogue & 2) {  // diagnosis: MMAs run on stale shared memory
+                mbar_arrive(&full[stage]);
+              } else {
+                mbar_expect_tx(&full[stage], C::TROWS * C::ROWB + B * C::ROWB);
+#pragma unroll
+                for (int at = 0; at < C::NATOM; ++at)
+                  tma_load_2d(sbase + at * C::TROWS * C::SW, &mapA0, &full[stage],
+                              st.x * B + at * C::SWE, t * C::TROWS);
+                const CUtensorMap* mw = pass == 0 ? &mapW0 : &mapW1;
+#pragma unroll
+                for (int at = 0; at < C::NATOM; ++at)
+                  tma_load_2d_hint(sbase + C::A_TILE + at * B * C::SW, mw, &full[stage],
+                                   at * C::SWE, kb * B, pol_w);
+              }
+            }
+            __syncwarp();
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    } else
     for (int item = i0; item < n_items; item += istep) {
       const int t = tile_of(item);
       const int s0 = nx_s0, s1 = nx_s1;
@@ -784,8 +842,49 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
       }
     };
-    prefetch(i0);
     const long long t_loop = dbg_on ? clock64() : 0;
+    if constexpr (SPLIT == 2) {
+      // sequential gate+up: stage i of an item is gate block i (i < n0) or up block i - n0
+      int nx_fl = i0 < n_items ? __ldg(&p.line_flags[i0 % p.n_lines]) : 0;
+      for (int item = i0; item < n_items; item += istep, ++it) {
+        const uint32_t as = it & 1;
+        const int fl = nx_fl;
+        if (item + istep < n_items) nx_fl = __ldg(&p.line_flags[(item + istep) % p.n_lines]);
+        const int n0 = (fl >> 2) & 0x7fff, n = n0 + ((fl >> 17) & 0x7fff);
+        named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
+        tc_fence_after();
+        const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
+        for (int i = 0; i < n; ++i) {
+          const uint32_t sel = i >= n0 ? 1u : 0u;
+          const uint32_t init = (i != 0 && i != n0) ? 1u : 0u;
+          named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
+          tc_fence_after();
+          const long long ti0 = dbg_on ? clock64() : 0;
+          if (elect_one()) {
+            const uint32_t soff = (stage * C::STAGE) >> 4;
+            const uint64_t bb = b_desc0 + soff;
+#pragma unroll
+            for (int h = 0; h < TM; ++h) {
+              const uint64_t ad = a_desc0 + soff + ((h * C::BM * C::SW) >> 4);
+              const uint32_t d = d_base + h * C::HALF_ACC + sel * B;
+#pragma unroll
+              for (int ks = 0; ks < C::KSL; ++ks)
+                mma_f16(d, ad + a_koff(ks), bb + b_koff(ks), C::IDESC, (init | ks) ? 1u : 0u);
+            }
+            mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (dbg_on) {
+            wc.acc[6] += static_cast<unsigned long long>(clock64() - ti0);
+            wc.acc[7] += 1;
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) mma_commit(&tmem_full[as]);
+        __syncwarp();
+      }
+    } else {
+    prefetch(i0);
     for (int item = i0; item < n_items; item += istep, ++it) {
       const uint32_t as = it & 1;
       const int s0 = nx_s0, s1 = nx_s1;
@@ -898,6 +997,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       if (elect_one()) mma_commit(&tmem_full[as]);
       __syncwarp();
     }
+    }
     if (dbg_on) wc.acc[4] += static_cast<unsigned long long>(clock64() - t_loop);
   } else if (warp == 2 && use_waiter<NMAT, TM, SPLIT>()) {
     // ------------------------------------------------------------ barrier waiter
@@ -907,7 +1007,13 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     for (int item = i0; item < n_items; item += istep, ++it) {
       const uint32_t as = it & 1, use = it >> 1;
       const int j = item % p.n_lines;
-      const int n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
+      int n_steps;
+      if constexpr (SPLIT == 2) {
+        const int fl = __ldg(&p.line_flags[j]);
+        n_steps = ((fl >> 2) & 0x7fff) + ((fl >> 17) & 0x7fff);
+      } else {
+        n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
+      }
       wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
       named_bar_arrive(kBarAcc + as, 64);
       for (int s = 0; s < n_steps; ++s) {
@@ -982,6 +1088,12 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     }
   }
 
+#ifdef BLAST_WAIT_COUNTERS
+  if (warp == 4 && dbg_on) {
+    wc.acc[1] += static_cast<unsigned long long>(clock64() - t_kernel0);
+    if (lane == 0) p.dbg[8 + 2 * blockIdx.x + 1] = globaltimer_ns();
+  }
+#endif
   if (warp <= 2 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
   if (CL > 1)

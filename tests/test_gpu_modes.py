@@ -36,6 +36,7 @@ np.save({out!r}, torch.stack([y.float(), y2.float()]).cpu().numpy())
 MODES = {
     "default": {},
     "split": {"BLAST_SPLIT_STAGES": "1"},
+    "sequential": {"BLAST_SPLIT_STAGES": "2"},
     "cluster": {"BLAST_CLUSTER_W": "1"},
     "pair": {"BLAST_PAIR_ENGINE": "1"},
     "fused": {"BLAST_FUSED_MLP": "1"},
