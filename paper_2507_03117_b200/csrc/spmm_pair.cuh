@@ -53,7 +53,13 @@ struct PairCfg {
   static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
   static constexpr int OUT_TILE = OUT_ELT ? (BM * OUT_ROWB + 1023) / 1024 * 1024 : 0;
-  static constexpr int STAGING = 2 * OUT_TILE;
+#ifndef BLAST_PAIR_OUTBUFS
+#define BLAST_PAIR_OUTBUFS (TM == 2 ? 1 : 2)
+#endif
+  // single-buffered output staging at TM = 2 buys a fifth panel stage (measured: 0.386 ->
+  // 0.362 ms per cfg3 step with streamed weights)
+  static constexpr int OUT_BUFS = BLAST_PAIR_OUTBUFS;
+  static constexpr int STAGING = OUT_BUFS * OUT_TILE;
   // dynamic shared memory: [1 KiB barriers + meta][staging][n_stages x STAGE][res_cap x WH]
   static constexpr int SMEM_BYTES = 232448;
   static constexpr int DATA_BYTES = SMEM_BYTES - 2048 - STAGING;  // stages + resident weights
@@ -326,7 +332,7 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
         int base_blocks = 0;  // stored blocks of this line before the current 32-step chunk
         for (int s = s0; s < s1; ++s) {
           const int i = (s - s0) & 31;
-          if (i == 0) {
+          if (NMAT > 1 && i == 0) {  // single-matrix plans: every step is block s - s0
             if (s != s0) {
               base_blocks += __popc(m0) + __popc(m1);
               const int idx = s + static_cast<int>(lane);
@@ -338,12 +344,13 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
             m1 = __ballot_sync(0xffffffffu, NMAT > 1 && mine.z >= 0);
           }
           const uint32_t below = (1u << i) - 1u;
-          const bool has0 = (m0 >> i) & 1u, has1 = NMAT > 1 && ((m1 >> i) & 1u);
-          const bool init0 = SUMACC ? (((m0 | m1) & below) | seen0 | seen1) != 0
-                                    : ((m0 & below) | seen0) != 0;
+          const bool has0 = NMAT == 1 || ((m0 >> i) & 1u), has1 = NMAT > 1 && ((m1 >> i) & 1u);
+          const bool init0 = NMAT == 1 ? s != s0
+                             : SUMACC ? (((m0 | m1) & below) | seen0 | seen1) != 0
+                                      : ((m0 & below) | seen0) != 0;
           const bool init1 = ((m1 & below) | seen1) != 0;
           // block order in the line: step order, matrix 0 before matrix 1 (the producer's)
-          const int b0 = base_blocks + __popc(m0 & below) + __popc(m1 & below);
+          const int b0 = NMAT == 1 ? s - s0 : base_blocks + __popc(m0 & below) + __popc(m1 & below);
           const int bidx[2] = {b0, b0 + (has0 ? 1 : 0)};
           named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
           tc_fence_after();
@@ -421,11 +428,11 @@ spmm_pair_kernel(const __grid_constant__ CUtensorMap mapO,
 #pragma unroll
         for (int h = 0; h < TM; ++h) {
           const int row0 = t * C::PT + h * 256 + static_cast<int>(rank) * C::BM;
-          uint8_t* stg = staging + ((tile_it * TM + h) & 1) * C::OUT_TILE;
+          uint8_t* stg = staging + ((tile_it * TM + h) % C::OUT_BUFS) * C::OUT_TILE;
           const uint32_t tacc =
               tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
-          epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW>(p, tacc, row0, j * B, flags, stg,
-                                                            half, q, lane, etid, vec_ok);
+          epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS>(
+              p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok);
           if (h == TM - 1) {
             tc_fence_before();
             __syncwarp();
