@@ -1,6 +1,9 @@
 // Host dispatch of the block-sparse engine and the C-ABI product entry points:
 // blast_bspmm (kernels.py:86/127), blast_bspmm_rt (kernels.py:143),
 // blast_mlp_forward (mlp.py:102), blast_mlp_backward_dgrad (mlp.py:118-142).
+#include <mutex>
+#include <unordered_map>
+
 #include "host.hpp"
 #include "spmm_simt.cuh"
 #include "spmm_pair.cuh"
@@ -98,6 +101,37 @@ static void dbg_end(const char* name, cudaStream_t st, int ctas) {
           "mma.wait_full=%.0f mma.wait_acc=%.0f mma.loop=%.0f epi.wait_acc=%.0f mma.issue=%.0f "
           "mma.steps=%.0f\n",
           name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n);
+}
+
+// Dynamic item queue of the tensor-core engine (SpmmParams::item_ctr): one {claimed, exited}
+// counter pair per stream, zeroed once; every launch leaves it zeroed (its last CTA resets
+// it), so stream-ordered launches and graph replays on that stream reuse it. A stream first
+// seen during graph capture gets the static schedule. BLAST_DYN_ITEMS=1 enables.
+static int32_t* item_queue_ctr(cudaStream_t st) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BLAST_DYN_ITEMS");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!on) return nullptr;
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, int32_t*> ctrs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ctrs.find(st);
+  if (it != ctrs.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  int32_t* d = nullptr;
+  if (cudaMalloc(&d, 2 * sizeof(int32_t)) != cudaSuccess ||
+      cudaMemset(d, 0, 2 * sizeof(int32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  ctrs[st] = d;
+  return d;
 }
 
 static SpmmParams make_params(const EngineCall& c) {
@@ -205,6 +239,7 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   SpmmParams p = make_params(c);
   p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
   const int64_t items = cdiv(p.n_tok_tiles, CL) * p.n_lines;  // per cluster
+  if (CL == 1 && items > num_sms()) p.item_ctr = item_queue_ctr(st);
   if (items <= 0) return BLAST_OK;
   int64_t clusters = std::min<int64_t>(items, num_sms() / CL);
   dbg_begin(st);
@@ -287,7 +322,7 @@ constexpr bool staged_fits() {
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
   constexpr int staging = (2 + 2 * IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
-  return (232448 - 1024 - 512 - staging) / stage >= 3;
+  return (232448 - 1024 - 640 - staging) / stage >= 3;
 }
 // gate+up with one weight block per stage and single-buffered output staging (TcCfg SPLIT):
 // 5 pipeline stages instead of 4. Measured equal on cfg3 (236.6 vs 236.5 us: the kernel is
