@@ -106,7 +106,8 @@ static void dbg_end(const char* name, cudaStream_t st, int ctas) {
 // Dynamic item queue of the tensor-core engine (SpmmParams::item_ctr): one {claimed, exited}
 // counter pair per stream, zeroed once; every launch leaves it zeroed (its last CTA resets
 // it), so stream-ordered launches and graph replays on that stream reuse it. A stream first
-// seen during graph capture gets the static schedule. BLAST_DYN_ITEMS=1 enables.
+// seen during graph capture gets the static schedule. Built with -DBLAST_DYN_QUEUE=1,
+// BLAST_DYN_ITEMS=1 enables it at run time.
 static int32_t* item_queue_ctr(cudaStream_t st) {
   static int on = -1;
   if (on < 0) {
@@ -239,7 +240,7 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   SpmmParams p = make_params(c);
   p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
   const int64_t items = cdiv(p.n_tok_tiles, CL) * p.n_lines;  // per cluster
-  if (CL == 1 && items > num_sms()) p.item_ctr = item_queue_ctr(st);
+  if (ItemQueue::kDyn && CL == 1 && items > num_sms()) p.item_ctr = item_queue_ctr(st);
   if (items <= 0) return BLAST_OK;
   int64_t clusters = std::min<int64_t>(items, num_sms() / CL);
   dbg_begin(st);

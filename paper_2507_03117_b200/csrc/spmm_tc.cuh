@@ -62,7 +62,11 @@ struct SpmmParams {
 // mbarrier pair per slot) that every other role reads once per item. Warp 0 claims two items
 // ahead of the one it starts (the claim's latency is never waited on) and publishes the next
 // item when it starts the current one, so consumers can prefetch the next item's metadata.
+#ifndef BLAST_DYN_QUEUE
+#define BLAST_DYN_QUEUE 0  // compiled in only on request: the static loops measured faster
+#endif
 struct ItemQueue {
+  static constexpr bool kDyn = BLAST_DYN_QUEUE != 0;
   int* ring;
   uint64_t* full;
   uint64_t* empty;
@@ -71,7 +75,7 @@ struct ItemQueue {
   __device__ __forceinline__ int first(int i0) const { return i0 < n ? i0 : -1; }
   // consumers: the item after `item`, the seq-th of this CTA (one call per item, whole warp)
   __device__ __forceinline__ int next(int item, uint32_t seq) const {
-    if (ctr == nullptr) {
+    if (!kDyn || ctr == nullptr) {
       const int x = item + istep;
       return x < n ? x : -1;
     }
@@ -85,7 +89,7 @@ struct ItemQueue {
   // producer warp 0: publish the item after `item`; `claim` (lane 0) holds the pending
   // counter value for it and receives the claim for the one after
   __device__ __forceinline__ int publish_next(int item, uint32_t seq, int& claim) const {
-    if (ctr == nullptr) {
+    if (!kDyn || ctr == nullptr) {
       const int x = item + istep;
       return x < n ? x : -1;
     }
@@ -644,7 +648,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   iq.ring = q_ring;
   iq.full = q_full;
   iq.empty = q_empty;
-  iq.ctr = CL == 1 ? p.item_ctr : nullptr;
+  iq.ctr = (ItemQueue::kDyn && CL == 1) ? p.item_ctr : nullptr;
   iq.n = n_items;
   iq.istep = istep;
   // warps that read the ring: producer 3, MMA 1, the waiter (2) when used, the epilogue
@@ -725,7 +729,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     };
     prefetch(i0);
     int claim = -1;  // warp 0, lane 0: pending queue claim
-    if (warp == 0 && iq.ctr != nullptr && lane == 0) claim = atomicAdd(iq.ctr, 1);
+    if (ItemQueue::kDyn && warp == 0 && iq.ctr != nullptr && lane == 0) claim = atomicAdd(iq.ctr, 1);
     auto next_item = [&](int item, uint32_t seq) -> int {
       return warp == 0 ? iq.publish_next(item, seq, claim) : iq.next(item, seq);
     };
@@ -1182,7 +1186,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
-  if (iq.ctr != nullptr && threadIdx.x == 0) {
+  if (ItemQueue::kDyn && iq.ctr != nullptr && threadIdx.x == 0) {
     // every claim of this CTA precedes its exit; the last CTA out re-arms the queue
     __threadfence();
     if (atomicAdd(iq.ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {

@@ -1,6 +1,6 @@
 """Opt-in engine modes (read once per process from the environment) give bitwise the same
 MLP forward as the default engine: split stages, cluster weight multicast, the CTA-pair engine,
-the fused gate+up->down kernel, and the narrow-tile / direct-store fallbacks. Each mode runs in
+the fused gate+up->down kernel, the sequential gate+up order, and the narrow-tile / direct-store fallbacks. Each mode runs in
 a subprocess."""
 import os
 import subprocess
