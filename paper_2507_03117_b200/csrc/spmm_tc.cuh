@@ -62,6 +62,11 @@ struct SpmmParams {
 // mbarrier pair per slot) that every other role reads once per item. Warp 0 claims two items
 // ahead of the one it starts (the claim's latency is never waited on) and publishes the next
 // item when it starts the current one, so consumers can prefetch the next item's metadata.
+// BLAST_SKIP_EPILOGUE's "skip operand loads" switch (diagnosis) is compiled in only on request
+#ifndef BLAST_DIAG_SWITCHES
+#define BLAST_DIAG_SWITCHES 0  // 0.3472 vs 0.3485 ms per cfg3 step with it in (same box)
+#endif
+constexpr bool kDiagSwitches = BLAST_DIAG_SWITCHES != 0;
 #ifndef BLAST_DYN_QUEUE
 #define BLAST_DYN_QUEUE 0  // compiled in only on request: the static loops measured faster
 #endif
@@ -761,7 +766,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
             if (elect_one()) {
               uint8_t* sbase = smem + stage * C::STAGE;
-              if (p.skip_epilogue & 2) {  // diagnosis: MMAs run on stale shared memory
+              if (kDiagSwitches && (p.skip_epilogue & 2)) {  // diagnosis: stale operands
                 mbar_arrive(&full[stage]);
               } else {
                 mbar_expect_tx(&full[stage], C::TROWS * C::ROWB + B * C::ROWB);
@@ -818,7 +823,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           for (int mm = 0; mm < NMAT; ++mm)
             if (kb[mm] >= 0) bytes += C::NCOPY * (B * C::ROWB);
           if (!use_waiter<NMAT, TM, SPLIT>()) stage_meta[stage] = meta;
-          if (p.skip_epilogue & 2) {  // diagnosis: MMAs run on stale shared memory
+          if (kDiagSwitches && (p.skip_epilogue & 2)) {  // diagnosis: stale operands
             mbar_arrive(&full[stage]);
             bytes = 0;
           } else {
@@ -827,7 +832,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           uint8_t* sbase = smem + stage * C::STAGE;
 #pragma unroll
           for (int a = 0; a < C::NA; ++a) {
-            if (bytes == 0) break;
+            if (kDiagSwitches && bytes == 0) break;
             if (SUMACC && kb[a] < 0) continue;
             const CUtensorMap* mh = (a == 0) ? &mapA0 : &mapA1;
             const CUtensorMap* ml = (a == 0) ? &mapA0lo : &mapA1lo;
@@ -842,7 +847,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           }
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm) {
-            if (kb[mm] < 0 || bytes == 0) continue;
+            if (kb[mm] < 0 || (kDiagSwitches && bytes == 0)) continue;
             const CUtensorMap* mh = (mm == 0) ? &mapW0 : &mapW1;
             const CUtensorMap* ml = (mm == 0) ? &mapW0lo : &mapW1lo;
             const int slot = SPLIT ? 0 : mm;
