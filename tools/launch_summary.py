@@ -18,7 +18,9 @@ def main(path, frac=0.25, top=16):
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = 0.0
     for d in last:
-        v = float(d["Metric Value"]) * (1e-3 if d["Metric Unit"] == "nsecond" else 1.0)
+        unit = d["Metric Unit"]
+        v = float(d["Metric Value"].replace(",", "")) * (1e-3 if unit in ("ns", "nsecond") else
+                                                         1e3 if unit in ("ms", "msecond") else 1.0)
         k = d["Kernel Name"][:90]
         agg[k][0] += 1
         agg[k][1] += v
