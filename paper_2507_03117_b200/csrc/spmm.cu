@@ -1,9 +1,6 @@
 // Host dispatch of the block-sparse engine and the C-ABI product entry points:
 // blast_bspmm (kernels.py:86/127), blast_bspmm_rt (kernels.py:143),
 // blast_mlp_forward (mlp.py:102), blast_mlp_backward_dgrad (mlp.py:118-142).
-#include <mutex>
-#include <unordered_map>
-
 #include "host.hpp"
 #include "spmm_simt.cuh"
 #include "spmm_pair.cuh"
@@ -101,38 +98,6 @@ static void dbg_end(const char* name, cudaStream_t st, int ctas) {
           "mma.wait_full=%.0f mma.wait_acc=%.0f mma.loop=%.0f epi.wait_acc=%.0f mma.issue=%.0f "
           "mma.steps=%.0f\n",
           name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n);
-}
-
-// Dynamic item queue of the tensor-core engine (SpmmParams::item_ctr): one {claimed, exited}
-// counter pair per stream, zeroed once; every launch leaves it zeroed (its last CTA resets
-// it), so stream-ordered launches and graph replays on that stream reuse it. A stream first
-// seen during graph capture gets the static schedule. Built with -DBLAST_DYN_QUEUE=1,
-// BLAST_DYN_ITEMS=1 enables it at run time.
-static int32_t* item_queue_ctr(cudaStream_t st) {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("BLAST_DYN_ITEMS");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (!on) return nullptr;
-  static std::mutex mu;
-  static std::unordered_map<cudaStream_t, int32_t*> ctrs;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = ctrs.find(st);
-  if (it != ctrs.end()) return it->second;
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  int32_t* d = nullptr;
-  if (cudaMalloc(&d, 2 * sizeof(int32_t)) != cudaSuccess ||
-      cudaMemset(d, 0, 2 * sizeof(int32_t)) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  ctrs[st] = d;
-  return d;
 }
 
 static SpmmParams make_params(const EngineCall& c) {
@@ -240,7 +205,6 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   SpmmParams p = make_params(c);
   p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
   const int64_t items = cdiv(p.n_tok_tiles, CL) * p.n_lines;  // per cluster
-  if (ItemQueue::kDyn && CL == 1 && items > num_sms()) p.item_ctr = item_queue_ctr(st);
   if (items <= 0) return BLAST_OK;
   int64_t clusters = std::min<int64_t>(items, num_sms() / CL);
   dbg_begin(st);
@@ -323,17 +287,20 @@ constexpr bool staged_fits() {
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
   constexpr int staging = (2 + 2 * IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
-  return (232448 - 1024 - 640 - staging) / stage >= 3;
+  return (232448 - 1024 - 512 - staging) / stage >= 3;
 }
-// gate+up with one weight block per stage and single-buffered output staging (TcCfg SPLIT):
-// 5 pipeline stages instead of 4. Measured equal on cfg3 (236.6 vs 236.5 us: the kernel is
-// bound by L2->SM bytes, not by stages in flight), so opt-in: BLAST_SPLIT_STAGES=1.
-// BLAST_SPLIT_STAGES=2: sequential gate+up (TcCfg SPLIT = 2).
+// gate+up stage layout (TcCfg SPLIT) for the 256-token staged product:
+//   2 (default): sequential items (all gate blocks of the line, then all up blocks), one weight
+//      block per stage, waiter warp; same box cfg3 0.3388 vs 0.3433 ms for the interleaved
+//      layout (gate+up 227 vs 235 us; profiles/r01/mma_side/mode_ab.txt)
+//   0: interleaved steps (a step holding both blocks loads the panel once), 48 KB stages
+//   1: interleaved steps, one weight block per stage (0.349 ms)
+// BLAST_SPLIT_STAGES=0/1/2 selects.
 static int split_stages() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BLAST_SPLIT_STAGES");
-    v = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+    v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
   }
   return v;
 }
@@ -386,7 +353,8 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
         if constexpr (staged_fits<B, ELT, NPASS, 2, false, 2>())
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
-            return split_stages() == 2
+            // (plan flags hold per-line block counts below 2^15)
+            return (split_stages() == 2 && c.a_cols / B < 0x7fff)
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 2>(c, a0lo, a1lo, st)
                    : split_stages() == 1
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 1>(c, a0lo, a1lo, st)

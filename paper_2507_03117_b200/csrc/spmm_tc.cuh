@@ -52,66 +52,13 @@ struct SpmmParams {
                             // 2 mark stages full without loading operands
   int32_t reverse_tiles;    // process token tiles last-to-first (reads the most recently
                             // written rows of the activations first, while they are in L2)
-  int32_t* item_ctr;        // dynamic item queue {claimed, exited} (zero on entry, reset by
-                            // the last CTA to exit); nullptr: static round-robin items
 };
 
-// Per-CTA item sequence. Static: items i0, i0 + istep, ... Dynamic (item_ctr set, one CTA
-// per cluster of 1): the first item is blockIdx.x, later ones are claimed from a global
-// counter by producer warp 0 and published through an 8-slot shared-memory ring (one
-// mbarrier pair per slot) that every other role reads once per item. Warp 0 claims two items
-// ahead of the one it starts (the claim's latency is never waited on) and publishes the next
-// item when it starts the current one, so consumers can prefetch the next item's metadata.
 // BLAST_SKIP_EPILOGUE's "skip operand loads" switch (diagnosis) is compiled in only on request
 #ifndef BLAST_DIAG_SWITCHES
 #define BLAST_DIAG_SWITCHES 0  // 0.3472 vs 0.3485 ms per cfg3 step with it in (same box)
 #endif
 constexpr bool kDiagSwitches = BLAST_DIAG_SWITCHES != 0;
-#ifndef BLAST_DYN_QUEUE
-#define BLAST_DYN_QUEUE 0  // compiled in only on request: the static loops measured faster
-#endif
-struct ItemQueue {
-  static constexpr bool kDyn = BLAST_DYN_QUEUE != 0;
-  int* ring;
-  uint64_t* full;
-  uint64_t* empty;
-  int32_t* ctr;
-  int n, istep;
-  __device__ __forceinline__ int first(int i0) const { return i0 < n ? i0 : -1; }
-  // consumers: the item after `item`, the seq-th of this CTA (one call per item, whole warp)
-  __device__ __forceinline__ int next(int item, uint32_t seq) const {
-    if (!kDyn || ctr == nullptr) {
-      const int x = item + istep;
-      return x < n ? x : -1;
-    }
-    const uint32_t slot = seq & 7u;  // publication seq carries the (seq + 1)-th item
-    mbar_wait(&full[slot], (seq >> 3) & 1u);
-    const int v = *reinterpret_cast<volatile const int*>(&ring[slot]);
-    __syncwarp();
-    if (lane_id() == 0) mbar_arrive(&empty[slot]);
-    return v;
-  }
-  // producer warp 0: publish the item after `item`; `claim` (lane 0) holds the pending
-  // counter value for it and receives the claim for the one after
-  __device__ __forceinline__ int publish_next(int item, uint32_t seq, int& claim) const {
-    if (!kDyn || ctr == nullptr) {
-      const int x = item + istep;
-      return x < n ? x : -1;
-    }
-    const int c = __shfl_sync(0xffffffffu, claim, 0);
-    int v = istep + c;
-    if (c < 0 || v >= n) v = -1;
-    const uint32_t slot = seq & 7u;
-    mbar_wait(&empty[slot], ((seq >> 3) & 1u) ^ 1u);
-    if (lane_id() == 0) {
-      *reinterpret_cast<volatile int*>(&ring[slot]) = v;
-      mbar_arrive(&full[slot]);
-      claim = v >= 0 ? atomicAdd(ctr, 1) : -1;
-    }
-    __syncwarp();
-    return v;
-  }
-};
 
 // token tile of a work item (items are t-major: item = t * n_lines + j)
 __device__ __forceinline__ int item_tile(const SpmmParams& p, int item) {
@@ -221,7 +168,7 @@ struct TcCfg {
   static constexpr int IN_STAGING = IN_ST ? 2 * TM * OUT_TILE : 0;  // double-buffered by item
   static constexpr int STAGING = OUT_BUFS * OUT_TILE + IN_STAGING;
   // 227 KB opt-in maximum minus barriers, alignment slack and the output staging
-  static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 640 - STAGING : 200 * 1024;
+  static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 512 - STAGING : 200 * 1024;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int NACC = SUMACC ? 1 : NMAT;
@@ -236,7 +183,7 @@ struct TcCfg {
   static constexpr uint32_t IDESC =
       make_idesc(BM, B, ELT == 2 ? 1u : 2u, 0u, B_KMAJOR ? 0u : 1u);
   // barriers + tmem slot live after the stages
-  static constexpr int BAR_BYTES = 640;  // stage + accumulator barriers, item queue ring
+  static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE + STAGING + BAR_BYTES + 1024;  // +1024 alignment slack
   static_assert(STAGES >= 2, "stage does not fit twice in shared memory");
   static_assert(B % 16 == 0 && B >= 16 && B <= 256, "tensor-core block size");
@@ -637,9 +584,6 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   // producer before its expect_tx arrive (release), read after the full wait (acquire)
   uint32_t* stage_meta = tmem_slot + 4;
   uint64_t* in_full = reinterpret_cast<uint64_t*>(stage_meta + 8);  // [2] staged in0 landed
-  uint64_t* q_full = reinterpret_cast<uint64_t*>(tmem_slot + 16);    // [8] item ring
-  uint64_t* q_empty = q_full + 8;                                      // [8]
-  int* q_ring = reinterpret_cast<int*>(q_empty + 8);                   // [8]
   uint8_t* in_staging = staging + C::OUT_BUFS * C::OUT_TILE;        // [2][TM][OUT_TILE] (IN_ST)
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
@@ -649,15 +593,6 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   const uint32_t crank = CL > 1 ? cluster_ctarank() : 0u;
   const int n_items = ((p.n_tok_tiles + CL - 1) / CL) * p.n_lines;
   const int i0 = static_cast<int>(blockIdx.x) / CL, istep = static_cast<int>(gridDim.x) / CL;
-  ItemQueue iq;
-  iq.ring = q_ring;
-  iq.full = q_full;
-  iq.empty = q_empty;
-  iq.ctr = (ItemQueue::kDyn && CL == 1) ? p.item_ctr : nullptr;
-  iq.n = n_items;
-  iq.istep = istep;
-  // warps that read the ring: producer 3, MMA 1, the waiter (2) when used, the epilogue
-  constexpr int kQueueReaders = 2 + (use_waiter<NMAT, TM, SPLIT>() ? 1 : 0) + kEpiWarps;
   auto tile_of = [&](int item) -> int {
     if (CL == 1) return item_tile(p, item);
     const int np = (p.n_tok_tiles + CL - 1) / CL;
@@ -682,10 +617,6 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     }
     mbar_init(&in_full[0], 1);
     mbar_init(&in_full[1], 1);
-    for (int s = 0; s < 8; ++s) {
-      mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], kQueueReaders);
-    }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -725,7 +656,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     int nx_s0 = 0, nx_s1 = 0;
     int4 nx_first = make_int4(0, -1, -1, 0);
     auto prefetch = [&](int item) {
-      if (item < 0 || item >= n_items) return;
+      if (item >= n_items) return;
       const int jn = item % p.n_lines;
       nx_s0 = __ldg(&p.step_ptr[jn]);
       nx_s1 = __ldg(&p.step_ptr[jn + 1]);
@@ -733,21 +664,14 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
     };
     prefetch(i0);
-    int claim = -1;  // warp 0, lane 0: pending queue claim
-    if (ItemQueue::kDyn && warp == 0 && iq.ctr != nullptr && lane == 0) claim = atomicAdd(iq.ctr, 1);
-    auto next_item = [&](int item, uint32_t seq) -> int {
-      return warp == 0 ? iq.publish_next(item, seq, claim) : iq.next(item, seq);
-    };
-    uint32_t qseq = 0;
     if constexpr (SPLIT == 2) {
       // sequential gate+up: pass 0 loads the line's gate blocks, pass 1 its up blocks; one
       // panel + one weight block (slot 0) per stage
-      for (int item = iq.first(i0), nxt; item >= 0; item = nxt, ++qseq) {
-        nxt = next_item(item, qseq);
+      for (int item = i0; item < n_items; item += istep) {
         const int t = tile_of(item);
         const int s0 = nx_s0, s1 = nx_s1;
         const int4 first = nx_first;
-        prefetch(nxt);
+        prefetch(item + istep);
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
           StepCursor cur;
@@ -787,8 +711,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         }
       }
     } else
-    for (int item = iq.first(i0), nxt; item >= 0; item = nxt, ++qseq) {
-      nxt = next_item(item, qseq);
+    for (int item = i0; item < n_items; item += istep) {
       const int t = tile_of(item);
       const int s0 = nx_s0, s1 = nx_s1;
       StepCursor cur;
@@ -796,7 +719,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       cur.end = s1;
       cur.base = s0;
       cur.mine = nx_first;
-      prefetch(nxt);
+      prefetch(item + istep);
       uint32_t init0 = 0, init1 = 0;  // accumulator i already holds a partial sum
       for (int s = s0; s < s1; ++s) {
         const int4 st = cur.get(s);
@@ -916,7 +839,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     // (single-matrix plans hold only present blocks: every step is one block of matrix 0)
     constexpr bool kBallot = NMAT > 1 && (kWaiter || (!SPLIT && BLAST_BALLOT_GU));
     auto prefetch = [&](int item) {
-      if (item < 0 || item >= n_items) return;
+      if (item >= n_items) return;
       const int jn = item % p.n_lines;
       nx_s0 = __ldg(&p.step_ptr[jn]);
       nx_s1 = __ldg(&p.step_ptr[jn + 1]);
@@ -929,11 +852,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     if constexpr (SPLIT == 2) {
       // sequential gate+up: stage i of an item is gate block i (i < n0) or up block i - n0
       int nx_fl = i0 < n_items ? __ldg(&p.line_flags[i0 % p.n_lines]) : 0;
-      for (int item = iq.first(i0), nxt; item >= 0; item = nxt, ++it) {
-        nxt = iq.next(item, it);
+      for (int item = i0; item < n_items; item += istep, ++it) {
         const uint32_t as = it & 1;
         const int fl = nx_fl;
-        if (nxt >= 0) nx_fl = __ldg(&p.line_flags[nxt % p.n_lines]);
+        if (item + istep < n_items) nx_fl = __ldg(&p.line_flags[(item + istep) % p.n_lines]);
         const int n0 = (fl >> 2) & 0x7fff, n = n0 + ((fl >> 17) & 0x7fff);
         named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
         tc_fence_after();
@@ -969,12 +891,11 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       }
     } else {
     prefetch(i0);
-    for (int item = iq.first(i0), nxt; item >= 0; item = nxt, ++it) {
-      nxt = iq.next(item, it);
+    for (int item = i0; item < n_items; item += istep, ++it) {
       const uint32_t as = it & 1;
       const int s0 = nx_s0, s1 = nx_s1;
       int4 mine = nx_first;
-      prefetch(nxt);
+      prefetch(item + istep);
       if constexpr (kWaiter)
         named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
       else
@@ -1089,8 +1010,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     // Mirrors the MMA warp's item / step sequence: waits on the accumulator-free and
     // stage-full mbarriers and releases the MMA warp through named barriers.
     uint32_t stage = 0, phase = 0, it = 0;
-    for (int item = iq.first(i0), nxt; item >= 0; item = nxt, ++it) {
-      nxt = iq.next(item, it);
+    for (int item = i0; item < n_items; item += istep, ++it) {
       const uint32_t as = it & 1, use = it >> 1;
       const int j = item % p.n_lines;
       int n_steps;
@@ -1118,8 +1038,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     const uint64_t pol_out = policy_evict_first();
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
-    for (int item = iq.first(i0), nxt; item >= 0; item = nxt, ++it) {
-      nxt = iq.next(item, it);
+    for (int item = i0; item < n_items; item += istep, ++it) {
       const int t = tile_of(item);
       const int j = item % p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
@@ -1141,7 +1060,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         };
         if (etid == 0) {
           if (it == 0) load_in(item, 0);
-          if (nxt >= 0) load_in(nxt, (it + 1) & 1);
+          if (item + istep < n_items) load_in(item + istep, (it + 1) & 1);
         }
       }
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
@@ -1190,15 +1109,6 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
-  }
-  if (ItemQueue::kDyn && iq.ctr != nullptr && threadIdx.x == 0) {
-    // every claim of this CTA precedes its exit; the last CTA out re-arms the queue
-    __threadfence();
-    if (atomicAdd(iq.ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-      iq.ctr[0] = 0;
-      iq.ctr[1] = 0;
-      __threadfence();
-    }
   }
 }
 

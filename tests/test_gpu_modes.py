@@ -1,6 +1,6 @@
 """Opt-in engine modes (read once per process from the environment) give bitwise the same
 MLP forward as the default engine: split stages, cluster weight multicast, the CTA-pair engine,
-the fused gate+up->down kernel, the sequential gate+up order, and the narrow-tile / direct-store fallbacks. Each mode runs in
+the fused gate+up->down kernel, the interleaved gate+up layout (default: sequential), and the narrow-tile / direct-store fallbacks. Each mode runs in
 a subprocess."""
 import os
 import subprocess
@@ -36,7 +36,7 @@ np.save({out!r}, torch.stack([y.float(), y2.float()]).cpu().numpy())
 MODES = {
     "default": {},
     "split": {"BLAST_SPLIT_STAGES": "1"},
-    "sequential": {"BLAST_SPLIT_STAGES": "2"},
+    "interleaved": {"BLAST_SPLIT_STAGES": "0"},
     "cluster": {"BLAST_CLUSTER_W": "1"},
     "pair": {"BLAST_PAIR_ENGINE": "1"},
     "fused": {"BLAST_FUSED_MLP": "1"},
