@@ -160,7 +160,13 @@ struct TcCfg {
   static constexpr int B_TILE = round1k(B * ROWB);
   static constexpr int WSLOTS = SPLIT ? 1 : NMAT;           // weight blocks per stage
   static constexpr int STAGE = NA * NCOPY * A_TILE + WSLOTS * NCOPY * B_TILE;
-  static constexpr int OUT_BUFS = SPLIT ? 1 : 2;
+#ifndef BLAST_ONE_OUTBUF_1MAT
+#define BLAST_ONE_OUTBUF_1MAT 1  // down: 0.3467 vs 0.3487 ms per cfg3 step (same box)
+#endif
+  // single-buffered output staging buys a fifth 40 KB stage (gate+up SPLIT layouts; with
+  // BLAST_ONE_OUTBUF_1MAT also the 256-token single-matrix products)
+  static constexpr int OUT_BUFS =
+      (SPLIT || (BLAST_ONE_OUTBUF_1MAT && NMAT == 1 && TM == 2 && IN_ST == 0)) ? 1 : 2;
   static constexpr int OUT_ROWB = B * OUT_ELT;                          // bytes of an output tile row
   static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
