@@ -296,6 +296,19 @@ constexpr bool staged_fits() {
 //   0: interleaved steps (a step holding both blocks loads the panel once), 48 KB stages
 //   1: interleaved steps, one weight block per stage (0.349 ms)
 // BLAST_SPLIT_STAGES=0/1/2 selects.
+// The sequential layout loads the panel once per block, so steps holding both a gate and an
+// up block cost a second panel load: it pays at b >= 64 when such steps are rare (cfg3 sweep,
+// profiles/r01/cfg3_sweep.jsonl: b = 64 at 70-95 % faster, at 50 % and b = 16 / 32 slower).
+// Plan flags hold per-line block counts below 2^15.
+template <int B>
+static bool seq_gate_up_pays(const EngineCall& c) {
+  if (B < 64 || c.a_cols / B >= 0x7fff) return false;
+  const double cells = static_cast<double>(c.a_cols / B) * static_cast<double>(c.n_lines);
+  const double d0 = c.nnzb0 / cells, d1 = c.nnzb1 / cells;
+  const double both = d0 * d1, any = d0 + d1 - both;
+  return any > 0.0 && both / any < 0.25;
+}
+
 static int split_stages() {
   static int v = -1;
   if (v < 0) {
@@ -353,8 +366,7 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
         if constexpr (staged_fits<B, ELT, NPASS, 2, false, 2>())
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
-            // (plan flags hold per-line block counts below 2^15)
-            return (split_stages() == 2 && c.a_cols / B < 0x7fff)
+            return (split_stages() == 2 && seq_gate_up_pays<B>(c))
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 2>(c, a0lo, a1lo, st)
                    : split_stages() == 1
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 1>(c, a0lo, a1lo, st)
