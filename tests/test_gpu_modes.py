@@ -63,3 +63,38 @@ def test_modes_bitwise_equal(m, tmp_path):
             continue
         got = run_mode(env, m, tmp_path, name)
         assert np.array_equal(got, ref), name
+
+
+SCRIPT_B = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import oracle
+import paper_2507_03117_b200 as bs
+rng = np.random.default_rng(7)
+mats = []
+for rows, cols in ((1024, 2048), (1024, 2048), (2048, 1024)):
+    w = oracle.random_bcsc(rows, cols, {b}, {sp}, rng)
+    w = w._replace(values=(w.values / np.sqrt(rows)).astype(np.float32))
+    mats.append(bs.from_host(w, torch.bfloat16))
+net = bs.SparseMlp.from_caches(*mats)
+x = torch.from_numpy(rng.standard_normal((777, 1024)).astype(np.float32)).cuda().bfloat16()
+y, _ = bs.mlp_forward(x, net, save_activations=False)
+torch.cuda.synchronize()
+np.save({out!r}, y.float().cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("b,sp", [(128, 0.9), (64, 0.5), (64, 0.7), (32, 0.9)])
+def test_gate_up_layouts_bitwise_equal(b, sp, tmp_path):
+    """The default picks the sequential or interleaved gate+up layout by block size and
+    density (csrc/spmm.cu seq_gate_up_pays); both give the same bits."""
+    outs = []
+    for name, env in (("default", {}), ("interleaved", {"BLAST_SPLIT_STAGES": "0"}),
+                      ("sequential", {"BLAST_SPLIT_STAGES": "2"})):
+        out = str(tmp_path / f"{name}.npy")
+        res = subprocess.run([sys.executable, "-c", SCRIPT_B.format(root=str(ROOT), b=b, sp=sp, out=out)],
+                             env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
