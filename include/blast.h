@@ -90,7 +90,10 @@ int blast_kmap_from_bcsc(const int64_t* col_ptr, const int32_t* row_idx, int64_t
 /* Step lists of one or two block maps of the same grid. by_rows = 0: one line per block
  * column (ascending block row, kernels.py:117); by_rows = 1: one line per block row
  * (ascending block column, kernels.py:159). Buffers: step_ptr[lines+1], steps[4*gr*gc],
- * flags[lines]. kmap1 may be NULL. */
+ * flags[lines]. kmap1 may be NULL. A step is {inner index, block of map 0 or -1, block of
+ * map 1 or -1, bits}: bit 0/1 = block of map 0/1 present, bit 2/3 = its first block in the
+ * line. flags: bit 0/1 = map 0/1 has a block in the line, bits 2..16 / 17..31 = its block
+ * count (saturating at 2^15 - 1). */
 int blast_build_plan(const int32_t* kmap0, const int32_t* kmap1, int64_t grid_rows,
                      int64_t grid_cols, int by_rows, int32_t* step_ptr, int32_t* steps,
                      int32_t* flags, void* stream);
