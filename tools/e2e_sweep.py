@@ -61,7 +61,7 @@ def main():
         ms = timed(fn)
         print(json.dumps({"what": name, "ms": ms, "GBps_per_direction": nbytes / ms / 1e6}))
     import time
-    for chunk in (0, 512, 1024, 2048, 4096, 8192):
+    for chunk in (0, 256, 512, 768, 1024, 1536, 2048, 4096):
         fn = lambda: bs.mlp_forward(xh, net, save_activations=False, out=yh,  # noqa: E731
                                     chunk_tokens=chunk)
         ms = timed(fn)
