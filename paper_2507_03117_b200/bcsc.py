@@ -110,22 +110,36 @@ class BlockSparseMatrix:
         return self._cache["wgrad"]
 
     def _tf32(self):
-        if "tf32" not in self._cache:
-            v = self.values
-            if v.dtype != torch.float32:
-                raise ValueError("3xTF32 operands only exist for float32 matrices")
+        """hi/lo tf32 images of the float32 blocks (3xTF32 operands). They are derived
+        data: re-split in place whenever ``values`` was modified since the last split
+        (tracked by the tensor's version counter, which in-place optimizer steps and
+        ``load_state_dict`` bump), so the tensor-core path never reads stale weights."""
+        v = self.values
+        if v.dtype != torch.float32:
+            raise ValueError("3xTF32 operands only exist for float32 matrices")
+        parts = self._cache.get("tf32")
+        if parts is None:
             parts = [torch.empty_like(v) for _ in range(4)]
+            self._cache["tf32"] = parts
+            self._cache["tf32_version"] = None
+        ver = (v.data_ptr(), v._version)
+        if self._cache["tf32_version"] != ver:
             if self.nnzb:
                 L.check(L.load().blast_tf32_prepare(v.data_ptr(), self.nnzb, self.block,
                                                     *[p.data_ptr() for p in parts], L.stream()),
                         "tf32_prepare")
-            self._cache["tf32"] = parts
-        return self._cache["tf32"]
+            self._cache["tf32_version"] = ver
+        return parts
 
     def desc(self) -> L.BcscDesc:
-        """C descriptor (include/blast.h blast_bcsc_t) with plans built on first use."""
-        if "desc" in self._cache:
-            return self._cache["desc"]
+        """C descriptor (include/blast.h blast_bcsc_t) with plans built on first use.
+        The descriptor is rebuilt if ``values`` was rebound to other storage, and the
+        3xTF32 images are refreshed when the values changed in place."""
+        d = self._cache.get("desc")
+        if d is not None and self._cache.get("desc_values") == self.values.data_ptr():
+            if self.values.dtype == torch.float32:
+                self._tf32()
+            return d
         fwd = self._plan(0)
         rt = self._plan(1)
         tf = self._tf32() if self.values.dtype == torch.float32 else [None] * 4
@@ -139,6 +153,7 @@ class BlockSparseMatrix:
             rt[0].data_ptr(), rt[1].data_ptr(), rt[2].data_ptr(),
         )
         self._cache["desc"] = d
+        self._cache["desc_values"] = self.values.data_ptr()
         return d
 
     # ------------------------------------------------------------ host views

@@ -34,7 +34,10 @@ def magnitude_mask(w: torch.Tensor, b: int, sparsity: float) -> BlockMask:
 
 def _bcsc_param(w: BlockSparseMatrix) -> nn.Parameter:
     p = nn.Parameter(w.values, requires_grad=True)
-    w.values = p.data  # the kernels read the parameter storage in place
+    # The kernels read the parameter storage in place. detach() (unlike .data) shares the
+    # parameter's version counter, so in-place optimizer steps / load_state_dict are visible
+    # to derived caches (the float32 3xTF32 images, BlockSparseMatrix._tf32).
+    w.values = p.detach()
     return p
 
 

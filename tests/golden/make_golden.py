@@ -200,11 +200,70 @@ def gen_format() -> None:
     np.savez_compressed(OUT / "format.npz", **d)
 
 
+TRAIN_CASES = {
+    # name: TrainConfig fields (schedule as a dict); fp32, toy sizes, 3+ refreshes each
+    "reg": dict(layers=2, embed_dim=32, hidden_dim=32, block_size=8, lr=0.1, batch_size=32,
+                seed=0, schedule=dict(initial_sparsity=0.0, max_sparsity=0.8, total_iters=24,
+                                      decay_iters=0, step_size=8)),
+    "reg_dense": dict(layers=3, embed_dim=32, hidden_dim=64, block_size=8, lr=0.05,
+                      batch_size=16, seed=3, dense_layers=1, lr_final_frac=0.5,
+                      teacher_in_dims=20, teacher_out_dims=12, distractor_scale=0.3,
+                      schedule=dict(initial_sparsity=0.2, max_sparsity=0.7, total_iters=20,
+                                    decay_iters=4, step_size=5)),
+    "cls": dict(layers=2, embed_dim=32, hidden_dim=32, block_size=8, lr=0.2, batch_size=32,
+                seed=1, task="classification", alpha=0.5, beta=0.5, teacher_hidden=16,
+                schedule=dict(initial_sparsity=0.0, max_sparsity=0.75, total_iters=18,
+                              decay_iters=0, step_size=6)),
+}
+
+
+def gen_trainer() -> None:
+    """Run the real train() (trainer.py:318-408) and record per-iteration losses, FLOPs
+    and refresh flags, every generate_masks call's kept/regrown grids and report counts,
+    and the final dense masters."""
+    from blocksparse import trainer
+    d = {}
+    orig = trainer.generate_masks
+    for name, raw in TRAIN_CASES.items():
+        calls = []
+
+        def rec(w, g, b, s, iteration=0, _calls=calls):
+            mask, rep = orig(w, g, b, s, iteration=iteration)
+            _calls.append((mask, rep, s))
+            return mask, rep
+
+        trainer.generate_masks = rec
+        try:
+            log, stack = trainer.train(trainer.TrainConfig.from_dict(raw))
+        finally:
+            trainer.generate_masks = orig
+        d[f"{name}_config"] = np.frombuffer(json.dumps(raw).encode(), dtype=np.uint8)
+        task = trainer.make_task(trainer.TrainConfig.from_dict(raw))  # data stream, 2 batches
+        for k in range(2):
+            for j, arr in enumerate(task.next_batch(raw["batch_size"])):
+                d[f"{name}_batch{k}_{j}"] = arr
+        d[f"{name}_loss"] = np.array([r.loss for r in log.records], dtype=np.float64)
+        d[f"{name}_flops"] = np.array([r.flops_cum for r in log.records], dtype=np.int64)
+        d[f"{name}_refresh"] = np.array([r.refresh for r in log.records], dtype=bool)
+        d[f"{name}_sparsity"] = np.array([r.layer_sparsity for r in log.records])
+        d[f"{name}_n_calls"] = np.array(len(calls))
+        for k, (mask, rep, s) in enumerate(calls):
+            d[f"{name}_call{k}_kept"] = mask.kept
+            d[f"{name}_call{k}_regrown"] = mask.regrown
+            d[f"{name}_call{k}_counts"] = np.array([rep.kept, rep.regrown, rep.iteration])
+            d[f"{name}_call{k}_s"] = np.array(s)
+        for li, blk in enumerate(stack.blocks):
+            for tag, mat in zip(("gate", "up", "down"), blk.matrices()):
+                d[f"{name}_final_l{li}_{tag}"] = mat.dense
+    np.savez_compressed(OUT / "trainer.npz", **d)
+
+
 def main() -> None:
     gen_products()
     gen_mlp()
     gen_prune()
     gen_format()
+    gen_trainer()
     meta = {"reference": str(REF_SRC), "numpy": np.__version__,
             "files": sorted(p.name for p in OUT.glob("*.npz"))}
     (OUT / "MANIFEST.json").write_text(json.dumps(meta, indent=1) + "\n")

@@ -103,3 +103,32 @@ def test_column_sums(dtype, m, n):
     scale = x.double().abs().sum(0).clamp_min(1e-30)
     assert ((got.double() - ref).abs() / scale).max().item() <= 1e-5
     assert torch.equal(got, column_sums(x))  # run-to-run bitwise
+
+
+@pytest.mark.parametrize("block", [64, 128])
+def test_float32_forward_sees_optimizer_step(block):
+    """float32 weights: the 3xTF32 tensor-core images are refreshed after an in-place
+    optimizer step / load_state_dict, so the next forward uses the updated values
+    (cached hi/lo copies went stale)."""
+    from transformers.models.llama.modeling_llama import LlamaMLP
+    torch.manual_seed(3)
+    mlp = LlamaMLP(llama_cfg()).cuda().float()
+    sp = integration.SparseGatedMLP.from_llama(mlp, block, 0.5, dtype=torch.float32)
+    x = torch.randn(130, 256, device="cuda")
+
+    def ref_out():
+        wg, wu, wd = (masked_dense(w) for w in (sp.net.gate.cache, sp.net.up.cache,
+                                                sp.net.down.cache))
+        return (torch.nn.functional.silu(x @ wg) * (x @ wu)) @ wd
+
+    with torch.no_grad():
+        assert mnr(sp(x), ref_out()) <= 1e-4
+    opt = torch.optim.SGD(sp.parameters(), lr=0.5)
+    y = sp(x.requires_grad_(True))
+    y.square().sum().backward()
+    opt.step()
+    with torch.no_grad():
+        assert mnr(sp(x), ref_out()) <= 1e-4
+        state = {k: v.clone() * 0.5 for k, v in sp.state_dict().items()}
+        sp.load_state_dict(state)
+        assert mnr(sp(x), ref_out()) <= 1e-4

@@ -1,5 +1,9 @@
-"""GPU training loop with prune-and-grow (ports of tests/test_trainer.py:100-210),
-plus a step-for-step comparison with the oracle's arithmetic on a toy stack."""
+"""GPU training loop with prune-and-grow: ports of the reference's tests/test_trainer.py:100-210,
+and a step-for-step comparison with the REAL reference ``train()`` (trainer.py:318-408) on three
+toy fp32 configurations recorded in tests/golden/trainer.npz (per-iteration losses, FLOPs and
+refresh flags; every generate_masks call's kept/regrown grids and counts; final masters)."""
+import json
+
 import numpy as np
 import pytest
 import torch
@@ -100,3 +104,41 @@ def test_save_model_bytes(tmp_path):
     w = bs.load(tmp_path / names[0])
     h = stack.blocks[0].gate.cache.to_host()
     np.testing.assert_array_equal(w.to_host().values, h.values)
+
+
+@pytest.mark.parametrize("name", ["reg", "reg_dense", "cls"])
+def test_train_matches_reference_train(name, monkeypatch):
+    from conftest import golden
+    d = golden("trainer")
+    raw = json.loads(bytes(d[f"{name}_config"]).decode())
+    calls = []
+    orig = trainer.generate_masks
+
+    def rec(w, g, b, s, iteration=0):
+        mask, rep = orig(w, g, b, s, iteration=iteration)
+        calls.append((mask, rep, s))
+        return mask, rep
+
+    monkeypatch.setattr(trainer, "generate_masks", rec)
+    log, stack = trainer.train(trainer.TrainConfig.from_dict(raw))
+    assert [r.refresh for r in log.records] == d[f"{name}_refresh"].tolist()
+    assert [r.flops_cum for r in log.records] == d[f"{name}_flops"].tolist()
+    loss = np.array([r.loss for r in log.records])
+    np.testing.assert_allclose(loss, d[f"{name}_loss"], rtol=1e-4, atol=0)
+    np.testing.assert_allclose(np.array([r.layer_sparsity for r in log.records]),
+                               d[f"{name}_sparsity"], rtol=0, atol=1e-12)
+    assert len(calls) == int(d[f"{name}_n_calls"])
+    for k, (mask, rep, s) in enumerate(calls):
+        kept = mask.kept.cpu().numpy() if hasattr(mask.kept, "cpu") else np.asarray(mask.kept)
+        reg = mask.regrown.cpu().numpy() if hasattr(mask.regrown, "cpu") else np.asarray(mask.regrown)
+        np.testing.assert_array_equal(kept, d[f"{name}_call{k}_kept"], err_msg=f"call {k} kept")
+        np.testing.assert_array_equal(reg, d[f"{name}_call{k}_regrown"], err_msg=f"call {k} regrown")
+        assert [rep.kept, rep.regrown, rep.iteration] == d[f"{name}_call{k}_counts"].tolist()
+        assert s == float(d[f"{name}_call{k}_s"])
+    for li, blk in enumerate(stack.blocks):
+        for tag, mat in zip(("gate", "up", "down"), blk.matrices()):
+            ref = d[f"{name}_final_l{li}_{tag}"]
+            got = mat.dense.cpu().numpy()
+            assert np.array_equal(got == 0, ref == 0), f"layer {li} {tag}: zero pattern"
+            err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
+            assert err <= 1e-4, f"layer {li} {tag}: master max-norm-relative {err:.2e}"
