@@ -77,13 +77,17 @@ typedef struct blast_mlp_plan {
 const char* blast_last_error(void);
 int blast_version(void);
 int blast_num_sms(void);
-/* Engine selection for bf16 products with >= 256 rows and b in {32, 64}: 1 = CTA-pair
- * engine (cta_group::2) with resident weights, 0 = single-CTA engine (default; also
- * BLAST_PAIR_ENGINE=1 in the environment). Returns the previous setting. Both give the
- * same accumulation order (bitwise equal results); used for ablations and tests. */
-int blast_set_pair_engine(int enabled);
 
 /* ---------------------------------------------------------------- format / plans */
+/* Cost-balanced work lists of the persistent engine (csrc/schedule.cu): item (t, j) of a
+ * product with n_tiles token tiles and n_lines output lines, assigned by batched
+ * longest-processing-time over the plan's per-line stage counts (step_ptr, or the gate+up
+ * counts in flags when seq_gu != 0). out[k * grid + c] = k-th item of CTA c, -1 past its end;
+ * out has ceil(n_tiles * n_lines / grid) * grid entries. The engine builds and caches these
+ * itself; this entry exposes them for tests. */
+int blast_balanced_schedule(const int32_t* step_ptr, const int32_t* flags, int32_t n_lines,
+                            int32_t n_tiles, int32_t grid, int32_t seq_gu, int32_t* out,
+                            void* stream);
 /* kmap from col_ptr/row_idx (inverse index of bcsc.py:205-210). */
 int blast_kmap_from_bcsc(const int64_t* col_ptr, const int32_t* row_idx, int64_t grid_rows,
                          int64_t grid_cols, int32_t* kmap, void* stream);
@@ -131,16 +135,6 @@ int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
                       const blast_bcsc_t* up, const blast_bcsc_t* down,
                       const blast_mlp_plan_t* plan, void* y, void* gate_pre, void* up_out,
                       void* gated, void* stream);
-/* Fused inference forward y = (silu(x Wg) * (x Wu)) Wd in one persistent kernel, the
- * intermediate G kept in a 4-tile (4 x 256 tokens) ring that stays in L2 instead of an
- * [m, h] tensor in HBM (mlp.py:102-115 without the saved activations). bf16, b = 64,
- * m >= 256, d and h multiples of 64; otherwise returns BLAST_EUNSUPPORTED without launching.
- * Results equal the two-launch path bit for bit. blast_mlp_forward takes this path only when
- * BLAST_FUSED_MLP=1: on cfg3 it is slower (0.435 vs 0.352 ms per 8192 tokens) and the ring
- * is written back to HBM anyway. */
-int blast_mlp_forward_fused(const void* x, int64_t m, const blast_bcsc_t* gate,
-                            const blast_bcsc_t* up, const blast_bcsc_t* down,
-                            const blast_mlp_plan_t* plan, void* y, void* stream);
 /* out[c] = sum_r x[r, c] (fp32) of a row-major [m, n] bf16 / f32 matrix: bias gradients of
  * layers with bias (GPT2MLP integration). Deterministic (fixed row splits, fixed order). */
 int blast_column_sums(const void* x, int dtype, int64_t m, int64_t n, float* out, void* stream);

@@ -47,9 +47,9 @@ _PROTOS = {
     "blast_last_error": (C.c_char_p, []),
     "blast_version": (C.c_int, []),
     "blast_num_sms": (C.c_int, []),
-    "blast_set_pair_engine": (C.c_int, [C.c_int]),
     "blast_kmap_from_bcsc": (C.c_int, [vp, vp, i64, i64, vp, vp]),
     "blast_build_plan": (C.c_int, [vp, vp, i64, i64, C.c_int, vp, vp, vp, vp]),
+    "blast_balanced_schedule": (C.c_int, [vp, vp, i32, i32, i32, i32, vp, vp]),
     "blast_split_tf32": (C.c_int, [vp, vp, vp, i64, vp]),
     "blast_tf32_prepare": (C.c_int, [vp, i64, i32, vp, vp, vp, vp, vp]),
     "blast_bspmm": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.c_int, vp, vp]),
@@ -61,8 +61,6 @@ _PROTOS = {
                                     C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp, vp, vp,
                                     vp]),
     "blast_column_sums": (C.c_int, [vp, C.c_int, i64, i64, vp, vp]),
-    "blast_mlp_forward_fused": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
-                                          C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp]),
     "blast_mlp_forward_host": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                          C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, i64,
                                          vp]),

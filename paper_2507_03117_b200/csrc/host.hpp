@@ -25,6 +25,19 @@ void retain_pool_memory();  // keep freed cudaMallocAsync blocks cached in the d
 
 inline int check_launch(const char* what) { return cuda_status(cudaGetLastError(), what); }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per kernel and per device: `configured`
+// is the calling kernel's own per-device flag array (a function-local static of the caller)
+template <typename K>
+inline int configure_smem(K kern, int bytes, bool (&configured)[64], const char* what) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_status(cudaGetLastError(), what);
+  if (dev >= 0 && dev < 64 && configured[dev]) return 0;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  if (dev >= 0 && dev < 64) configured[dev] = true;
+  return 0;
+}
+
 // 2-D tiled tensor map over a row-major [outer, inner] array (inner contiguous).
 // box = {box_inner, box_outer}; swizzle in bytes (0, 32, 64, 128).
 bool encode_map_2d(CUtensorMap* map, const void* base, int dtype, uint64_t inner, uint64_t outer,

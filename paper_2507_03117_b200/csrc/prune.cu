@@ -545,14 +545,9 @@ __global__ void sumsq_final_kernel(const double* partial, int n, double* out) {
 
 static int topk_smem_launch(const double* n0, uint8_t* k0, const double* n1, uint8_t* k1,
                             int64_t gr, int64_t gc, int64_t k, cudaStream_t st) {
-  static bool configured = false;
+  static bool configured[64] = {};
   const int smem = kTopkSmemMax * 8;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(topk_smem_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_status(e, "topk smem attribute");
-    configured = true;
-  }
+  if (int rc = configure_smem(topk_smem_kernel, smem, configured, "topk smem attribute")) return rc;
   const int n = static_cast<int>(gr * gc);
   topk_smem_kernel<<<n1 ? 2 : 1, 1024, n * 8, st>>>(n0, k0, n1, k1, gr, gc, k);
   return check_launch("topk_smem");

@@ -3,12 +3,7 @@
 // blast_mlp_forward (mlp.py:102), blast_mlp_backward_dgrad (mlp.py:118-142).
 #include "host.hpp"
 #include "spmm_simt.cuh"
-#include "spmm_pair.cuh"
 #include "spmm_tc.cuh"
-
-int blast_mlp_forward_fused_if_enabled(const void* x, int64_t m, const blast_bcsc_t* gate,
-                                       const blast_bcsc_t* up, const blast_bcsc_t* down,
-                                       const blast_mlp_plan_t* plan, void* y, void* stream);
 
 namespace blast {
 
@@ -141,19 +136,19 @@ static bool pdl_enabled() {
   return v == 1;
 }
 
+const int32_t* balanced_schedule(const int32_t* step_ptr, const int32_t* flags, int n_lines,
+                                 int n_tiles, int grid, bool seq_gu, cudaStream_t st,
+                                 int* rows_out);
+
 template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
-          int OUT_ELT = 0, int TM = 1, int SPLIT = 0, int CL = 1>
+          int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
   using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM, IN_ST, SPLIT>;
-  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM, SPLIT, CL>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "spmm_tc smem attribute");
-    configured = true;
-  }
+  auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM, SPLIT>;
+  static bool configured[64] = {};
+  if (int rc = configure_smem(kern, Cfg::SMEM_BYTES, configured, "spmm_tc smem attribute"))
+    return rc;
   const int dt = ELT == 2 ? BLAST_BF16 : BLAST_F32;
   CUtensorMap mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo;
   auto mkA = [&](CUtensorMap* mp, const void* ptr) {
@@ -204,51 +199,33 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   if (!ok) return BLAST_EINVAL;
   SpmmParams p = make_params(c);
   p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
-  const int64_t items = cdiv(p.n_tok_tiles, CL) * p.n_lines;  // per cluster
+  const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
   if (items <= 0) return BLAST_OK;
-  int64_t clusters = std::min<int64_t>(items, num_sms() / CL);
+  const int grid = static_cast<int>(std::min<int64_t>(items, num_sms()));
+  // Persistent CTAs of single-matrix products take cost-balanced item lists (csrc/schedule.cu).
+  // Same box, cfg3 (profiles/r02/cta_spans.txt): down 111.3 -> 108.0 us (CTA ends within 8.6
+  // instead of 18.0 us); the gate+up kernel got slower (238.7 -> 243.0 us) although its CTAs
+  // also end together: its per-CTA work rose by the same amount, i.e. it is bound by the
+  // chip-wide L2 -> SM feed, which an even split cannot raise, so it keeps round robin.
+  if (NMAT == 1)
+    p.sched = balanced_schedule(c.step_ptr, c.flags, p.n_lines, p.n_tok_tiles, grid, SPLIT == 2,
+                                st, &p.sched_rows);
   dbg_begin(st);
-  if constexpr (CL > 1) {
-    cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    // persistent clusters: no more than can be resident at once (GPCs may not split evenly)
-    static int max_clusters = 0;
-    if (max_clusters == 0) {
-      cfg.gridDim = dim3(static_cast<unsigned>(num_sms() / CL * CL));
-      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess ||
-          max_clusters <= 0)
-        max_clusters = num_sms() / CL;
-      cudaGetLastError();
-    }
-    clusters = std::min<int64_t>(clusters, max_clusters);
-    cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
-    cudaLaunchKernelEx(&cfg, kern, mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
-  } else {
-    // programmatic dependent launch: this grid's CTAs start their setup on SMs freed by the
-    // previous kernel's tail and wait in-kernel (griddep_wait) for its completion
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(clusters));
-    cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
-  }
+  // programmatic dependent launch: this grid's CTAs start their setup on SMs freed by the
+  // previous kernel's tail and wait in-kernel (griddep_wait) for its completion
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
   const int rc = check_launch("spmm_tc");
-  dbg_end("spmm_tc", st, static_cast<int>(clusters * CL));
+  dbg_end("spmm_tc", st, grid);
   return rc;
 }
 
@@ -294,8 +271,7 @@ constexpr bool staged_fits() {
 //      block per stage, waiter warp; same box cfg3 0.3388 vs 0.3433 ms for the interleaved
 //      layout (gate+up 227 vs 235 us; profiles/r01/mma_side/mode_ab.txt)
 //   0: interleaved steps (a step holding both blocks loads the panel once), 48 KB stages
-//   1: interleaved steps, one weight block per stage (0.349 ms)
-// BLAST_SPLIT_STAGES=0/1/2 selects.
+// BLAST_SPLIT_STAGES=0/2 selects.
 // The sequential layout loads the panel once per block, so steps holding both a gate and an
 // up block cost a second panel load: it pays at b >= 64 when such steps are rare (cfg3 sweep,
 // profiles/r01/cfg3_sweep.jsonl: b = 64 at 70-95 % faster, at 50 % and b = 16 / 32 slower).
@@ -313,21 +289,9 @@ static int split_stages() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BLAST_SPLIT_STAGES");
-    v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
+    v = (e && e[0] == '0') ? 0 : 2;
   }
   return v;
-}
-// Clusters of two CTAs sharing weight blocks through TMA multicast (spmm_tc_kernel CL = 2) for
-// the 256-token forward products. Measured slower on cfg3 (gate+up 243 vs 232 us, down 123 vs
-// 119 us: the lockstep coupling of the pair costs more than the 10 % fewer L2 -> SM bytes), so
-// opt-in: BLAST_CLUSTER_W=1.
-static bool cluster_weights() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("BLAST_CLUSTER_W");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
 }
 // 256-token items (TcCfg TM = 2) for the forward products; BLAST_WIDE_TILES=0 disables.
 static bool wide_tiles() {
@@ -354,9 +318,7 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>()) {
         if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2>())
           if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles())
-            return (c.m >= 512 && cluster_weights())
-                       ? launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO, 2, 0, 2>(c, a0lo, a1lo, st)
-                       : launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO, 2>(c, a0lo, a1lo, st);
+            return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 1, false>())
           if (use_staged<B, ELT, NPASS, 1, false>(c))
             return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
@@ -368,10 +330,6 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
             return (split_stages() == 2 && seq_gate_up_pays<B>(c))
                        ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 2>(c, a0lo, a1lo, st)
-                   : split_stages() == 1
-                       ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 1>(c, a0lo, a1lo, st)
-                   : (c.m >= 512 && cluster_weights())
-                       ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 0, 2>(c, a0lo, a1lo, st)
                        : launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 2, false>())
           if (use_staged<B, ELT, NPASS, 2, false>(c))
@@ -405,123 +363,6 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
     }
   }
   return -1;  // not available on the tensor-core path
-}
-
-// ---------------------------------------------------------------- CTA-pair engine
-static int pair_stages_override() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("BLAST_PAIR_STAGES");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-template <int B, int NMAT, bool SUM, bool BK, int EPI, int OUT_ELT = 0, int TM = 1>
-static int launch_pair(const EngineCall& c, cudaStream_t st) {
-  using Cfg = PairCfg<B, NMAT, SUM, BK, OUT_ELT, TM>;
-  auto kern = spmm_pair_kernel<B, NMAT, SUM, BK, EPI, __nv_bfloat16, OUT_ELT, TM>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "spmm_pair smem attribute");
-    configured = true;
-  }
-  CUtensorMap mA0, mA1, mW0, mW1;
-  auto mkA = [&](CUtensorMap* mp, const void* ptr) {
-    return encode_map_2d(mp, ptr, BLAST_BF16, c.a_cols, c.m, c.a_cols * 2, Cfg::SWE, Cfg::BM,
-                         Cfg::SW);
-  };
-  auto mkW = [&](CUtensorMap* mp, const void* ptr, int64_t nnzb) {
-    if (ptr == nullptr || nnzb <= 0) {
-      ptr = c.a0;
-      nnzb = 1;
-    }
-    if (BK)  // [B/2 rows x B cols] halves, rows r*B + rank*B/2
-      return encode_map_2d(mp, ptr, BLAST_BF16, B, nnzb * B, B * 2, Cfg::WH_SW / 2, B / 2,
-                           Cfg::WH_SW);
-    return encode_map_2d(mp, ptr, BLAST_BF16, B, nnzb * B, B * 2, B / 2, B, Cfg::WH_SW);
-  };
-  bool ok = mkA(&mA0, c.a0);
-  mA1 = mA0;
-  if (ok && SUM) ok = mkA(&mA1, c.a1);
-  if (ok) ok = mkW(&mW0, c.w0, c.nnzb0);
-  mW1 = mW0;
-  if (ok && NMAT > 1) ok = mkW(&mW1, c.w1, c.nnzb1);
-  CUtensorMap mO = mA0;
-  if (ok && OUT_ELT > 0)
-    ok = encode_map_2d(&mO, c.out0, BLAST_BF16, static_cast<uint64_t>(c.n_valid),
-                       static_cast<uint64_t>(c.m), static_cast<uint64_t>(c.ld_out) * 2,
-                       Cfg::OUT_SW / 2, Cfg::BM, Cfg::OUT_SW);
-  if (!ok) return BLAST_EINVAL;
-  PairParams pp{};
-  pp.p = make_params(c);
-  pp.n_pair_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::PT));
-  const int64_t n_pairs = num_sms() / 2;
-  int64_t r = (c.n_lines * pp.n_pair_tiles) / (12 * n_pairs);
-  if (const char* e = getenv("BLAST_PAIR_R")) r = atoi(e);
-  r = std::max<int64_t>(1, std::min<int64_t>(r, pp.n_pair_tiles));
-  pp.tiles_per_item = static_cast<int32_t>(r);
-  pp.n_chunks = static_cast<int32_t>(cdiv(pp.n_pair_tiles, r));
-  // Pipeline depth vs resident weights: room for ~1.6x the mean stored blocks per line
-  // (so nearly every line is fully resident), then as many panel stages as fit (4..8).
-  const int64_t nnzb_all = c.nnzb0 + (NMAT > 1 ? c.nnzb1 : 0);
-  const int64_t want_res = (16 * nnzb_all + 10 * c.n_lines - 1) / (10 * c.n_lines);
-  int stages = pair_stages_override();
-  if (stages <= 0)
-    stages = static_cast<int>((Cfg::DATA_BYTES - want_res * Cfg::WH) / Cfg::STAGE);
-  stages = std::max(4, std::min(stages, std::min(8, Cfg::DATA_BYTES / Cfg::STAGE)));
-  pp.n_stages = stages;
-  pp.res_cap = std::min<int64_t>(254, (Cfg::DATA_BYTES - stages * Cfg::STAGE) / Cfg::WH);
-  if (const char* e = getenv("BLAST_PAIR_RESCAP")) pp.res_cap = std::min(pp.res_cap, atoi(e));
-  const int64_t items = static_cast<int64_t>(pp.n_chunks) * c.n_lines;
-  if (items <= 0) return BLAST_OK;
-  const int grid = static_cast<int>(2 * std::min<int64_t>(items, n_pairs));
-  dbg_begin(st);
-  kern<<<grid, kTcThreads, Cfg::SMEM_BYTES, st>>>(mO, mA0, mA1, mW0, mW1, pp);
-  const int rc = check_launch("spmm_pair");
-  dbg_end("spmm_pair", st, grid);
-  return rc;
-}
-
-template <int B>
-static int dispatch_pair_b(const EngineCall& c, cudaStream_t st) {
-  if (!c.transposed) {
-    const bool staged = !staged_out_disabled() && !c.accumulate && aligned16(c.out0) &&
-                        (c.ld_out * 2) % 16 == 0;
-    const bool wide = staged && c.m >= 512 && wide_tiles();
-    if (c.nmat == 1 && c.epi == EPI_STORE && c.act == ACT_NONE && !c.accumulate)
-      return wide ? launch_pair<B, 1, false, false, EPI_STORE, 2, 2>(c, st)
-             : staged ? launch_pair<B, 1, false, false, EPI_STORE, 2>(c, st)
-                      : launch_pair<B, 1, false, false, EPI_STORE>(c, st);
-    if (c.nmat == 2 && c.epi == EPI_GATED_FWD)
-      return wide ? launch_pair<B, 2, false, false, EPI_GATED_FWD, 2, 2>(c, st)
-             : staged ? launch_pair<B, 2, false, false, EPI_GATED_FWD, 2>(c, st)
-                      : launch_pair<B, 2, false, false, EPI_GATED_FWD>(c, st);
-  } else {
-    if (c.nmat == 1 && c.epi == EPI_STORE)
-      return launch_pair<B, 1, false, true, EPI_STORE>(c, st);
-    if (c.nmat == 1 && c.epi == EPI_GATED_BWD)
-      return launch_pair<B, 1, false, true, EPI_GATED_BWD>(c, st);
-    if (c.nmat == 2 && c.sumacc && c.epi == EPI_STORE)
-      return launch_pair<B, 2, true, true, EPI_STORE>(c, st);
-  }
-  return -1;
-}
-
-// The pair engine halves weight traffic but both engines sit on the same
-// shared-memory operand bandwidth ceiling at b = 64 (tools/mma_rate.cu,
-// profiles/); measured on cfg3 the single-CTA engine is still faster, so the
-// pair engine is opt-in (BLAST_PAIR_ENGINE=1 or blast_set_pair_engine(1)).
-static int g_pair_engine = -1;  // -1: from the environment, else 0/1
-
-static bool pair_disabled() {
-  if (g_pair_engine < 0) {
-    const char* e = getenv("BLAST_PAIR_ENGINE");
-    g_pair_engine = (e && e[0] == '1') ? 1 : 0;
-  }
-  return g_pair_engine == 0;
 }
 
 // Which configurations the tensor-core engine takes (the rest run on CUDA cores).
@@ -578,11 +419,6 @@ int run_engine(const EngineCall& c_in, cudaStream_t st) {
   }
   if (tc_shape_ok(c_in)) {
     if (c_in.dtype == BLAST_BF16) {
-      // CTA pairs with resident weights once there is at least one 256-token tile
-      if (!pair_disabled() && c_in.m >= 256 && (c_in.block == 32 || c_in.block == 64)) {
-        int r = c_in.block == 64 ? dispatch_pair_b<64>(c_in, st) : dispatch_pair_b<32>(c_in, st);
-        if (r >= 0) return r;
-      }
       int r = dispatch_tc<__nv_bfloat16, 2, 1>(c_in, nullptr, nullptr, st);
       if (r >= 0) return r;
     } else {
@@ -631,12 +467,6 @@ static bool check_w(const blast_bcsc_t* w) {
 }  // namespace blast
 
 using namespace blast;
-
-extern "C" int blast_set_pair_engine(int enabled) {
-  const int prev = pair_disabled() ? 0 : 1;
-  g_pair_engine = enabled ? 1 : 0;
-  return prev;
-}
 
 extern "C" int blast_bspmm(const void* x, int64_t m, const blast_bcsc_t* w, int act, void* y,
                            void* stream) {
@@ -765,10 +595,6 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
     return BLAST_EMISMATCH;
   }
   if (m <= 0) return BLAST_OK;
-  if (!gated && !gate_pre && !up_out) {
-    const int rf = blast_mlp_forward_fused_if_enabled(x, m, gate, up, down, plan, y, stream);
-    if (rf != BLAST_EUNSUPPORTED) return rf;
-  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t elt = bytes_of(gate->dtype);
   Scratch sg;

@@ -52,6 +52,10 @@ struct SpmmParams {
                             // 2 mark stages full without loading operands
   int32_t reverse_tiles;    // process token tiles last-to-first (reads the most recently
                             // written rows of the activations first, while they are in L2)
+  const int32_t* sched;     // optional cost-balanced item lists: sched[k * gridDim.x + cta] is
+                            // the k-th item of CTA `cta`, -1 past its end (csrc/schedule.cu);
+                            // nullptr: static round robin (item = cta + k * gridDim.x)
+  int32_t sched_rows;       // rows of `sched`
 };
 
 // BLAST_SKIP_EPILOGUE's "skip operand loads" switch (diagnosis) is compiled in only on request
@@ -64,6 +68,19 @@ constexpr bool kDiagSwitches = BLAST_DIAG_SWITCHES != 0;
 __device__ __forceinline__ int item_tile(const SpmmParams& p, int item) {
   const int t = item / p.n_lines;
   return p.reverse_tiles ? p.n_tok_tiles - 1 - t : t;
+}
+
+// k-th work item of this CTA (n_items once its list is exhausted). Every role warp walks the
+// same sequence, so all of them agree on the item order without communicating.
+__device__ __forceinline__ int item_at(const SpmmParams& p, int k, int n_items) {
+  if (p.sched) {
+    const int v = k < p.sched_rows ? __ldg(&p.sched[k * static_cast<int>(gridDim.x) +
+                                                     static_cast<int>(blockIdx.x)])
+                                   : -1;
+    return v < 0 ? n_items : v;
+  }
+  const int it = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+  return it < n_items ? it : n_items;
 }
 
 // v[i] += bias[col + i] for the valid columns of a 16-column chunk
@@ -555,12 +572,8 @@ constexpr int kEpiWarps = kEpiWarpsT;
 template <int EPI, int OUT_ELT>
 constexpr int in_staged() { return (EPI == EPI_GATED_BWD && OUT_ELT > 0) ? 1 : 0; }
 
-// CL = 2: launched as clusters of two CTAs that work on the same output line for two
-// consecutive token tiles in lockstep; each weight block is read from L2 once and multicast
-// into both CTAs' stages (halving the weight share of the L2 -> SM bytes), and every MMA
-// commit releases the stage in both CTAs (empty barriers count 2 arrivals).
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
-          int OUT_ELT = 0, int TM = 1, int SPLIT = 0, int CL = 1>
+          int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
 __global__ void __launch_bounds__(kTcThreads, 1)
 spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapI,
                const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
@@ -594,18 +607,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
-  // items: CL = 1: (token tile, line); CL = 2: (pair of token tiles, line), this CTA's tile is
-  // 2 * pair + rank (a tile past the end runs on zero-filled rows, stores clipped)
-  const uint32_t crank = CL > 1 ? cluster_ctarank() : 0u;
-  const int n_items = ((p.n_tok_tiles + CL - 1) / CL) * p.n_lines;
-  const int i0 = static_cast<int>(blockIdx.x) / CL, istep = static_cast<int>(gridDim.x) / CL;
-  auto tile_of = [&](int item) -> int {
-    if (CL == 1) return item_tile(p, item);
-    const int np = (p.n_tok_tiles + CL - 1) / CL;
-    int pt = item / p.n_lines;
-    if (p.reverse_tiles) pt = np - 1 - pt;
-    return pt * CL + static_cast<int>(crank);
-  };
+  // items: (token tile, line); this CTA's sequence is item_at(p, 0), item_at(p, 1), ...
+  const int n_items = p.n_tok_tiles * p.n_lines;
+  auto tile_of = [&](int item) -> int { return item_tile(p, item); };
 
   if (warp == 0 && lane == 0) {
     if (OUT_ELT) tma_prefetch(&mapO);
@@ -615,7 +619,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     if (SUMACC) tma_prefetch(&mapA1);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
@@ -630,10 +634,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     tmem_relinquish();
   }
   tc_fence_before();
-  if (CL > 1)
-    cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
-  else
-    __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Everything above (barriers, TMEM, descriptor prefetch) may overlap the previous kernel's
@@ -669,15 +670,16 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       const int idx = nx_s0 + static_cast<int>(lane);
       nx_first = idx < nx_s1 ? __ldg(&p.steps[idx]) : make_int4(0, -1, -1, 0);
     };
-    prefetch(i0);
+    prefetch(item_at(p, 0, n_items));
     if constexpr (SPLIT == 2) {
       // sequential gate+up: pass 0 loads the line's gate blocks, pass 1 its up blocks; one
       // panel + one weight block (slot 0) per stage
-      for (int item = i0; item < n_items; item += istep) {
+      for (int k = 0, item = item_at(p, 0, n_items); item < n_items;
+           item = item_at(p, ++k, n_items)) {
         const int t = tile_of(item);
         const int s0 = nx_s0, s1 = nx_s1;
         const int4 first = nx_first;
-        prefetch(item + istep);
+        prefetch(item_at(p, k + 1, n_items));
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
           StepCursor cur;
@@ -717,7 +719,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         }
       }
     } else
-    for (int item = i0; item < n_items; item += istep) {
+    for (int k = 0, item = item_at(p, 0, n_items); item < n_items;
+         item = item_at(p, ++k, n_items)) {
       const int t = tile_of(item);
       const int s0 = nx_s0, s1 = nx_s1;
       StepCursor cur;
@@ -725,7 +728,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       cur.end = s1;
       cur.base = s0;
       cur.mine = nx_first;
-      prefetch(item + istep);
+      prefetch(item_at(p, k + 1, n_items));
       uint32_t init0 = 0, init1 = 0;  // accumulator i already holds a partial sum
       for (int s = s0; s < s1; ++s) {
         const int4 st = cur.get(s);
@@ -785,15 +788,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
               uint8_t* dst = sbase + C::NA * C::NCOPY * C::A_TILE + (slot * C::NCOPY + c) * C::B_TILE;
 #pragma unroll
               for (int at = 0; at < C::NATOM; ++at) {
-                if constexpr (CL > 1) {
-                  if (crank == 0)
-                    tma_load_2d_mc(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
-                                   at * C::SWE, kb[mm] * B, static_cast<uint16_t>((1u << CL) - 1u),
-                                   pol_w);
-                } else {
-                  tma_load_2d_hint(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
-                                   at * C::SWE, kb[mm] * B, pol_w);
-                }
+                tma_load_2d_hint(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
+                                 at * C::SWE, kb[mm] * B, pol_w);
               }
             }
           }
@@ -857,11 +853,13 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     const long long t_loop = dbg_on ? clock64() : 0;
     if constexpr (SPLIT == 2) {
       // sequential gate+up: stage i of an item is gate block i (i < n0) or up block i - n0
-      int nx_fl = i0 < n_items ? __ldg(&p.line_flags[i0 % p.n_lines]) : 0;
-      for (int item = i0; item < n_items; item += istep, ++it) {
+      int nxt = item_at(p, 0, n_items);
+      int nx_fl = nxt < n_items ? __ldg(&p.line_flags[nxt % p.n_lines]) : 0;
+      for (int k = 0, item = nxt; item < n_items; item = nxt, ++k, ++it) {
         const uint32_t as = it & 1;
         const int fl = nx_fl;
-        if (item + istep < n_items) nx_fl = __ldg(&p.line_flags[(item + istep) % p.n_lines]);
+        nxt = item_at(p, k + 1, n_items);
+        if (nxt < n_items) nx_fl = __ldg(&p.line_flags[nxt % p.n_lines]);
         const int n0 = (fl >> 2) & 0x7fff, n = n0 + ((fl >> 17) & 0x7fff);
         named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
         tc_fence_after();
@@ -896,12 +894,13 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         __syncwarp();
       }
     } else {
-    prefetch(i0);
-    for (int item = i0; item < n_items; item += istep, ++it) {
+    prefetch(item_at(p, 0, n_items));
+    for (int k = 0, item = item_at(p, 0, n_items); item < n_items;
+         item = item_at(p, ++k, n_items), ++it) {
       const uint32_t as = it & 1;
       const int s0 = nx_s0, s1 = nx_s1;
       int4 mine = nx_first;
-      prefetch(item + istep);
+      prefetch(item_at(p, k + 1, n_items));
       if constexpr (kWaiter)
         named_bar_sync(kBarAcc + as, 64);  // warp 2 saw tmem_empty[as]
       else
@@ -994,10 +993,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
               }
             }
           }
-          if constexpr (CL > 1)
-            mma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << CL) - 1u));
-          else
-            mma_commit(&empty[stage]);
+          mma_commit(&empty[stage]);
         }
         __syncwarp();
         if (dbg_on) {
@@ -1016,7 +1012,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     // Mirrors the MMA warp's item / step sequence: waits on the accumulator-free and
     // stage-full mbarriers and releases the MMA warp through named barriers.
     uint32_t stage = 0, phase = 0, it = 0;
-    for (int item = i0; item < n_items; item += istep, ++it) {
+    for (int k = 0, item = item_at(p, 0, n_items); item < n_items;
+         item = item_at(p, ++k, n_items), ++it) {
       const uint32_t as = it & 1, use = it >> 1;
       const int j = item % p.n_lines;
       int n_steps;
@@ -1044,7 +1041,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     const uint64_t pol_out = policy_evict_first();
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
-    for (int item = i0; item < n_items; item += istep, ++it) {
+    for (int k = 0, item = item_at(p, 0, n_items); item < n_items;
+         item = item_at(p, ++k, n_items), ++it) {
       const int t = tile_of(item);
       const int j = item % p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
@@ -1066,7 +1064,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         };
         if (etid == 0) {
           if (it == 0) load_in(item, 0);
-          if (item + istep < n_items) load_in(item + istep, (it + 1) & 1);
+          const int nxt = item_at(p, k + 1, n_items);
+          if (nxt < n_items) load_in(nxt, (it + 1) & 1);
         }
       }
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
@@ -1108,10 +1107,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 #endif
   if (warp <= 2 || warp == 4) wc.flush(p.dbg);
   tc_fence_before();
-  if (CL > 1)
-    cluster_sync();  // no CTA leaves while its peer may still multicast into it
-  else
-    __syncthreads();
+  __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);

@@ -334,13 +334,8 @@ template <int B>
 static int launch_wgrad_tc(const void* a, const void* d, const WgradParams& p, cudaStream_t st) {
   using C = WgCfg<B>;
   auto kern = wgrad_tc_kernel<B>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "wgrad smem attribute");
-    configured = true;
-  }
+  static bool configured[64] = {};
+  if (int rc = configure_smem(kern, C::SMEM_BYTES, configured, "wgrad smem attribute")) return rc;
   CUtensorMap ma, md;
   if (!encode_map_2d(&ma, a, BLAST_BF16, p.rows, p.m, p.rows * 2, 64, C::TK, 128)) return BLAST_EINVAL;
   if (!encode_map_2d(&md, d, BLAST_BF16, p.cols, p.m, p.cols * 2, 64, C::TK, 128)) return BLAST_EINVAL;

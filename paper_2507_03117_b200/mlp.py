@@ -10,7 +10,6 @@ weight gradients either on the full grid (the reference's dense gradients,
 """
 from __future__ import annotations
 
-import os
 
 import ctypes as C
 from dataclasses import dataclass, field
@@ -172,14 +171,6 @@ def _forward_host(x, mlp: SparseMlp, out: torch.Tensor | None, chunk_tokens: int
     return A.to_host(y)
 
 
-def fused_forward_ok(mlp: SparseMlp, m: int) -> bool:
-    """Shapes the fused inference forward covers (blast_mlp_forward_fused in include/blast.h);
-    the library takes it only when BLAST_FUSED_MLP=1, else it allocates G itself."""
-    return (os.environ.get("BLAST_FUSED_MLP") == "1" and mlp.dtype == torch.bfloat16
-            and mlp.block == 64 and m >= 256 and mlp.embed_dim % 64 == 0
-            and mlp.hidden_dim % 64 == 0)
-
-
 def mlp_forward(x, mlp: SparseMlp, save_activations: bool = True, out=None,
                 chunk_tokens: int = 0):
     """Run the gated MLP; returns (y, MlpActivations) (mlp.py:102-115).
@@ -207,8 +198,6 @@ def mlp_forward(x, mlp: SparseMlp, save_activations: bool = True, out=None,
     a = b = None
     if save_activations:
         a, b, g = (torch.empty(m, h, dtype=dt, device=A.DEVICE) for _ in range(3))
-    elif fused_forward_ok(mlp, m):
-        g = None  # one persistent kernel; G lives in an L2-resident ring (csrc/mlp_fused.cuh)
     else:
         g = mlp.workspace(m)
     if m:

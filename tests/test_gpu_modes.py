@@ -1,7 +1,7 @@
-"""Opt-in engine modes (read once per process from the environment) give bitwise the same
-MLP forward as the default engine: split stages, cluster weight multicast, the CTA-pair engine,
-the fused gate+up->down kernel, the interleaved gate+up layout (default: sequential), and the narrow-tile / direct-store fallbacks. Each mode runs in
-a subprocess."""
+"""Engine modes (read once per process from the environment) give bitwise the same MLP
+forward as the default engine: the interleaved gate+up layout (default: sequential), round-robin
+items instead of the cost-balanced schedule, and the narrow-tile / direct-store fallbacks. Each
+mode runs in a subprocess."""
 import os
 import subprocess
 import sys
@@ -35,11 +35,8 @@ np.save({out!r}, torch.stack([y.float(), y2.float()]).cpu().numpy())
 
 MODES = {
     "default": {},
-    "split": {"BLAST_SPLIT_STAGES": "1"},
     "interleaved": {"BLAST_SPLIT_STAGES": "0"},
-    "cluster": {"BLAST_CLUSTER_W": "1"},
-    "pair": {"BLAST_PAIR_ENGINE": "1"},
-    "fused": {"BLAST_FUSED_MLP": "1"},
+    "round_robin": {"BLAST_SCHEDULE": "0"},
     "narrow": {"BLAST_WIDE_TILES": "0"},
     "direct": {"BLAST_DIRECT_STORES": "1"},
 }

@@ -62,3 +62,53 @@ def test_plan_matches_numpy(gr, gc, density, two, by_rows):
     got = steps.cpu().numpy()[: 4 * n].reshape(-1, 4).astype(np.int64)
     assert np.array_equal(got, esteps)
     assert np.array_equal(flags.cpu().numpy().astype(np.int64), eflags)
+
+
+def lpt_reference(costs, n_tiles, grid):
+    """numpy restatement of csrc/schedule.cu: t-major sequence with each tile's lines in
+    descending cost (ties by index); batches of `grid` items, the k-th largest item of a batch
+    (ties by sequence position) to the k-th least loaded CTA (ties by CTA index)."""
+    L = len(costs)
+    order = sorted(range(L), key=lambda j: (-costs[j], j))
+    total = n_tiles * L
+    rows = -(-total // grid)
+    out = -np.ones((rows, grid), np.int64)
+    load = np.zeros(grid, np.int64)
+    for r in range(rows):
+        pos = list(range(r * grid, min(total, (r + 1) * grid)))
+        items = sorted(pos, key=lambda p: (-costs[order[p % L]], p - r * grid))
+        ctas = sorted(range(grid), key=lambda c: (load[c], c))
+        for k, p in enumerate(items):
+            j = order[p % L]
+            out[r, ctas[k]] = (p // L) * L + j
+            load[ctas[k]] += costs[j]
+    return out
+
+
+@pytest.mark.parametrize("gr,gc,density,n_tiles,grid,seq",
+                         [(64, 64, 0.1, 32, 148, 0), (64, 224, 0.1, 32, 148, 1),
+                          (12, 48, 0.3, 5, 148, 0), (8, 8, 0.5, 3, 7, 1)])
+def test_balanced_schedule(gr, gc, density, n_tiles, grid, seq):
+    from paper_2507_03117_b200 import _lib as L
+    rng = np.random.default_rng(gr * gc + n_tiles)
+    k0, k1 = kmap(rng, gr, gc, density), kmap(rng, gr, gc, density)
+    step_ptr, steps, flags = bcsc.build_plan(torch.from_numpy(k0).cuda(),
+                                            torch.from_numpy(k1).cuda() if seq else None,
+                                            gr, gc, 0)
+    rows = -(-n_tiles * gc // grid)
+    out = torch.full((rows * grid,), -7, dtype=torch.int32, device="cuda")
+    L.check(L.load().blast_balanced_schedule(step_ptr.data_ptr(), flags.data_ptr(), gc, n_tiles,
+                                             grid, seq, out.data_ptr(), L.stream()), "schedule")
+    got = out.cpu().numpy().reshape(rows, grid)
+    sp, fl = step_ptr.cpu().numpy(), flags.cpu().numpy()
+    stages = ((fl >> 2) & 0x7fff) + ((fl >> 17) & 0x7fff) if seq else np.diff(sp)
+    costs = [int(4 * s + 3) for s in stages[:gc]]
+    # every item exactly once: the schedule is a permutation (results are order-independent)
+    items = got[got >= 0]
+    assert np.array_equal(np.sort(items), np.arange(n_tiles * gc))
+    assert np.array_equal(got, lpt_reference(costs, n_tiles, grid))
+    # balance: no CTA above the mean by more than one item
+    load = np.zeros(grid)
+    for c in range(grid):
+        load[c] = sum(costs[i % gc] for i in got[:, c] if i >= 0)
+    assert load.max() - load.mean() <= max(costs) + 1e-9
