@@ -7,14 +7,25 @@ the reference's bench.random_bcsc), bf16, 8192 tokens per GPU. One step = one
 sparse MLP forward y = (silu(x Wg) * (x Wu)) Wd over the step's tokens through
 the package API (2 kernel launches: fused gate/up + down).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--no-extras]
 
-N > 1 runs under torchrun: every rank processes its own 8192 tokens with the
-same weights (token-sharded data parallelism: the MLP has no cross-token
-dependency, so there is no data-path collective; scaling "weak"). Timing: CUDA
-events per step on the launching stream, L2 flushed (256 MiB write) between
-steps outside the events, barrier + synchronize around the K timed steps, max
-over ranks.
+N > 1 runs one rank per GPU: under torchrun, or, when started without WORLD_SIZE, this
+script re-launches itself through torch.distributed.run with N ranks. Every rank processes
+its own 8192 tokens with the same weights (token-sharded data parallelism: the MLP has no
+cross-token dependency, so there is no data-path collective; scaling "weak"). Timing: CUDA
+events per step on the launching stream, L2 flushed (256 MiB write) between steps outside
+the events, barrier + synchronize around the K timed steps, max over ranks.
+
+The same JSON line carries the rest of the north-star path as extra keys (each timed with
+CUDA events, each with its roofline fraction; ``--no-extras`` skips them):
+  train_step    cfg3 training step: forward with saved activations + mlp_backward
+                (dX and stored-block dW); N > 1 adds the NCCL all-reduce of the stored-block
+                gradients (data-parallel pretraining)
+  prune_refresh cfg3 gate matrix (fp32 masters): generate_masks + apply_mask, GB/s
+  cfg0_fp32     configs[0]: d=2048 h=8192 b=64 90 % 2048 tokens fp32 (3xTF32) forward
+  decode        cfg3 shape at 95 %, 128 tokens, CUDA-graph replay (HBM regime)
+  cpu_baseline_1core / cpu_train_step  the reference algorithm on 1 host core, and its
+                training step (forward + backward + masks) on all cores
 
 ``--impl reference`` times the reference algorithm on the host CPU (the numpy
 restatement in oracle/, the reference being pure numpy) on bounded token
@@ -147,6 +158,191 @@ def cpu_reference_time(weights, tokens: int, reps: int, warmup: int, seed: int):
     return times, cores
 
 
+# ---------------------------------------------------------------- extra keys
+def _ev_median(fn, iters: int, flush=None, warmup: int = 3) -> float:
+    """Median milliseconds of fn() between CUDA events on the current stream (L2 flushed
+    before each timed call when `flush` is given; the flush is outside the events)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(iters)]
+    for a, b in ev:
+        if flush is not None:
+            flush.zero_()
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return float(np.median([a.elapsed_time(b) for a, b in ev]))
+
+
+def extra_train_step(bs, net, x, world, flush, tf_peak, iters):
+    """cfg3 training step: mlp_forward (saved a, b, g) + mlp_backward(grad_mode="active")
+    (mlp.py:102-143); with N > 1 ranks the stored-block gradients are averaged over NCCL
+    (data-parallel pretraining)."""
+    import torch
+    import torch.distributed as dist
+    m = x.shape[0]
+    dy = (torch.randn(m, x.shape[1], device="cuda", generator=torch.Generator(device="cuda")
+                      .manual_seed(7)) * 0.1).bfloat16()
+    n = [w.cache.nnzb for w in net.matrices()]
+    b = net.block
+
+    def step():
+        _, acts = bs.mlp_forward(x, net)
+        grads = bs.mlp_backward(dy, acts, net, grad_mode="active")
+        if world > 1:
+            for g in grads[1:]:
+                dist.all_reduce(g)
+                g.div_(world)
+        return grads
+
+    ms = _ev_median(step, iters, flush)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    flops = 3 * 2 * m * sum(n) * b * b  # forward 3 products, dgrad 3, stored-block wgrad 3
+    ach = flops / (ms * 1e-3) / 1e12
+    return {"ms_per_step": ms, "tokens_per_s": world * m / (ms * 1e-3),
+            "flops_per_step": flops, "achieved_tflops": ach, "frac": ach / tf_peak,
+            "grad_mode": "active (stored blocks)",
+            "dp_allreduce": "NCCL all-reduce of the stored-block gradients" if world > 1 else None,
+            "path": "mlp_forward(save_activations=True) + mlp_backward(grad_mode='active')"}
+
+
+def extra_prune_refresh(bs, L, flush, hbm_peak, iters):
+    """One prune-and-grow refresh of the cfg3 gate matrix (pruner.py:128-186) on float32
+    masters W and gradient G: generate_masks (norms of W and G, two top-k, difference, counts
+    to host) + apply_mask (repack to bf16 BCSC). Bytes: W and G read by the norms, W read +
+    masked W written + the stored blocks written by the repack."""
+    import torch
+    rows, cols, b, s = D, H, BLOCK, SPARSITY
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    w = torch.randn(rows, cols, device="cuda", generator=gen) * rows ** -0.5
+    g = torch.randn(rows, cols, device="cuda", generator=gen)
+    res = {}
+
+    def refresh():
+        mask, rep = bs.generate_masks(w, g, b, s)
+        res["mask"], res["rep"] = mask, rep
+        return bs.apply_mask(w, mask, b, dtype=torch.bfloat16)
+
+    ms = _ev_median(refresh, iters, flush)
+    ms_gen = _ev_median(lambda: bs.generate_masks(w, g, b, s), iters, flush)
+    gr, gc = rows // b, cols // b
+    nw = torch.empty(gr, gc, dtype=torch.float64, device="cuda")
+    ng = torch.empty_like(nw)
+    ms_norms = _ev_median(lambda: L.check(L.load().blast_block_norms(
+        w.data_ptr(), g.data_ptr(), rows, cols, b, L.F32, nw.data_ptr(), ng.data_ptr(),
+        L.stream()), "norms"), iters, flush)
+    rep = res["rep"]
+    nnzb = rep.kept + rep.regrown
+    norm_bytes = 2 * rows * cols * 4
+    total_bytes = norm_bytes + 2 * rows * cols * 4 + nnzb * b * b * 2
+    return {"matrix": f"cfg3 gate {rows}x{cols} fp32 masters, b={b}, s={s}",
+            "ms_refresh": ms, "ms_generate_masks": ms_gen, "ms_apply_mask": ms - ms_gen,
+            "norms_us": ms_norms * 1e3, "norms_gbs": norm_bytes / (ms_norms * 1e-3) / 1e9,
+            "norms_frac_hbm": norm_bytes / (ms_norms * 1e-3) / 1e9 / hbm_peak,
+            "refresh_bytes": total_bytes,
+            "refresh_gbs": total_bytes / (ms * 1e-3) / 1e9,
+            "refresh_frac_hbm": total_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
+            "kept": rep.kept, "regrown": rep.regrown,
+            "host_syncs": "one (PruneReport counts)"}
+
+
+def extra_cfg0_fp32(bs, flush, tf_peak, iters, seed):
+    """configs[0]: one sparse MLP layer forward, d=2048 h=8192 b=64 90 %, 2048 tokens, fp32
+    (the reference's own precision; 3xTF32 tensor-core products)."""
+    import torch
+    d, h, m = 2048, 8192, 2048
+    ws = make_weights(d, h, BLOCK, SPARSITY, seed)
+    net = bs.SparseMlp.from_caches(*[bs.from_host(w, torch.float32) for w in ws])
+    x = torch.randn(m, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
+    ms = _ev_median(lambda: bs.mlp_forward(x, net, save_activations=False), iters, flush)
+    n = [len(w.block_row_idx) for w in ws]
+    flops = 2 * m * sum(n) * BLOCK * BLOCK
+    tf32_peak = tf_peak / 2  # no measured TF32 figure: dense TF32 is half the bf16 rate
+    ceiling_ms = 3 * flops / (tf32_peak * 1e12) * 1e3  # 3xTF32 issues three MMAs per product
+    return {"workload": "cfg0 fp32 fwd d=2048 h=8192 b=64 s=0.9, 2048 tokens", "ms": ms,
+            "tokens_per_s": m / (ms * 1e-3), "flops": flops,
+            "achieved_tflops_fp32": flops / (ms * 1e-3) / 1e12,
+            "ceiling_3xtf32_ms": ceiling_ms, "frac_of_3xtf32_ceiling": ceiling_ms / ms,
+            "tf32_peak_source": "measured bf16 burst / 2 (TF32 not measured)"}
+
+
+def extra_decode(bs, flush, hbm_peak, iters, seed):
+    """Decode-size forward: cfg3 shape at 95 % sparsity, 128 tokens, replayed as a CUDA graph
+    (GraphedMlpForward), L2 flushed before each replay so the weights come from HBM."""
+    import torch
+    m, s = 128, 0.95
+    ws = make_weights(D, H, BLOCK, s, seed)
+    mats = [bs.from_host(w, torch.bfloat16) for w in ws]
+    net = bs.SparseMlp.from_caches(*mats)
+    graphed = bs.GraphedMlpForward(net, m)
+    graphed.x.copy_(torch.randn(m, D, device="cuda").bfloat16())
+    ms = _ev_median(graphed.graph.replay, iters, flush)
+    wbytes = sum(w.nnzb for w in mats) * BLOCK * BLOCK * 2
+    idx = sum((w.grid_cols + 1) * 8 + w.nnzb * 4 for w in mats)
+    bytes_ = wbytes + idx + 2 * m * D * 2
+    return {"workload": "cfg3 shape, s=0.95, 128 tokens, CUDA graph replay", "us": ms * 1e3,
+            "bytes": bytes_, "gbs": bytes_ / (ms * 1e-3) / 1e9,
+            "frac_hbm": bytes_ / (ms * 1e-3) / 1e9 / hbm_peak,
+            "tokens_per_s": m / (ms * 1e-3)}
+
+
+def extra_cpu(weights, seed):
+    """The reference algorithm on the host: the cfg3 forward on ONE core, and its training
+    step (forward + backward + generate_masks + apply_mask of the three matrices,
+    mlp.py:102-143 and pruner.py:128-186) on all cores."""
+    import contextlib
+    import oracle
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    mats = [oracle.Bcsc(w.rows, w.cols, w.block, w.col_ptr, w.block_row_idx, w.values)
+            for w in weights]
+    rng = np.random.default_rng(seed)
+    out = {}
+    tok1 = 128
+    x = rng.standard_normal((tok1, D)).astype(np.float32)
+    ctx = threadpool_limits(limits=1) if threadpool_limits else contextlib.nullcontext()
+    with ctx:
+        oracle.mlp_forward(x, *mats)
+        t = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            oracle.mlp_forward(x, *mats)
+            t.append(time.perf_counter() - t0)
+    out["cpu_baseline_1core"] = {"value": tok1 / float(np.median(t)), "unit": "tokens/s",
+                                 "cores": 1, "kind": "port",
+                                 "sample": f"{tok1} tokens of the cfg3 forward, median of 2, "
+                                           "numpy/OpenBLAS fp32 on one thread"}
+    cores = len(os.sched_getaffinity(0))
+    tok = 256
+    x = rng.standard_normal((tok, D)).astype(np.float32)
+    dy = rng.standard_normal((tok, D)).astype(np.float32)
+    dense = [oracle.dense_of(w) for w in mats]
+    ctx = threadpool_limits(limits=cores) if threadpool_limits else contextlib.nullcontext()
+    with ctx:
+        t0 = time.perf_counter()
+        _, acts = oracle.mlp_forward(x, *mats)
+        grads = oracle.mlp_backward(dy, acts, *mats)
+        for wd, gd, w in zip(dense, grads[1:], mats):
+            mask, _ = oracle.generate_masks(wd, gd, w.block, SPARSITY)
+            oracle.apply_mask(wd, mask, w.block)
+        dt = time.perf_counter() - t0
+    out["cpu_train_step"] = {"value": tok / dt, "unit": "tokens/s", "cores": cores,
+                             "kind": "port", "seconds_per_step": dt,
+                             "sample": f"one training step over {tok} tokens of the cfg3 MLP: "
+                                       "forward + backward (full-grid dW) + generate_masks + "
+                                       "apply_mask of the 3 matrices, numpy/OpenBLAS fp32"}
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -154,7 +350,7 @@ def run_reference(args):
     weights = make_weights(D, H, BLOCK, SPARSITY, args.seed)
     tokens = args.ref_tokens
     times, cores = cpu_reference_time(weights, tokens, args.steps, args.warmup, args.seed)
-    step = float(np.mean(times))
+    step = float(np.median(times))
     value = tokens / step
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
@@ -353,8 +549,47 @@ def run_blast(args):
         line["dense_cublas"] = {"ms_per_step": dense_ms, "tokens_per_s": world * m / (dense_ms * 1e-3),
                                 "speedup_sparse_vs_dense": dense_ms / ms_per_step,
                                 "formulation": "torch bf16 F.linear x3 + silu*mul (HF LlamaMLP)"}
+    if not args.no_extras:
+        it = max(5, min(args.steps, 20))
+        line["train_step"] = extra_train_step(bs, net, x, world, flush, tf_peak, it)
+        if rank == 0:
+            line["prune_refresh"] = extra_prune_refresh(bs, L, flush, hbm_peak, it)
+            line["cfg0_fp32"] = extra_cfg0_fp32(bs, flush, tf_peak, it, args.seed)
+            line["decode"] = extra_decode(bs, flush, hbm_peak, it, args.seed)
+            if world == 1 and not args.no_cpu:
+                line.update(extra_cpu(weights, args.seed))
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def relaunch_with_ranks(n: int) -> int:
+    """Start this script with n ranks (one per GPU) through torch.distributed.run."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """Launcher check without a GPU: the ranks meet over gloo and rank 0 prints the
+    line skeleton (n_gpus = world size)."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "dry_run": True}),
+              flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -372,9 +607,18 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=2048)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--ref-tokens", type=int, default=512)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launcher check, no GPU work")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    if args.impl == "reference":
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_with_ranks(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_blast(args)

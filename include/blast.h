@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-enum { BLAST_F32 = 0, BLAST_BF16 = 1 };
+enum { BLAST_F32 = 0, BLAST_BF16 = 1, BLAST_F64 = 2 /* norms / masks inputs only */ };
 enum { BLAST_ACT_NONE = 0, BLAST_ACT_RELU = 1, BLAST_ACT_GELU = 2, BLAST_ACT_SILU = 3 };
 enum {
   BLAST_OK = 0,
@@ -183,7 +183,8 @@ int blast_block_wgrad_planned(const void* a, const void* d, int64_t m, int64_t r
 
 /* ---------------------------------------------------------------- prune-and-grow */
 /* Frobenius norm per b x b block in float64 (pruner.py:88-98); zero-padded edges.
- * x2 may be NULL; when given, its norms go to norms2 in the same pass (W and G). */
+ * x2 may be NULL; when given, its norms go to norms2 in the same pass (W and G).
+ * dtype: BLAST_F32, BLAST_BF16 or BLAST_F64 (every element squared in fp64). */
 int blast_block_norms(const void* x, const void* x2, int64_t rows, int64_t cols, int32_t block,
                       int dtype, double* norms, double* norms2, void* stream);
 /* Keep the k blocks with the largest norms; ties -> ascending (block col, block row)
@@ -201,6 +202,16 @@ int blast_topk_mask2(const double* norms_a, const double* norms_b, int64_t grid_
  * (pruner.py:142-156) */
 int blast_mask_difference(const uint8_t* kept, const uint8_t* grad_sel, int64_t n,
                           uint8_t* regrown, int64_t* counts, void* stream);
+/* generate_masks in one call (pruner.py:128-157): fp64 block norms of W and G, each in its
+ * own dtype (F32 / BF16 / F64; one pass when they match), kept = top-k(norms_w),
+ * regrown = top-k(norms_g) & ~kept, counts (device int64[2]) = |kept|, |regrown|; k as
+ * pruner.py:111. norms_* are [gr][gc] f64, kept / regrown uint8 [gr][gc]. When counts_host is
+ * not NULL the counts are copied there and the call synchronizes the stream (the one host
+ * sync of a refresh: PruneReport needs them). */
+int blast_generate_masks(const void* w, int dtype_w, const void* g, int dtype_g, int64_t rows,
+                         int64_t cols, int32_t block, int64_t k, double* norms_w,
+                         double* norms_g, uint8_t* kept, uint8_t* regrown, int64_t* counts,
+                         int64_t* counts_host, void* stream);
 /* Repack step 1 (bcsc.py:200-209): store = active mask (or any-nonzero blocks when
  * mask == NULL); col_ptr (int64 [gc+1]) by column counts + scan; kmap [gr][gc].
  * nnzb is col_ptr[gc] (left on device). */

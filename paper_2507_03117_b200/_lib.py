@@ -14,7 +14,7 @@ import torch
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libblast_b200.so"
 
-F32, BF16 = 0, 1
+F32, BF16, F64 = 0, 1, 2
 ACT = {"none": 0, "relu": 1, "gelu": 2, "silu": 3}
 
 OK, EINVAL, EMISMATCH, EGRID, ECUDA, ENOMEM = range(6)
@@ -74,6 +74,8 @@ _PROTOS = {
     "blast_wgrad_plan": (C.c_int, [vp, i64, i64, i32, vp, vp, vp]),
     "blast_block_wgrad_planned": (C.c_int, [vp, vp, i64, i64, i64, i32, C.c_int, vp, vp, i64,
                                             vp, vp, vp, vp]),
+    "blast_generate_masks": (C.c_int, [vp, C.c_int, vp, C.c_int, i64, i64, i32, i64, vp, vp, vp,
+                                       vp, vp, vp, vp]),
     "blast_block_norms": (C.c_int, [vp, vp, i64, i64, i32, C.c_int, vp, vp, vp]),
     "blast_topk_mask": (C.c_int, [vp, i64, i64, i64, vp, vp]),
     "blast_topk_mask2": (C.c_int, [vp, vp, i64, i64, i64, vp, vp, vp]),

@@ -234,6 +234,23 @@ class BlockMask:
     host callers or CUDA bool tensors for device callers."""
     kept: object
     regrown: object
+    # (|kept|, |regrown|) when known from the kernels that built the mask (generate_masks):
+    # lets apply_mask size the repack without reading nnzb back from the device
+    counts: tuple | None = field(default=None, compare=False, repr=False)
+
+    @classmethod
+    def trusted(cls, kept, regrown, n_kept: int, n_regrown: int) -> "BlockMask":
+        """Mask from grids that are disjoint by construction (device bool grids of
+        generate_masks): skips the validation pass and its host synchronisation."""
+        m = object.__new__(cls)
+        object.__setattr__(m, "kept", kept)
+        object.__setattr__(m, "regrown", regrown)
+        object.__setattr__(m, "counts", (int(n_kept), int(n_regrown)))
+        return m
+
+    @property
+    def known_active(self) -> int | None:
+        return None if self.counts is None else self.counts[0] + self.counts[1]
 
     def __post_init__(self):
         if A.shape(self.kept) != A.shape(self.regrown):
@@ -262,6 +279,8 @@ class BlockMask:
 
     @property
     def n_active(self) -> int:
+        if self.counts is not None:
+            return self.counts[0] + self.counts[1]
         a = self.active
         return int(a.sum().item()) if isinstance(a, torch.Tensor) else int(np.count_nonzero(a))
 
@@ -270,8 +289,12 @@ class BlockMask:
 
     def device_u8(self):
         """(kept, regrown) as contiguous uint8 CUDA grids for the kernels."""
-        return (A.to_device(self.kept).to(torch.uint8).contiguous(),
-                A.to_device(self.regrown).to(torch.uint8).contiguous())
+        def u8(g):
+            t = A.to_device(g)
+            if t.dtype == torch.bool and t.is_contiguous():
+                return t.view(torch.uint8)  # same bytes (0 / 1), no conversion kernel
+            return t.to(torch.uint8).contiguous()
+        return u8(self.kept), u8(self.regrown)
 
     @classmethod
     def all_active(cls, grid_rows: int, grid_cols: int, device: bool = False) -> "BlockMask":
@@ -302,8 +325,11 @@ def _check_dense(dense, b: int):
     return rows, cols
 
 
-def _repack(dense_t: torch.Tensor, b: int, kept_u8, regrown_u8, values_dtype: torch.dtype):
-    """Index pass of the repack: col_ptr + kmap on device, then nnzb (one D2H sync)."""
+def _repack(dense_t: torch.Tensor, b: int, kept_u8, regrown_u8, values_dtype: torch.dtype,
+            nnzb: int | None = None):
+    """Index pass of the repack: col_ptr + kmap on device. ``nnzb`` (the active-block count,
+    known after generate_masks) sizes the outputs without a host round trip; otherwise it is
+    read back from col_ptr (one D2H sync)."""
     lib = L.load()
     rows, cols = dense_t.shape
     gr, gc = _grid_dim(rows, b), _grid_dim(cols, b)
@@ -312,7 +338,8 @@ def _repack(dense_t: torch.Tensor, b: int, kept_u8, regrown_u8, values_dtype: to
     L.check(lib.blast_repack_index(L.ptr(kept_u8), L.ptr(regrown_u8), dense_t.data_ptr(), rows,
                                    cols, b, L.dtype_code(dense_t.dtype), col_ptr.data_ptr(),
                                    kmap.data_ptr(), L.stream()), "repack_index")
-    nnzb = int(col_ptr[-1].item())
+    if nnzb is None:
+        nnzb = int(col_ptr[-1].item())
     row_idx = torch.empty(nnzb, dtype=torch.int32, device=A.DEVICE)
     if nnzb:
         L.check(lib.blast_repack_rows(kmap.data_ptr(), col_ptr.data_ptr(), gr, gc,

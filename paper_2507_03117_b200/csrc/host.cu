@@ -34,7 +34,7 @@ int num_sms() {
   return n[dev];
 }
 
-int bytes_of(int dtype) { return dtype == BLAST_BF16 ? 2 : 4; }
+int bytes_of(int dtype) { return dtype == BLAST_BF16 ? 2 : dtype == BLAST_F64 ? 8 : 4; }
 
 void retain_pool_memory() {
   // The default stream-ordered pool returns freed memory to the driver at every

@@ -19,6 +19,12 @@ namespace blast {
 // geometry allows it, accumulating x*x in float64 (each product of two fp32
 // values is exact in fp64, as in pruner.py:95's astype(float64)). The warp
 // reduction tree is fixed, so the result is deterministic.
+__device__ __forceinline__ double to_f64(double v) { return v; }
+__device__ __forceinline__ double to_f64(float v) { return static_cast<double>(v); }
+__device__ __forceinline__ double to_f64(__nv_bfloat16 v) {
+  return static_cast<double>(__bfloat162float(v));
+}
+
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) block_norms_kernel(const T* __restrict__ x,
                                                           const T* __restrict__ x2, int64_t rows,
@@ -44,7 +50,12 @@ __global__ void __launch_bounds__(256) block_norms_kernel(const T* __restrict__ 
       for (int e = lane; e < total; e += 32) {
         const int ii = e / per_row, jj = (e - ii * per_row) * VW;
         const uint4 q = __ldg(reinterpret_cast<const uint4*>(src + (i0 + ii) * cols + j0 + jj));
-        if constexpr (sizeof(T) == 4) {
+        if constexpr (sizeof(T) == 8) {
+          const double d0 = __hiloint2double(static_cast<int>(q.y), static_cast<int>(q.x));
+          const double d1 = __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z));
+          acc = fma(d0, d0, acc);
+          acc = fma(d1, d1, acc);
+        } else if constexpr (sizeof(T) == 4) {
           const float f[4] = {__uint_as_float(q.x), __uint_as_float(q.y), __uint_as_float(q.z),
                               __uint_as_float(q.w)};
 #pragma unroll
@@ -63,7 +74,7 @@ __global__ void __launch_bounds__(256) block_norms_kernel(const T* __restrict__ 
       const int64_t total = ih * jw;
       for (int64_t e = lane; e < total; e += 32) {
         const int64_t ii = e / jw, jj = e - ii * jw;
-        const double v = (double)to_f32<T>(src[(i0 + ii) * cols + j0 + jj]);
+        const double v = to_f64(src[(i0 + ii) * cols + j0 + jj]);
         acc = fma(v, v, acc);
       }
     }
@@ -564,42 +575,57 @@ static int grid_for(int64_t n, int threads, int per_sm = 16) {
 
 using namespace blast;
 
-extern "C" int blast_block_norms(const void* x, const void* x2, int64_t rows, int64_t cols,
-                                 int32_t block, int dtype, double* norms, double* norms2,
-                                 void* stream) {
+namespace blast {
+template <typename T>
+static void norms_launch(const void* x, const void* x2, int64_t rows, int64_t cols, int block,
+                         double* norms, double* norms2, cudaStream_t st) {
+  const int64_t gr = cdiv(rows, block), gc = cdiv(cols, block);
+  constexpr int vw = 16 / sizeof(T);
+  const bool vec = block % vw == 0 && rows % block == 0 && cols % block == 0 && aligned16(x) &&
+                   (!x2 || aligned16(x2)) && (cols * static_cast<int64_t>(sizeof(T))) % 16 == 0;
+  dim3 grid(grid_for(gr * gc * 32, 256, 32), x2 ? 2 : 1);
+  auto* a = static_cast<const T*>(x);
+  auto* a2 = static_cast<const T*>(x2);
+  if (vec)
+    block_norms_kernel<T, true><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr, gc, norms, norms2);
+  else
+    block_norms_kernel<T, false><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr, gc, norms, norms2);
+}
+
+// norms of x (dtype) and, when given, of x2 (dtype2): one launch covers both when they share a
+// dtype (blockIdx.y picks the matrix), else one launch each; every element is squared in fp64.
+static int norms_any(const void* x, int dtype, const void* x2, int dtype2, int64_t rows,
+                     int64_t cols, int block, double* norms, double* norms2, cudaStream_t st) {
   if (rows < 1 || cols < 1 || block < 1) {
     set_error("block_norms: invalid shape %lld x %lld block %d", (long long)rows, (long long)cols,
               block);
     return BLAST_EINVAL;
   }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t gr = cdiv(rows, block), gc = cdiv(cols, block);
-  const int64_t nblk = gr * gc;
-  const int elt = bytes_of(dtype);
-  const int vw = 16 / elt;
-  const bool vec = block % vw == 0 && rows % block == 0 && cols % block == 0 && aligned16(x) &&
-                   (!x2 || aligned16(x2)) && (cols * elt) % 16 == 0;
-  dim3 grid(grid_for(nblk * 32, 256, 32), x2 ? 2 : 1);
-  if (dtype == BLAST_BF16) {
-    auto* a = static_cast<const __nv_bfloat16*>(x);
-    auto* a2 = static_cast<const __nv_bfloat16*>(x2);
-    if (vec)
-      block_norms_kernel<__nv_bfloat16, true><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr,
-                                                                    gc, norms, norms2);
-    else
-      block_norms_kernel<__nv_bfloat16, false><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr,
-                                                                     gc, norms, norms2);
+  for (int d : {dtype, x2 ? dtype2 : dtype})
+    if (d != BLAST_F32 && d != BLAST_BF16 && d != BLAST_F64) {
+      set_error("block_norms: unsupported dtype %d", d);
+      return BLAST_EINVAL;
+    }
+  auto one = [&](const void* a, const void* a2, int d, double* o, double* o2) {
+    if (d == BLAST_BF16) norms_launch<__nv_bfloat16>(a, a2, rows, cols, block, o, o2, st);
+    else if (d == BLAST_F64) norms_launch<double>(a, a2, rows, cols, block, o, o2, st);
+    else norms_launch<float>(a, a2, rows, cols, block, o, o2, st);
+  };
+  if (!x2 || dtype2 == dtype) {
+    one(x, x2, dtype, norms, norms2);
   } else {
-    auto* a = static_cast<const float*>(x);
-    auto* a2 = static_cast<const float*>(x2);
-    if (vec)
-      block_norms_kernel<float, true><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr, gc,
-                                                            norms, norms2);
-    else
-      block_norms_kernel<float, false><<<grid, 256, 0, st>>>(a, a2, rows, cols, block, gr, gc,
-                                                             norms, norms2);
+    one(x, nullptr, dtype, norms, nullptr);
+    one(x2, nullptr, dtype2, norms2, nullptr);
   }
   return check_launch("block_norms");
+}
+}  // namespace blast
+
+extern "C" int blast_block_norms(const void* x, const void* x2, int64_t rows, int64_t cols,
+                                 int32_t block, int dtype, double* norms, double* norms2,
+                                 void* stream) {
+  return norms_any(x, dtype, x2, dtype, rows, cols, block, norms, norms2,
+                   static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int blast_topk_mask(const double* norms, int64_t grid_rows, int64_t grid_cols,
@@ -653,6 +679,30 @@ extern "C" int blast_mask_difference(const uint8_t* kept, const uint8_t* grad_se
       kept, grad_sel, n, regrown, reinterpret_cast<unsigned long long*>(counts));
   return check_launch("mask_difference");
 }
+
+extern "C" int blast_generate_masks(const void* w, int dtype_w, const void* g, int dtype_g,
+                                    int64_t rows, int64_t cols, int32_t block, int64_t k,
+                                    double* norms_w, double* norms_g, uint8_t* kept,
+                                    uint8_t* regrown, int64_t* counts, int64_t* counts_host,
+                                    void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int r = norms_any(w, dtype_w, g, dtype_g, rows, cols, block, norms_w, norms_g, st);
+  if (r) return r;
+  const int64_t gr = cdiv(rows, block), gc = cdiv(cols, block);
+  // grad_sel goes into `regrown` and is turned into grad_sel & ~kept in place
+  r = blast_topk_mask2(norms_w, norms_g, gr, gc, k, kept, regrown, stream);
+  if (r) return r;
+  r = blast_mask_difference(kept, regrown, gr * gc, regrown, counts, stream);
+  if (r) return r;
+  if (counts_host) {
+    cudaError_t e = cudaMemcpyAsync(counts_host, counts, 2 * sizeof(int64_t),
+                                    cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return cuda_status(e, "generate_masks counts");
+  }
+  return BLAST_OK;
+}
+
 
 extern "C" int blast_repack_index(const uint8_t* kept, const uint8_t* regrown, const void* dense,
                                   int64_t rows, int64_t cols, int32_t block, int dtype,

@@ -146,8 +146,11 @@ class TPShardedMlp:
             mats.append(ops.MaskedMatrix.dense_init(dense, b, dtype))
         return cls(ops.SparseMlp(*mats), rank, world, ops, group)
 
-    def forward(self, x):
-        y_part, acts = self.ops.mlp_forward(x, self.net)
+    def forward(self, x, save_activations: bool = True):
+        """Column/row-parallel forward + all-reduce of the partial Y. Inference
+        (save_activations=False) keeps the intermediate inside the library and returns
+        (y, None)."""
+        y_part, acts = self.ops.mlp_forward(x, self.net, save_activations=save_activations)
         y = _all_reduce_sum_(torch.as_tensor(y_part), self.group)
         return y, acts
 

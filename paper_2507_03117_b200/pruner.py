@@ -91,37 +91,17 @@ def _norms_device(w: torch.Tensor, g: torch.Tensor | None, b: int):
     gr, gc = -(-rows // b), -(-cols // b)
     nw = torch.empty(gr, gc, dtype=torch.float64, device=A.DEVICE)
     ng = torch.empty(gr, gc, dtype=torch.float64, device=A.DEVICE) if g is not None else None
-    L.check(L.load().blast_block_norms(w.data_ptr(), L.ptr(g), rows, cols, b,
-                                       L.dtype_code(w.dtype), nw.data_ptr(), L.ptr(ng),
-                                       L.stream()), "block_norms")
+    L.check(L.load().blast_block_norms(w.data_ptr(), L.ptr(g), rows, cols, b, _norm_code(w),
+                                       nw.data_ptr(), L.ptr(ng), L.stream()), "block_norms")
     return nw, ng
 
 
-def _as_compute(x):
-    """float32 / bfloat16 device tensor of a dense matrix (float64 inputs become float32:
-    the reference's norms of an f32 master are norms of f32 values)."""
-    t = A.to_device(x)
-    if t.dtype not in (torch.float32, torch.bfloat16):
-        t = t.to(torch.float32)
-    return t.contiguous()
-
-
 def block_norms(dense, b: int):
-    """Frobenius norm of each b x b block in float64 (boundary blocks zero-padded)."""
+    """Frobenius norm of each b x b block in float64 (boundary blocks zero-padded)
+    (pruner.py:88-98). float32, bfloat16 and float64 inputs are read in their own precision."""
     _check_block_input(dense, b)
     host = A.is_host(dense)
-    arr = dense
-    if host and np.asarray(dense).dtype == np.float64:
-        # float64 input: the reference keeps full float64 precision (pruner.py:95); this
-        # non-hot-path case is evaluated with fp64 torch reductions on the device.
-        t = A.to_device(np.asarray(dense, dtype=np.float64))
-        rows, cols = t.shape
-        gr, gc = -(-rows // b), -(-cols // b)
-        pad = torch.zeros(gr * b, gc * b, dtype=torch.float64, device=A.DEVICE)
-        pad[:rows, :cols] = t
-        out = pad.view(gr, b, gc, b).square().sum(dim=(1, 3)).sqrt()
-        return A.to_host(out)
-    nw, _ = _norms_device(_as_compute(arr), None, b)
+    nw, _ = _norms_device(_norm_input(dense), None, b)
     return A.like_input(nw, host)
 
 
@@ -151,33 +131,64 @@ def prune_s(norms, s: float):
     return A.like_input(keep, host)
 
 
+def _norm_input(x) -> torch.Tensor:
+    """Device tensor of a dense matrix for the norm kernels, in its own precision: float32,
+    bfloat16 and float64 are read as given (every element squared in fp64, pruner.py:95);
+    other dtypes are widened to float32."""
+    t = A.to_device(x)
+    if t.dtype not in (torch.float32, torch.bfloat16, torch.float64):
+        t = t.to(torch.float32)
+    return t.contiguous()
+
+
+def _norm_code(t: torch.Tensor) -> int:
+    return L.F64 if t.dtype == torch.float64 else L.dtype_code(t.dtype)
+
+
+_COUNTS_HOST = {}
+
+
+def _pinned_counts() -> torch.Tensor:
+    dev = torch.cuda.current_device()
+    buf = _COUNTS_HOST.get(dev)
+    if buf is None:
+        buf = torch.zeros(2, dtype=torch.int64).pin_memory()
+        _COUNTS_HOST[dev] = buf
+    return buf
+
+
 def generate_masks(w_dense, g_dense, b: int, s: float, iteration: int = 0):
     """kept = top-k(|W| block norms), regrown = top-k(|G| block norms) minus kept
-    (pruner.py:128-157). One fused norm pass reads W and G; the report counts come
-    back in a single 16-byte device-to-host copy."""
+    (pruner.py:128-157). One library call (blast_generate_masks): a fused norm pass over W
+    and G, each in its own dtype, both top-k selections and the set difference; the report
+    counts come back in the one host synchronisation of a refresh."""
     if A.shape(w_dense) != A.shape(g_dense):
         raise ValueError(f"weight shape {A.shape(w_dense)} != gradient shape {A.shape(g_dense)}")
     _check_block_input(w_dense, b)
     if not 0.0 <= s <= 1.0:
         raise ValueError(f"sparsity must be in [0, 1], got {s}")
     host = A.is_host(w_dense)
-    w = _as_compute(w_dense)
-    g = _as_compute(g_dense).to(w.dtype)
-    nw, ng = _norms_device(w, g, b)
-    gr, gc = nw.shape
+    w, g = _norm_input(w_dense), _norm_input(g_dense)
+    rows, cols = w.shape
+    gr, gc = -(-rows // b), -(-cols // b)
     total = gr * gc
     k = _k_of(s, total)
+    nw = torch.empty(gr, gc, dtype=torch.float64, device=A.DEVICE)
+    ng = torch.empty_like(nw)
     kept = torch.empty(gr, gc, dtype=torch.uint8, device=A.DEVICE)
-    gsel = torch.empty_like(kept)
-    L.check(L.load().blast_topk_mask2(nw.data_ptr(), ng.data_ptr(), gr, gc, k, kept.data_ptr(),
-                                      gsel.data_ptr(), L.stream()), "topk")
     regrown = torch.empty_like(kept)
     counts = torch.empty(2, dtype=torch.int64, device=A.DEVICE)
-    L.check(L.load().blast_mask_difference(kept.data_ptr(), gsel.data_ptr(), total,
-                                           regrown.data_ptr(), counts.data_ptr(), L.stream()),
-            "mask_difference")
-    n_kept, n_regrown = (int(v) for v in counts.cpu().tolist())
-    mask = BlockMask(kept=A.like_input(kept.bool(), host), regrown=A.like_input(regrown.bool(), host))
+    counts_h = _pinned_counts()
+    L.check(L.load().blast_generate_masks(w.data_ptr(), _norm_code(w), g.data_ptr(), _norm_code(g),
+                                          rows, cols, b, k, nw.data_ptr(), ng.data_ptr(),
+                                          kept.data_ptr(), regrown.data_ptr(), counts.data_ptr(),
+                                          counts_h.data_ptr(), L.stream()), "generate_masks")
+    n_kept, n_regrown = int(counts_h[0]), int(counts_h[1])
+    kept_b, regrown_b = kept.view(torch.bool), regrown.view(torch.bool)
+    if host:
+        mask = BlockMask(kept=A.to_host(kept_b), regrown=A.to_host(regrown_b))
+    else:  # disjoint by construction; the counts ride along for apply_mask (no nnzb sync)
+        mask = BlockMask.trusted(kept_b, regrown_b, n_kept, n_regrown)
     report = PruneReport(iteration=iteration, s_target=s, kept=n_kept, regrown=n_regrown,
                          regrown_ratio=n_regrown / total,
                          s_achieved=1.0 - (n_kept + n_regrown) / total)
@@ -209,7 +220,8 @@ def apply_mask(w_dense, mask: BlockMask, b: int, zero_regrown: bool = True,
         values = alloc((structure.nnzb, b, b), dtype=vdt, device=A.DEVICE)
         plans = {k: v for k, v in structure._cache.items() if k[0] == "plan"}
     else:
-        col_ptr, row_idx, kmap, values = bcsc._repack(w, b, kept, regrown, vdt)
+        col_ptr, row_idx, kmap, values = bcsc._repack(w, b, kept, regrown, vdt,
+                                                      nnzb=mask.known_active)
         plans = {}
     masked = torch.empty_like(w)
     L.check(L.load().blast_apply_mask_gather(w.data_ptr(), rows, cols, b, L.F32, kept.data_ptr(),

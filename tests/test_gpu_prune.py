@@ -217,3 +217,46 @@ class TestApplyMask:
         _, c32 = bs.apply_mask(w, mask, 64)
         _, c16 = bs.apply_mask(w, mask, 64, dtype=torch.bfloat16)
         assert torch.equal(c32.values.bfloat16(), c16.values)
+
+
+@pytest.mark.parametrize("wdt,gdt", [(torch.float64, torch.float64), (torch.bfloat16, torch.float32),
+                                     (torch.float32, torch.bfloat16), (torch.float64, torch.float32)])
+def test_generate_masks_input_precisions(wdt, gdt):
+    """Norms are taken of each matrix in its own precision (pruner.py:95 squares the values
+    as given in float64): W and G of different dtypes, and float64 masters, give the oracle's
+    masks and counts on the same values."""
+    rng = np.random.default_rng(11)
+    rows, cols, b, s = 320, 448, 32, 0.8
+    w = torch.from_numpy(rng.standard_normal((rows, cols))).to(wdt).cuda()
+    g = torch.from_numpy(rng.standard_normal((rows, cols))).to(gdt).cuda()
+    mask, rep = bs.generate_masks(w, g, b, s)
+    wn, gn = (t.double().cpu().numpy() for t in (w, g))
+    np.testing.assert_allclose(bs.block_norms(w, b).cpu().numpy(), oracle.block_norms(wn, b),
+                               rtol=1e-13, atol=0)
+    ref_mask, ref_rep = oracle.generate_masks(wn, gn, b, s)
+    np.testing.assert_array_equal(mask.kept.cpu().numpy(), ref_mask.kept)
+    np.testing.assert_array_equal(mask.regrown.cpu().numpy(), ref_mask.regrown)
+    assert (rep.kept, rep.regrown) == (int(ref_mask.kept.sum()), int(ref_mask.regrown.sum()))
+
+
+def test_device_refresh_without_host_round_trips():
+    """Device masks carry their counts from generate_masks, so apply_mask sizes the repack
+    without reading nnzb back; the result equals the host-input path bit for bit."""
+    rng = np.random.default_rng(12)
+    rows, cols, b, s = 512, 768, 64, 0.75
+    w = rng.standard_normal((rows, cols)).astype(np.float32)
+    g = rng.standard_normal((rows, cols)).astype(np.float32)
+    mask_d, rep_d = bs.generate_masks(torch.from_numpy(w).cuda(), torch.from_numpy(g).cuda(), b, s)
+    assert mask_d.counts == (rep_d.kept, rep_d.regrown)
+    assert mask_d.n_active == rep_d.kept + rep_d.regrown
+    masked_d, cache_d = bs.apply_mask(torch.from_numpy(w).cuda(), mask_d, b)
+    mask_h, rep_h = bs.generate_masks(w, g, b, s)
+    masked_h, cache_h = bs.apply_mask(w, mask_h, b)
+    assert (rep_d.kept, rep_d.regrown) == (rep_h.kept, rep_h.regrown)
+    assert_bits_equal(masked_d.cpu().numpy(), masked_h)
+    hd, hh = cache_d.to_host(), cache_h.to_host()
+    np.testing.assert_array_equal(hd.col_ptr, hh.col_ptr)
+    np.testing.assert_array_equal(hd.block_row_idx, hh.block_row_idx)
+    assert_bits_equal(hd.values, hh.values)
+    ref = oracle.apply_mask(w, oracle.generate_masks(w, g, b, s)[0], b)
+    assert_cache_equal(cache_d, ref[1])

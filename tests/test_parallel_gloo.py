@@ -35,9 +35,9 @@ class OracleOps:
             self.mats = (gate.cache, up.cache, down.cache)
 
     @staticmethod
-    def mlp_forward(x, net):
+    def mlp_forward(x, net, save_activations=True):
         y, acts = oracle.mlp_forward(np.asarray(x), *net.mats)
-        return torch.from_numpy(y), acts
+        return torch.from_numpy(y), (acts if save_activations else None)
 
     @staticmethod
     def mlp_backward(dy, acts, net, grad_mode="full"):
@@ -97,6 +97,8 @@ def _tp_fwd_bwd(rank, world):
     shard = parallel.TPShardedMlp.from_dense(wg, wu, wd, B, rank, world, ops=OracleOps)
     y, acts = shard.forward(torch.from_numpy(x))
     dx, dwg, dwu, dwd = shard.backward(torch.from_numpy(dy), acts)
+    y_inf, none = shard.forward(torch.from_numpy(x), save_activations=False)
+    assert none is None and np.array_equal(y_inf.numpy(), y.numpy())
     return y.numpy(), dx.numpy(), dwg, dwu, dwd
 
 
