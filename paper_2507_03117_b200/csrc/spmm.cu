@@ -144,7 +144,7 @@ template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typen
           int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
-  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM, IN_ST, SPLIT>;
+  using Cfg = TcCfg<B, ELT, NPASS, NMAT, SUM, BK, OUT_ELT, TM, IN_ST, SPLIT, staged_outputs<EPI>()>;
   auto kern = spmm_tc_kernel<B, ELT, NPASS, NMAT, SUM, BK, EPI, OutT, OUT_ELT, TM, SPLIT>;
   static bool configured[64] = {};
   if (int rc = configure_smem(kern, Cfg::SMEM_BYTES, configured, "spmm_tc smem attribute"))
@@ -190,12 +190,17 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
                        static_cast<uint64_t>(c.n_valid), static_cast<uint64_t>(c.m),
                        static_cast<uint64_t>(c.ld_out) * OUT_ELT, Cfg::OUT_SW / (OUT_ELT ? OUT_ELT : 1),
                        Cfg::BM, Cfg::OUT_SW);
-  // staged in0 tiles (activation-derivative epilogue): same geometry as the output
-  CUtensorMap mI = mO;
-  if (ok && IN_ST)
-    ok = encode_map_2d(&mI, c.in0, BLAST_BF16, static_cast<uint64_t>(c.n_valid),
-                       static_cast<uint64_t>(c.m), static_cast<uint64_t>(c.ld_out) * 2,
-                       Cfg::OUT_SW / 2, Cfg::BM, Cfg::OUT_SW);
+  // staged in0 (and in1) tiles (activation-derivative / gating-backward epilogues) and the
+  // second staged output (dB): same geometry as the output
+  CUtensorMap mI = mO, mI1 = mO, mO1 = mO, mO2 = mO;
+  auto mkTile = [&](CUtensorMap* mp, const void* ptr) {
+    return encode_map_2d(mp, ptr, BLAST_BF16, static_cast<uint64_t>(c.n_valid),
+                         static_cast<uint64_t>(c.m), static_cast<uint64_t>(c.ld_out) * 2,
+                         Cfg::OUT_SW / 2, Cfg::BM, Cfg::OUT_SW);
+  };
+  if (ok && IN_ST) ok = mkTile(&mI, c.in0);
+  if (ok && IN_ST == 2) ok = mkTile(&mI1, c.in1) && mkTile(&mO1, c.out1);
+  if (ok && EPI == EPI_GATED_FWD_SAVE) ok = mkTile(&mO1, c.out1) && mkTile(&mO2, c.out2);
   if (!ok) return BLAST_EINVAL;
   SpmmParams p = make_params(c);
   p.n_tok_tiles = static_cast<int32_t>(cdiv(c.m, Cfg::TROWS));
@@ -223,7 +228,8 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, mO, mI, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1, mW1lo, p);
+  cudaLaunchKernelEx(&cfg, kern, mO, mI, mO1, mI1, mO2, mA0, mA0lo, mA1, mA1lo, mW0, mW0lo, mW1,
+                     mW1lo, p);
   const int rc = check_launch("spmm_tc");
   dbg_end("spmm_tc", st, grid);
   return rc;
@@ -263,7 +269,8 @@ constexpr bool staged_fits() {
   constexpr int b_tile = (B * rowb + 1023) / 1024 * 1024;
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
-  constexpr int staging = (2 + 2 * IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
+  constexpr int nout = IN_ST == 2 ? 2 : 1;
+  constexpr int staging = (2 * nout + 2 * IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
   return (232448 - 1024 - 512 - staging) / stage >= 3;
 }
 // gate+up stage layout (TcCfg SPLIT) for the 256-token staged product:
@@ -306,8 +313,11 @@ template <int B, int ELT, int NPASS, int NMAT, bool SUM>
 static bool use_staged(const EngineCall& c) {
   if (!staged_fits<B, ELT, NPASS, NMAT, SUM>() || staged_out_disabled()) return false;
   if (c.accumulate || !aligned16(c.out0) || (c.ld_out * 2) % 16 != 0) return false;
-  // EPI_GATED_BWD: only the single-output form (y = (x W^T) * act'(pre)) is staged
-  return c.epi == EPI_STORE || c.epi == EPI_GATED_FWD || (c.epi == EPI_GATED_BWD && !c.in1);
+  // EPI_GATED_BWD: the single-output form (y = (x W^T) * act'(pre)) and the two-input gating
+  // backward (EPI_GATED_BWD2, needs its second input / output 16-byte aligned too)
+  if (c.epi == EPI_GATED_BWD && c.in1)
+    return aligned16(c.in0) && aligned16(c.in1) && c.out1 && aligned16(c.out1);
+  return c.epi == EPI_STORE || c.epi == EPI_GATED_FWD || c.epi == EPI_GATED_BWD;
 }
 
 template <int B, int ELT, int NPASS, typename OutT>
@@ -329,7 +339,10 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
         if constexpr (staged_fits<B, ELT, NPASS, 2, false, 2>())
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
             return (split_stages() == 2 && seq_gate_up_pays<B>(c))
-                       ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 2>(c, a0lo, a1lo, st)
+                       ? ((c.out1 && c.out2 && aligned16(c.out1) && aligned16(c.out2))
+                              // training forward: G, a and b all through staged TMA stores
+                              ? launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD_SAVE, OutT, SO, 2, 2>(c, a0lo, a1lo, st)
+                              : launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2, 2>(c, a0lo, a1lo, st))
                        : launch_tc<B, ELT, NPASS, 2, false, (ELT == 4), EPI_GATED_FWD, OutT, SO, 2>(c, a0lo, a1lo, st);
         if constexpr (staged_fits<B, ELT, NPASS, 2, false>())
           if (use_staged<B, ELT, NPASS, 2, false>(c))
@@ -347,6 +360,13 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
           return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
+    } else if (c.nmat == 1 && c.epi == EPI_GATED_BWD && c.in1) {
+      // gating backward (dA, dB): a, b in and dA, dB out through staged TMA tiles
+      if constexpr (staged_fits<B, ELT, NPASS, 1, false, 1, 2>())
+        if (use_staged<B, ELT, NPASS, 1, false>(c))
+          return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD2, OutT, SO>(c, a0lo, a1lo, st);
+      if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
+        return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT>(c, a0lo, a1lo, st);
     } else if (c.nmat == 1 && c.epi == EPI_GATED_BWD) {
       if constexpr (staged_fits<B, ELT, NPASS, 1, false, 2, 1>())
         if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles() &&
@@ -358,6 +378,16 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT>(c, a0lo, a1lo, st);
     } else if (c.nmat == 2 && c.sumacc && c.epi == EPI_STORE) {
+      // dX = dA Wg^T + dB Wu^T in one accumulator, staged (TMA-store) output. 256-token items
+      // with the sequential layout (all dA blocks of the line, then all dB blocks; one panel +
+      // one weight block per stage, as the gate+up forward) where steps holding both are rare
+      if constexpr (ELT == 2 && NPASS == 1 && B >= 64)
+        if (use_staged<B, ELT, NPASS, 2, true>(c) && c.m >= 256 && wide_tiles() &&
+            split_stages() == 2 && seq_gate_up_pays<B>(c))
+          return launch_tc<B, ELT, NPASS, 2, true, true, EPI_STORE, OutT, SO, 2, 2>(c, a0lo, a1lo, st);
+      if constexpr (staged_fits<B, ELT, NPASS, 2, true>())
+        if (use_staged<B, ELT, NPASS, 2, true>(c))
+          return launch_tc<B, ELT, NPASS, 2, true, true, EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
       if constexpr (tc_fits<B, ELT, NPASS, 2, true>())
         return launch_tc<B, ELT, NPASS, 2, true, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
     }

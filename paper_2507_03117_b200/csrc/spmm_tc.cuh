@@ -27,7 +27,23 @@
 
 namespace blast {
 
-enum Epi : int { EPI_STORE = 0, EPI_GATED_FWD = 1, EPI_GATED_BWD = 2 };
+// EPI_GATED_BWD2: the two-input gating backward (dA, dB from dG, a, b) with both inputs and
+// both outputs staged through shared memory by TMA (the engine-level form of EPI_GATED_BWD
+// with in1 set; see in_staged)
+// EPI_GATED_FWD_SAVE: the training gated forward (G plus the saved a, b), all three outputs
+// staged through shared memory and written by TMA stores.
+enum Epi : int {
+  EPI_STORE = 0,
+  EPI_GATED_FWD = 1,
+  EPI_GATED_BWD = 2,
+  EPI_GATED_BWD2 = 3,
+  EPI_GATED_FWD_SAVE = 4
+};
+// staged output tiles per 128-row output tile
+template <int EPI>
+constexpr int staged_outputs() {
+  return EPI == EPI_GATED_BWD2 ? 2 : EPI == EPI_GATED_FWD_SAVE ? 3 : 1;
+}
 
 struct SpmmParams {
   int32_t m;            // activation rows (tokens)
@@ -151,6 +167,8 @@ struct StepCursor {
 // IN_ST = 1 (staged single-input activation-derivative epilogue): the epilogue also stages the
 // items' `in0` tiles (TM x 128 rows x B) in shared memory with one TMA load per tile, one item
 // ahead (double-buffered), instead of row-strided per-thread loads.
+// IN_ST = 2 (EPI_GATED_BWD2): both inputs (a, b) staged that way, and both outputs (dA, dB)
+// leave through staged tiles and TMA stores.
 // SPLIT = 1 (gate+up): a stage carries ONE weight block; a step with both a gate and an up
 // block becomes two stages (the panel is loaded twice, ~5 % of steps at 90 % sparsity), and
 // the output is staged single-buffered. The 16 + 16 KB saved buy a fifth pipeline stage,
@@ -160,7 +178,7 @@ struct StepCursor {
 // the stage index against the line's gate-block count (plan flags) and a waiter warp
 // handles the mbarriers, as for single-matrix products.
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int OUT_ELT = 0,
-          int TM = 1, int IN_ST = 0, int SPLIT = 0>
+          int TM = 1, int IN_ST = 0, int SPLIT = 0, int NOUT_ = 1>
 struct TcCfg {
   static constexpr int BM = 128;                          // rows per MMA / per output tile
   static constexpr int TROWS = BM * TM;                   // token rows per item
@@ -171,7 +189,7 @@ struct TcCfg {
   static constexpr int MMA_K = 32 / ELT;                  // 16 (bf16) / 8 (tf32)
   static constexpr int KSL = B / MMA_K;                   // MMAs per block along K
   static constexpr int NCOPY = NPASS == 3 ? 2 : 1;        // hi / lo operand copies
-  static constexpr int NA = SUMACC ? NMAT : 1;            // distinct A panels per step
+  static constexpr int NA = (SUMACC && !SPLIT) ? NMAT : 1;  // distinct A panels per stage
   static constexpr int round1k(int x) { return (x + 1023) / 1024 * 1024; }
   static constexpr int A_TILE = round1k(TROWS * ROWB);
   static constexpr int B_TILE = round1k(B * ROWB);
@@ -188,8 +206,9 @@ struct TcCfg {
   static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
   static constexpr int OUT_TILE = OUT_ELT ? round1k(BM * OUT_ROWB) : 0;
-  static constexpr int IN_STAGING = IN_ST ? 2 * TM * OUT_TILE : 0;  // double-buffered by item
-  static constexpr int STAGING = OUT_BUFS * OUT_TILE + IN_STAGING;
+  static constexpr int NOUT = NOUT_;                                // staged outputs per tile
+  static constexpr int IN_STAGING = IN_ST * 2 * TM * OUT_TILE;      // [2 bufs][IN_ST][TM] tiles
+  static constexpr int STAGING = OUT_BUFS * NOUT * OUT_TILE + IN_STAGING;
   // 227 KB opt-in maximum minus barriers, alignment slack and the output staging
   static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 512 - STAGING : 200 * 1024;
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
@@ -362,7 +381,8 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
                                                float (&v1)[16], int flags, bool row_ok,
                                                int col, int valid, int64_t off, bool vec_ok,
                                                uint8_t* stg = nullptr, int trow = 0,
-                                               int tcol = 0, const uint8_t* in_stg = nullptr) {
+                                               int tcol = 0, const uint8_t* in_stg = nullptr,
+                                               int out1_off = 0, int in1_off = 0) {
   const bool live = row_ok && valid > 0;
   if constexpr (EPI == EPI_STORE) {
     add_bias16(v0, p.bias, col, valid);
@@ -409,6 +429,39 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
       else
         store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
     }
+  } else if constexpr (EPI == EPI_GATED_FWD_SAVE) {
+    // G, a, b into three staged tiles (rows / columns outside the tensor clipped by TMA)
+    static_assert(STG_SW > 0, "EPI_GATED_FWD_SAVE is the staged form");
+    if (!(flags & 2)) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v1[i] = 0.0f;
+    }
+    float g[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if constexpr (sizeof(OutT) == 2)
+        g[i] = gated_fwd_fast(v0[i], v1[i]);
+      else
+        g[i] = gated_fwd(v0[i], v1[i]);
+    }
+    stage_chunk16<OutT, STG_SW>(stg, trow, tcol, g);
+    stage_chunk16<OutT, STG_SW>(stg + out1_off, trow, tcol, v0);
+    stage_chunk16<OutT, STG_SW>(stg + 2 * out1_off, trow, tcol, v1);
+  } else if constexpr (EPI == EPI_GATED_BWD2) {
+    // staged a, b tiles in; staged dA, dB tiles out (rows past the end are clipped by TMA)
+    static_assert(STG_SW > 0, "EPI_GATED_BWD2 is the staged form");
+    float a[16], b[16], da[16], db[16];
+    unstage_chunk16<OutT, STG_SW>(in_stg, trow, tcol, a);
+    unstage_chunk16<OutT, STG_SW>(in_stg + in1_off, trow, tcol, b);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if constexpr (sizeof(OutT) == 2)
+        gated_bwd_fast(v0[i], a[i], b[i], da[i], db[i]);
+      else
+        gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
+    }
+    stage_chunk16<OutT, STG_SW>(stg, trow, tcol, da);
+    stage_chunk16<OutT, STG_SW>(stg + out1_off, trow, tcol, db);
   } else {
     if (!live) return;
     if (p.in1) {
@@ -416,7 +469,12 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
       load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in0) + off, a, valid, vec_ok);
       load_chunk16<OutT>(reinterpret_cast<const OutT*>(p.in1) + off, b, valid, vec_ok);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
+      for (int i = 0; i < 16; ++i) {
+        if constexpr (sizeof(OutT) == 2)
+          gated_bwd_fast(v0[i], a[i], b[i], da[i], db[i]);
+        else
+          gated_bwd(v0[i], a[i], b[i], da[i], db[i]);
+      }
       store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, da, valid, vec_ok);
       store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out1) + off, db, valid, vec_ok);
     } else {
@@ -458,7 +516,8 @@ template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW, int NBUF = 2>
 __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t tacc, int row0,
                                                  int col0, int flags, uint8_t* stg, int half,
                                                  uint32_t q, uint32_t lane, uint32_t etid,
-                                                 bool vec_ok, const uint8_t* in_stg = nullptr) {
+                                                 bool vec_ok, const uint8_t* in_stg = nullptr,
+                                                 int out1_off = 0, int in1_off = 0) {
   if constexpr (OUT_SW > 0) {
     if (etid == 0) bulk_wait_group_read<NBUF - 1>();
     named_bar_sync(1, kEpiWarpsT * 32);
@@ -467,7 +526,7 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
   const int row = row0 + trow;
   const bool row_ok = row < p.m;
   constexpr int NCH = B / 16;
-  constexpr bool kTwoAcc = EPI == EPI_GATED_FWD;
+  constexpr bool kTwoAcc = EPI == EPI_GATED_FWD || EPI == EPI_GATED_FWD_SAVE;
   const bool acc0_init = SUMACC ? ((flags & 3) != 0) : ((flags & 1) != 0);
   // this warp's 16-column chunks are c = half, half + 2, ...; the TMEM loads of two chunks
   // (both accumulators when gated) are issued before one wait
@@ -497,21 +556,26 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
         v1[i] = kTwoAcc ? __uint_as_float(r1[k][i]) : 0.0f;
       }
       epilogue_chunk<EPI, OutT, OUT_SW>(p, v0, v1, flags, row_ok, col, valid, off, vec_ok, stg,
-                                        trow, c * 16, in_stg);
+                                        trow, c * 16, in_stg, out1_off, in1_off);
     }
   }
 }
-template <int OUT_SW, int OUT_NATOM, int OUT_ELT>
-__device__ __forceinline__ void epi_tile_store(const CUtensorMap* mapO, uint8_t* stg, int row0,
-                                               int col0, uint32_t etid, uint64_t pol_out) {
+template <int OUT_SW, int OUT_NATOM, int OUT_ELT, int NOUT = 1>
+__device__ __forceinline__ void epi_tile_store(const CUtensorMap* mapO, const CUtensorMap* mapO1,
+                                               const CUtensorMap* mapO2, uint8_t* stg,
+                                               int out1_off, int row0, int col0, uint32_t etid,
+                                               uint64_t pol_out) {
   if constexpr (OUT_SW > 0) {
     fence_proxy_async_smem();
     named_bar_sync(1, kEpiWarpsT * 32);
     if (etid == 0) {
 #pragma unroll
-      for (int a = 0; a < OUT_NATOM; ++a)
-        tma_store_2d_hint(mapO, stg + a * (128 * OUT_SW), col0 + a * (OUT_SW / OUT_ELT), row0,
-                          pol_out);
+      for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+        for (int a = 0; a < OUT_NATOM; ++a)
+          tma_store_2d_hint(o == 0 ? mapO : o == 1 ? mapO1 : mapO2,
+                            stg + o * out1_off + a * (128 * OUT_SW),
+                            col0 + a * (OUT_SW / OUT_ELT), row0, pol_out);
       bulk_commit_group();
     }
   }
@@ -570,20 +634,25 @@ constexpr int kTcThreads = 384;
 constexpr int kEpiWarps = kEpiWarpsT;
 
 template <int EPI, int OUT_ELT>
-constexpr int in_staged() { return (EPI == EPI_GATED_BWD && OUT_ELT > 0) ? 1 : 0; }
+constexpr int in_staged() {
+  return OUT_ELT == 0 ? 0 : EPI == EPI_GATED_BWD ? 1 : EPI == EPI_GATED_BWD2 ? 2 : 0;
+}
 
 template <int B, int ELT, int NPASS, int NMAT, bool SUMACC, bool B_KMAJOR, int EPI, typename OutT,
           int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
 __global__ void __launch_bounds__(kTcThreads, 1)
 spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__ CUtensorMap mapI,
+               const __grid_constant__ CUtensorMap mapO1, const __grid_constant__ CUtensorMap mapI1,
+               const __grid_constant__ CUtensorMap mapO2,
                const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA0lo,
                const __grid_constant__ CUtensorMap mapA1, const __grid_constant__ CUtensorMap mapA1lo,
                const __grid_constant__ CUtensorMap mapW0, const __grid_constant__ CUtensorMap mapW0lo,
                const __grid_constant__ CUtensorMap mapW1, const __grid_constant__ CUtensorMap mapW1lo,
                const SpmmParams p) {
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
-  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST, SPLIT>;
-  static_assert(!SPLIT || (NMAT == 2 && !SUMACC && NPASS == 1 &&
+  using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST, SPLIT,
+                  staged_outputs<EPI>()>;
+  static_assert(!SPLIT || (NMAT == 2 && NPASS == 1 &&
                            (SPLIT == 2) == use_waiter<NMAT, TM, SPLIT>()),
                 "split stages: gate+up products only");
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
@@ -603,7 +672,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   // producer before its expect_tx arrive (release), read after the full wait (acquire)
   uint32_t* stage_meta = tmem_slot + 4;
   uint64_t* in_full = reinterpret_cast<uint64_t*>(stage_meta + 8);  // [2] staged in0 landed
-  uint8_t* in_staging = staging + C::OUT_BUFS * C::OUT_TILE;        // [2][TM][OUT_TILE] (IN_ST)
+  uint8_t* in_staging = staging + C::OUT_BUFS * C::NOUT * C::OUT_TILE;  // [2][IN_ST][TM][OUT_TILE]
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -613,6 +682,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 
   if (warp == 0 && lane == 0) {
     if (OUT_ELT) tma_prefetch(&mapO);
+    if (C::NOUT > 1) tma_prefetch(&mapO1);
+    if (C::NOUT > 2) tma_prefetch(&mapO2);
+    if (IN_ST == 2) tma_prefetch(&mapI1);
     tma_prefetch(&mapA0);
     tma_prefetch(&mapW0);
     if (NMAT > 1) tma_prefetch(&mapW1);
@@ -704,7 +776,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
                 mbar_expect_tx(&full[stage], C::TROWS * C::ROWB + B * C::ROWB);
 #pragma unroll
                 for (int at = 0; at < C::NATOM; ++at)
-                  tma_load_2d(sbase + at * C::TROWS * C::SW, &mapA0, &full[stage],
+                  tma_load_2d(sbase + at * C::TROWS * C::SW,
+                              (SUMACC && pass == 1) ? &mapA1 : &mapA0, &full[stage],
                               st.x * B + at * C::SWE, t * C::TROWS);
                 const CUtensorMap* mw = pass == 0 ? &mapW0 : &mapW1;
 #pragma unroll
@@ -865,8 +938,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         tc_fence_after();
         const uint32_t d_base = tmem_base + as * C::ACC_STRIDE;
         for (int i = 0; i < n; ++i) {
-          const uint32_t sel = i >= n0 ? 1u : 0u;
-          const uint32_t init = (i != 0 && i != n0) ? 1u : 0u;
+          // SUMACC (dX = dA Wg^T + dB Wu^T): both passes accumulate into one accumulator
+          const uint32_t sel = (!SUMACC && i >= n0) ? 1u : 0u;
+          const uint32_t init = SUMACC ? (i != 0 ? 1u : 0u) : ((i != 0 && i != n0) ? 1u : 0u);
           named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
           tc_fence_after();
           const long long ti0 = dbg_on ? clock64() : 0;
@@ -1053,14 +1127,17 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         // whose reads all precede its final barrier
         auto load_in = [&](int itm, uint32_t buf) {
           const int tt = tile_of(itm), jj = itm % p.n_lines;
-          mbar_expect_tx(&in_full[buf], TM * C::BM * C::OUT_ROWB);
+          mbar_expect_tx(&in_full[buf], IN_ST * TM * C::BM * C::OUT_ROWB);
 #pragma unroll
-          for (int h = 0; h < TM; ++h)
+          for (int i = 0; i < IN_ST; ++i)
 #pragma unroll
-            for (int a = 0; a < C::OUT_NATOM; ++a)
-              tma_load_2d(in_staging + (buf * TM + h) * C::OUT_TILE + a * (C::BM * C::OUT_SW),
-                          &mapI, &in_full[buf], jj * B + a * (C::OUT_SW / OUT_ELT),
-                          tt * C::TROWS + h * C::BM);
+            for (int h = 0; h < TM; ++h)
+#pragma unroll
+              for (int a = 0; a < C::OUT_NATOM; ++a)
+                tma_load_2d(in_staging + ((buf * IN_ST + i) * TM + h) * C::OUT_TILE +
+                                a * (C::BM * C::OUT_SW),
+                            i == 0 ? &mapI : &mapI1, &in_full[buf],
+                            jj * B + a * (C::OUT_SW / OUT_ELT), tt * C::TROWS + h * C::BM);
         };
         if (etid == 0) {
           if (it == 0) load_in(item, 0);
@@ -1079,19 +1156,22 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       }
 #pragma unroll
       for (int h = 0; h < TM; ++h) {
-        uint8_t* stg = staging + ((it * TM + h) % C::OUT_BUFS) * C::OUT_TILE;
+        uint8_t* stg = staging + ((it * TM + h) % C::OUT_BUFS) * C::NOUT * C::OUT_TILE;
         const uint32_t tacc =
             tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
         const int row0 = t * C::TROWS + h * C::BM;
         epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS>(
             p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
-            IN_ST ? in_staging + ((it & 1) * TM + h) * C::OUT_TILE : nullptr);
+            IN_ST ? in_staging + ((it & 1) * IN_ST * TM + h) * C::OUT_TILE : nullptr,
+            C::OUT_TILE, TM * C::OUT_TILE);
         if (h == TM - 1) {  // every TMEM read of this accumulator stage is done
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tmem_empty[as]);
         }
-        epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT>(&mapO, stg, row0, j * B, etid, pol_out);
+        epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT, C::NOUT>(&mapO, &mapO1, &mapO2, stg,
+                                                                  C::OUT_TILE, row0, j * B, etid,
+                                                                  pol_out);
       }
     }
     if constexpr (OUT_ELT > 0) {
