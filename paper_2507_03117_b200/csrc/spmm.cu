@@ -212,7 +212,9 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   // instead of 18.0 us); the gate+up kernel got slower (238.7 -> 243.0 us) although its CTAs
   // also end together: its per-CTA work rose by the same amount, i.e. it is bound by the
   // chip-wide L2 -> SM feed, which an even split cannot raise, so it keeps round robin.
-  if (NMAT == 1)
+  // Decode-size products (fewer than two items per CTA) balance the gate+up product too:
+  // cfg3 shape at 95 %, 128 tokens, graph replay 18.6 -> 16.7 us (profiles/r02/decode_ab.txt).
+  if (NMAT == 1 || items < 2 * static_cast<int64_t>(num_sms()))
     p.sched = balanced_schedule(c.step_ptr, c.flags, p.n_lines, p.n_tok_tiles, grid, SPLIT == 2,
                                 st, &p.sched_rows);
   dbg_begin(st);

@@ -187,3 +187,24 @@ class TestActivations:
         for f in ("relu", "gelu", "silu"):
             got = bs.apply_nonlinearity(x, f)
             np.testing.assert_allclose(got, oracle.activation(x, f), rtol=4e-6, atol=2e-6)
+
+
+@pytest.mark.parametrize("m,rows,cols,sp", [(128, 3584, 1024, 0.9), (100, 4096, 512, 0.8),
+                                            (37, 2048, 256, 0.5)])
+def test_decode_size_products(m, rows, cols, sp):
+    """Decode-size products (one token tile, few output lines, long lines): oracle parity in
+    fp32 and bf16, and run-to-run bitwise determinism."""
+    rng = np.random.default_rng(m + rows)
+    w = oracle.random_bcsc(rows, cols, 64, sp, rng)
+    w = w._replace(values=(w.values / np.sqrt(rows)).astype(np.float32))
+    x = rng.standard_normal((m, rows)).astype(np.float32)
+    for dt, tol in ((torch.float32, 1e-4), (torch.bfloat16, 2e-2)):
+        cache = bs.from_host(w, dt)
+        xd = torch.from_numpy(x).cuda().to(dt)
+        y = bs.bspmm(xd, cache)
+        y2 = bs.bspmm(xd, cache)
+        assert torch.equal(y, y2)
+        xr = xd.float().cpu().numpy()
+        wr = w._replace(values=torch.from_numpy(w.values).to(dt).float().numpy())
+        ref = oracle.bspmm(xr, wr)
+        assert oracle.max_norm_rel(y.float().cpu().numpy(), ref) <= tol
