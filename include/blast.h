@@ -74,6 +74,28 @@ typedef struct blast_mlp_plan {
   const int32_t* dx_step_ptr; const int32_t* dx_steps; const int32_t* dx_flags;
 } blast_mlp_plan_t;
 
+/* Tensor-parallel group for the fused down-projection + all-reduce (SURVEY.md section 8e/8f-4,
+ * blast_tp_mlp_forward). Every rank holds the same table; entry r of each array is rank r's
+ * buffer as mapped into THIS process (torch symmetric memory / CUDA IPC peer pointers over
+ * NVLink, or plain local buffers when the "ranks" share one device). Buffers:
+ *   recv[r]  float [2][n][tiles][owned][128][b]  partial output tiles sent to owner r
+ *            (tiles = ceil(m / 128); owned = ceil(lines / n), line j owned by rank j % n)
+ *   flags[r] uint32 [tiles][owned]  arrival counters, zero-initialised, monotonic
+ *   y[r]     [m][d] output of rank r (every rank receives the full all-reduced Y)
+ *   done[r]  uint32 tiles written into y[r], zero-initialised, monotonic
+ * `epoch` counts the group's fused launches (0, 1, 2, ...; identical on every rank); recv is
+ * double-buffered by its parity. n <= 8. */
+#define BLAST_TP_MAX 8
+typedef struct blast_tp {
+  int32_t n, rank;
+  uint32_t epoch;
+  int32_t reserved;
+  float* recv[BLAST_TP_MAX];
+  uint32_t* flags[BLAST_TP_MAX];
+  void* y[BLAST_TP_MAX];
+  uint32_t* done[BLAST_TP_MAX];
+} blast_tp_t;
+
 const char* blast_last_error(void);
 int blast_version(void);
 int blast_num_sms(void);
@@ -135,6 +157,23 @@ int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
                       const blast_bcsc_t* up, const blast_bcsc_t* down,
                       const blast_mlp_plan_t* plan, void* y, void* gate_pre, void* up_out,
                       void* gated, void* stream);
+/* Row-parallel down projection of one TP rank fused with the all-reduce of the partial Y
+ * (reference mlp.py:114 on a sharded hidden dimension):
+ * y[r] (every rank r of tp) += nothing until all ranks of the group have run this call with the
+ * same tp->epoch; then y[r] = sum over ranks of G_rank Wd_rank, rounded once. Partial tiles go
+ * to their owner rank over peer memory as they are produced (blast_tp_t). Asynchronous: the
+ * caller waits with blast_tp_wait(tp->done[rank], (epoch + 1) * tiles * lines) before using y,
+ * tiles = ceil(m / 128), lines = ceil(d / b). Tensor-core engine only (b in 16/32/64/128). */
+int blast_tp_down_allreduce(const void* g, int64_t m, const blast_bcsc_t* down_shard,
+                            const blast_tp_t* tp, void* stream);
+/* One TP rank's MLP forward (column-parallel gate/up shards, row-parallel down shard) with the
+ * fused all-reduce (the K9 entry of SURVEY.md section 8b). */
+int blast_tp_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate_shard,
+                         const blast_bcsc_t* up_shard, const blast_bcsc_t* down_shard,
+                         const blast_mlp_plan_t* plan, const blast_tp_t* tp, void* stream);
+/* Stream-ordered wait until *done (system scope) reaches target (wrapping compare); traps
+ * after 20 s so a missing peer is a reported error, not a hung device. */
+int blast_tp_wait(const uint32_t* done, uint32_t target, void* stream);
 /* out[c] = sum_r x[r, c] (fp32) of a row-major [m, n] bf16 / f32 matrix: bias gradients of
  * layers with bias (GPT2MLP integration). Deterministic (fixed row splits, fixed order). */
 int blast_column_sums(const void* x, int dtype, int64_t m, int64_t n, float* out, void* stream);

@@ -42,6 +42,17 @@ class MlpPlanDesc(C.Structure):
     ]
 
 
+TP_MAX = 8
+
+
+class TpDesc(C.Structure):
+    """include/blast.h blast_tp_t"""
+    _fields_ = [
+        ("n", C.c_int32), ("rank", C.c_int32), ("epoch", C.c_uint32), ("reserved", C.c_int32),
+        ("recv", vp * TP_MAX), ("flags", vp * TP_MAX), ("y", vp * TP_MAX), ("done", vp * TP_MAX),
+    ]
+
+
 # name -> (restype, argtypes)
 _PROTOS = {
     "blast_last_error": (C.c_char_p, []),
@@ -61,6 +72,11 @@ _PROTOS = {
                                     C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, vp, vp, vp,
                                     vp]),
     "blast_column_sums": (C.c_int, [vp, C.c_int, i64, i64, vp, vp]),
+    "blast_tp_down_allreduce": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(TpDesc), vp]),
+    "blast_tp_mlp_forward": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
+                                       C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc),
+                                       C.POINTER(TpDesc), vp]),
+    "blast_tp_wait": (C.c_int, [vp, C.c_uint32, vp]),
     "blast_mlp_forward_host": (C.c_int, [vp, i64, C.POINTER(BcscDesc), C.POINTER(BcscDesc),
                                          C.POINTER(BcscDesc), C.POINTER(MlpPlanDesc), vp, i64,
                                          vp]),

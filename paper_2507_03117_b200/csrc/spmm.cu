@@ -40,6 +40,7 @@ struct EngineCall {
   int64_t ld_out = 0;
   const float* bias = nullptr;
   bool reverse_tiles = false;  // last token tile first (see SpmmParams::reverse_tiles)
+  const blast_tp_t* tp = nullptr;  // fused TP all-reduce epilogue (single-matrix products)
 };
 
 // BLAST_DEBUG_COUNTERS=1: per-role wait cycles of every tensor-core launch to stderr
@@ -123,6 +124,7 @@ static SpmmParams make_params(const EngineCall& c) {
   p.ld_out = c.ld_out;
   p.bias = c.bias;
   p.reverse_tiles = c.reverse_tiles ? 1 : 0;
+  if (c.tp) p.tp = *c.tp;
   return p;
 }
 
@@ -449,6 +451,10 @@ int run_engine(const EngineCall& c_in, cudaStream_t st) {
     set_error("execution plan missing (build it with blast_build_plan)");
     return BLAST_EINVAL;
   }
+  if (c_in.tp && (c_in.nmat != 1 || c_in.epi != EPI_STORE || c_in.transposed || c_in.accumulate)) {
+    set_error("fused TP all-reduce: single-matrix forward products only");
+    return BLAST_EINVAL;
+  }
   if (tc_shape_ok(c_in)) {
     if (c_in.dtype == BLAST_BF16) {
       int r = dispatch_tc<__nv_bfloat16, 2, 1>(c_in, nullptr, nullptr, st);
@@ -480,6 +486,10 @@ int run_engine(const EngineCall& c_in, cudaStream_t st) {
         if (r >= 0) return r;
       }
     }
+  }
+  if (c_in.tp) {
+    set_error("fused TP all-reduce needs the tensor-core engine (b in {16, 32, 64, 128})");
+    return BLAST_EUNSUPPORTED;
   }
   return run_simt(c_in, st);
 }
@@ -639,6 +649,89 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
   // gate+up wrote G tile by tile in order: read it back last tile first, while the most
   // recently written rows are still in L2
   return bspmm_impl(gated, m, down, nullptr, BLAST_ACT_NONE, y, nullptr, true, stream);
+}
+
+namespace blast {
+static bool check_tp(const blast_tp_t* tp) {
+  if (!tp || tp->n < 1 || tp->n > BLAST_TP_MAX || tp->rank < 0 || tp->rank >= tp->n) {
+    set_error("invalid TP group descriptor");
+    return false;
+  }
+  for (int r = 0; r < tp->n; ++r)
+    if (!tp->recv[r] || !tp->flags[r] || !tp->y[r] || !tp->done[r]) {
+      set_error("TP group descriptor: missing buffer of rank %d", r);
+      return false;
+    }
+  return true;
+}
+
+// one thread polls the counter (system scope) until it reaches `target`; a bounded wait
+// turns a missing peer into a reported launch error instead of a hung device
+__global__ void tp_wait_kernel(const uint32_t* done, uint32_t target) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if (static_cast<int32_t>(v - target) >= 0) break;
+    if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) {
+      printf("blast: tp_wait timed out (done %u < %u)\n", v, target);
+      __trap();
+    }
+    __nanosleep(200);
+  }
+}
+}  // namespace blast
+
+extern "C" int blast_tp_down_allreduce(const void* g, int64_t m, const blast_bcsc_t* down_shard,
+                                       const blast_tp_t* tp, void* stream) {
+  if (!check_w(down_shard) || !check_tp(tp)) return BLAST_EINVAL;
+  if (m <= 0) return BLAST_OK;
+  EngineCall c;
+  c.dtype = down_shard->dtype;
+  c.block = down_shard->block;
+  c.m = m;
+  c.a_cols = down_shard->rows;
+  c.a0 = g;
+  c.w0 = down_shard->values;
+  c.w0_hi = down_shard->tf32_fwd_hi;
+  c.w0_lo = down_shard->tf32_fwd_lo;
+  c.nnzb0 = down_shard->nnzb;
+  c.n_lines = cdiv(down_shard->cols, down_shard->block);
+  c.n_valid = down_shard->cols;
+  c.step_ptr = down_shard->fwd_step_ptr;
+  c.steps = down_shard->fwd_steps;
+  c.flags = down_shard->fwd_flags;
+  c.out0 = tp->y[tp->rank];
+  c.ld_out = down_shard->cols;
+  c.tp = tp;
+  return run_engine(c, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int blast_tp_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate_shard,
+                                    const blast_bcsc_t* up_shard, const blast_bcsc_t* down_shard,
+                                    const blast_mlp_plan_t* plan, const blast_tp_t* tp,
+                                    void* stream) {
+  if (!check_w(gate_shard) || !check_w(up_shard) || !check_w(down_shard) || !check_tp(tp))
+    return BLAST_EINVAL;
+  if (gate_shard->cols != down_shard->rows || up_shard->cols != gate_shard->cols ||
+      down_shard->cols != gate_shard->rows) {
+    set_error("TP shard shape mismatch");
+    return BLAST_EMISMATCH;
+  }
+  if (m <= 0) return BLAST_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Scratch sg;
+  if (!sg.alloc(bytes_of(gate_shard->dtype) * m * gate_shard->cols, st))
+    return cuda_status(cudaGetLastError(), "scratch G");
+  int r = blast_mlp_gate_up(x, m, gate_shard, up_shard, plan, sg.ptr, nullptr, nullptr, stream);
+  if (r) return r;
+  return blast_tp_down_allreduce(sg.ptr, m, down_shard, tp, stream);
+}
+
+extern "C" int blast_tp_wait(const uint32_t* done, uint32_t target, void* stream) {
+  if (!done) return BLAST_EINVAL;
+  tp_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(done, target);
+  return check_launch("tp_wait");
 }
 
 extern "C" int blast_mlp_gate_up(const void* x, int64_t m, const blast_bcsc_t* gate,

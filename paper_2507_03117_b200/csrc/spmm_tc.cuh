@@ -24,6 +24,7 @@
 
 #include "activations.cuh"
 #include "ptx.cuh"
+#include "../../include/blast.h"
 
 namespace blast {
 
@@ -72,6 +73,7 @@ struct SpmmParams {
                             // the k-th item of CTA `cta`, -1 past its end (csrc/schedule.cu);
                             // nullptr: static round robin (item = cta + k * gridDim.x)
   int32_t sched_rows;       // rows of `sched`
+  blast_tp_t tp;            // tp.n > 0: fused down-projection + all-reduce epilogue (epi_tp_tile)
 };
 
 // BLAST_SKIP_EPILOGUE's "skip operand loads" switch (diagnosis) is compiled in only on request
@@ -579,6 +581,110 @@ __device__ __forceinline__ void epi_tile_store(const CUtensorMap* mapO, const CU
       bulk_commit_group();
     }
   }
+}
+
+// ---------------------------------------------------------------- fused TP all-reduce
+__device__ __forceinline__ uint32_t atomic_add_sys(uint32_t* addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.sys.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ float4 ld_volatile_f4(const float* p) {
+  return __ldcv(reinterpret_cast<const float4*>(p));
+}
+
+// Fused tensor-parallel epilogue of one 128-row output tile of the row-parallel down
+// projection (partial Y summed over the TP ranks):
+//   1. the tile's fp32 partial goes straight into the recv buffer of the line's owner rank
+//      (peer stores over NVLink; slot [epoch parity][this rank][tile][line]);
+//   2. a system-scope arrival counter on the owner counts the ranks' partials;
+//   3. the rank whose partial completes the tile (whichever arrives last) sums the n partials
+//      in rank order (deterministic) and writes the rounded sum into every rank's y, then
+//      bumps every rank's `done` counter.
+// No CTA ever waits on another GPU inside the kernel, so ranks overlap the exchange with
+// their own remaining tiles; consumers wait for done[rank] (blast_tp_wait) before reading y.
+// The TMEM reads come first; `release` frees the accumulator stage right after them.
+template <int B, typename OutT>
+__device__ __noinline__ void epi_tp_tile(const SpmmParams& p, uint32_t tacc, int t128, int j,
+                                         int flags, int half, uint32_t q, uint32_t lane,
+                                         uint32_t etid, bool release, uint64_t* acc_empty,
+                                         volatile int* last_flag) {
+  constexpr int NCH = B / 16;
+  const blast_tp_t& tp = p.tp;
+  const int n = tp.n;
+  const int trow = static_cast<int>(q * 32 + lane);
+  const int tiles = (p.m + 127) / 128;
+  const int owned = (p.n_lines + n - 1) / n;
+  const int o = j % n, lo = j / n;
+  const int par = static_cast<int>(tp.epoch & 1u);
+  float v[NCH / 2 + 1][16];
+#pragma unroll
+  for (int k = 0; k < (NCH + 1) / 2; ++k) {
+    const int c = half + 2 * k;
+    if (c < NCH) tmem_ld16(tacc + c * 16, v[k]);
+  }
+  if (release) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_empty);
+  }
+  const int64_t tile_elems = 128 * B;
+  const int64_t slot = (((static_cast<int64_t>(par) * n + tp.rank) * tiles + t128) * owned + lo);
+  float* dst = tp.recv[o] + slot * tile_elems + static_cast<int64_t>(trow) * B;
+#pragma unroll
+  for (int k = 0; k < (NCH + 1) / 2; ++k) {
+    const int c = half + 2 * k;
+    if (c >= NCH) break;
+    if (!(flags & 1)) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[k][i] = 0.0f;
+    }
+    float4* d4 = reinterpret_cast<float4*>(dst + c * 16);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      d4[i] = make_float4(v[k][4 * i], v[k][4 * i + 1], v[k][4 * i + 2], v[k][4 * i + 3]);
+  }
+  __threadfence_system();
+  named_bar_sync(1, kEpiWarpsT * 32);
+  if (etid == 0) {
+    const uint32_t old = atomic_add_sys(tp.flags[o] + static_cast<int64_t>(t128) * owned + lo, 1u);
+    *last_flag = old == static_cast<uint32_t>(n) * tp.epoch + static_cast<uint32_t>(n - 1);
+  }
+  named_bar_sync(1, kEpiWarpsT * 32);
+  if (!*last_flag) return;
+  __threadfence_system();
+  const int row = t128 * 128 + trow;
+  if (row < p.m) {
+    const float* src0 = tp.recv[o] + ((static_cast<int64_t>(par) * n * tiles + t128) * owned + lo) *
+                                         tile_elems + static_cast<int64_t>(trow) * B;
+    const int64_t rank_stride = static_cast<int64_t>(tiles) * owned * tile_elems;
+#pragma unroll 1
+    for (int c = half; c < NCH; c += 2) {
+      float s[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s[i] = 0.0f;
+      for (int r = 0; r < n; ++r) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 f = ld_volatile_f4(src0 + r * rank_stride + c * 16 + 4 * i);
+          s[4 * i] = __fadd_rn(s[4 * i], f.x);
+          s[4 * i + 1] = __fadd_rn(s[4 * i + 1], f.y);
+          s[4 * i + 2] = __fadd_rn(s[4 * i + 2], f.z);
+          s[4 * i + 3] = __fadd_rn(s[4 * i + 3], f.w);
+        }
+      }
+      const int col = j * B + c * 16;
+      const int valid = p.n_valid - col;
+      const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
+      for (int r = 0; r < n; ++r)
+        store_chunk16<OutT>(reinterpret_cast<OutT*>(tp.y[r]) + off, s, valid,
+                            (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0);
+    }
+  }
+  __threadfence_system();
+  named_bar_sync(1, kEpiWarpsT * 32);
+  if (etid == 0)
+    for (int r = 0; r < n; ++r) atomic_add_sys(tp.done[r], 1u);
 }
 
 // per-stage MMA recipe bits (producer -> MMA warp through shared memory)
@@ -1153,6 +1259,17 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[as]);
         continue;
+      }
+      if constexpr (NMAT == 1 && EPI == EPI_STORE) {
+        if (p.tp.n > 0) {  // fused TP all-reduce of the row-parallel down projection
+#pragma unroll 1
+          for (int h = 0; h < TM; ++h)
+            epi_tp_tile<B, OutT>(p, tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE +
+                                        h * C::HALF_ACC,
+                                 t * TM + h, j, flags, half, q, lane, etid, h == TM - 1,
+                                 &tmem_empty[as], reinterpret_cast<volatile int*>(in_full + 2));
+          continue;
+        }
       }
 #pragma unroll
       for (int h = 0; h < TM; ++h) {

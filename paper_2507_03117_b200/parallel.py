@@ -15,6 +15,14 @@ layouts the north star names, one process per GPU over ``torch.distributed``
   all-gathered, and every rank runs the same global top-k (ties by global
   (column, row)) and keeps its slice. A per-shard top-k would change the
   semantics of pruner.py:101-125.
+* **Fused TP all-reduce.** ``FusedTPGroup`` runs the row-parallel
+  down projection with the reduction inside its epilogue (``blast_tp_mlp_forward``): each
+  finished fp32 partial tile is stored straight into its owner rank's receive buffer over
+  peer memory, a system-scope counter on the owner counts the ranks' tiles, and the rank whose
+  tile completes the set sums the partials in rank order and writes the result into every
+  rank's output. The exchange overlaps the remaining tiles; no NCCL call sits on the path.
+  Buffers come from torch symmetric memory (one process per GPU) or, for single-device tests,
+  from plain allocations shared by "virtual" ranks.
 * **Data parallel (pretraining, cfg2).** Replicated weights, token-sharded
   batches, weight gradients averaged with one all-reduce per step. Masks stay
   identical on all ranks because they derive from identical weights and the
@@ -172,3 +180,114 @@ def tp_roofline_ns_per_token(d: int, h: int, b: int, nnzb_total: int, world: int
     t_c = flop / (tflops * 1e12) * 1e9
     t_n = comm_bytes_per_token(d, world) / (link_gbs * 1e9) * 1e9
     return {"compute_ns": t_c, "comm_ns": t_n, "bound": "comm" if t_n > t_c else "compute"}
+
+
+# ---------------------------------------------------------------- fused TP all-reduce
+class FusedTPGroup:
+    """Buffers and launch state of the fused down-projection + all-reduce (blast_tp_t in
+    include/blast.h) for token count ``m``, output width ``d`` and block size ``b``.
+
+    ``FusedTPGroup.symmetric(group, ...)`` allocates one rank's buffers with torch symmetric
+    memory and exchanges the peer pointers (one process per GPU, NVLink peer access).
+    ``FusedTPGroup.local(n, ...)`` puts all n ranks' buffers on the current device: n "virtual"
+    ranks then run their shards one after another in one process (the protocol is identical,
+    used by the single-GPU tests)."""
+
+    def __init__(self, n: int, m: int, d: int, b: int, dtype: torch.dtype, ptrs, keep):
+        self.n, self.m, self.d, self.b, self.dtype = n, m, d, b, dtype
+        self.tiles = -(-m // 128)
+        self.lines = -(-d // b)
+        self.owned = -(-self.lines // n)
+        self.ptrs = ptrs          # {"recv": [..n], "flags": [..], "y": [..], "done": [..]}
+        self._keep = keep         # tensors / handles that own the memory
+        self.epoch = 0
+
+    @staticmethod
+    def _sizes(n, m, d, b, dtype):
+        tiles, lines = -(-m // 128), -(-d // b)
+        owned = -(-lines // n)
+        recv = 2 * n * tiles * owned * 128 * b * 4
+        flags = tiles * owned * 4
+        y = m * d * torch.tensor([], dtype=dtype).element_size()
+        return recv, flags, y, 64
+
+    @classmethod
+    def local(cls, n: int, m: int, d: int, b: int, dtype=torch.bfloat16):
+        if not 1 <= n <= 8:
+            raise ValueError("TP group size must be 1..8")
+        recv_b, flags_b, y_b, done_b = cls._sizes(n, m, d, b, dtype)
+        keep, ptrs = [], {"recv": [], "flags": [], "y": [], "done": []}
+        for _ in range(n):
+            recv = torch.empty(recv_b // 4, dtype=torch.float32, device="cuda")
+            flags = torch.zeros(flags_b // 4, dtype=torch.int32, device="cuda")
+            y = torch.empty(m, d, dtype=dtype, device="cuda")
+            done = torch.zeros(done_b // 4, dtype=torch.int32, device="cuda")
+            keep += [recv, flags, y, done]
+            for k, t in zip(("recv", "flags", "y", "done"), (recv, flags, y, done)):
+                ptrs[k].append(t.data_ptr())
+        g = cls(n, m, d, b, dtype, ptrs, keep)
+        g._y = keep[2::4]
+        return g
+
+    @classmethod
+    def symmetric(cls, group, m: int, d: int, b: int, dtype=torch.bfloat16):
+        """Collective over ``group`` (one rank per GPU): symmetric-memory buffers and the peer
+        pointer table of every rank."""
+        import torch.distributed._symmetric_memory as symm_mem
+        n = dist.get_world_size(group)
+        recv_b, flags_b, y_b, done_b = cls._sizes(n, m, d, b, dtype)
+        keep, ptrs = [], {}
+        dev = torch.device("cuda", torch.cuda.current_device())
+        for key, nbytes in (("recv", recv_b), ("flags", flags_b), ("y", y_b), ("done", done_b)):
+            t = symm_mem.empty(nbytes, dtype=torch.uint8, device=dev)
+            if key in ("flags", "done"):
+                t.zero_()
+            hdl = symm_mem.rendezvous(t, group)
+            keep += [t, hdl]
+            ptrs[key] = list(hdl.buffer_ptrs)
+        torch.cuda.synchronize()
+        dist.barrier(group)
+        g = cls(n, m, d, b, dtype, ptrs, keep)
+        rank = dist.get_rank(group)
+        g._y = [None] * n
+        g._y[rank] = keep[2 * 2].view(dtype).view(m, d)
+        return g
+
+    def desc(self, rank: int):
+        from . import _lib as L
+        dsc = L.TpDesc()
+        dsc.n, dsc.rank, dsc.epoch = self.n, rank, self.epoch & 0xFFFFFFFF
+        for r in range(self.n):
+            dsc.recv[r] = self.ptrs["recv"][r]
+            dsc.flags[r] = self.ptrs["flags"][r]
+            dsc.y[r] = self.ptrs["y"][r]
+            dsc.done[r] = self.ptrs["done"][r]
+        return dsc
+
+    def y(self, rank: int) -> torch.Tensor:
+        return self._y[rank]
+
+    def forward(self, x: torch.Tensor, net, rank: int) -> None:
+        """Launch rank ``rank``'s fused forward for the current epoch (asynchronous)."""
+        import ctypes as C
+        from . import _lib as L
+        if x.shape != (self.m, net.embed_dim) or net.embed_dim != self.d:
+            raise ValueError(f"x shape {tuple(x.shape)} does not match the group ({self.m}, {self.d})")
+        dg, du, dd = (mat.cache.desc() for mat in net.matrices())
+        plan = net.plan()
+        dsc = self.desc(rank)
+        L.check(L.load().blast_tp_mlp_forward(x.data_ptr(), self.m, C.byref(dg), C.byref(du),
+                                              C.byref(dd), C.byref(plan), C.byref(dsc),
+                                              L.stream()), "tp_mlp_forward")
+
+    def wait(self, rank: int) -> torch.Tensor:
+        """Stream-ordered wait until rank's output holds the current epoch's sum; returns it
+        and advances the epoch."""
+        from . import _lib as L
+        target = ((self.epoch + 1) * self.tiles * self.lines) & 0xFFFFFFFF
+        L.check(L.load().blast_tp_wait(self.ptrs["done"][rank], target, L.stream()), "tp_wait")
+        return self.y(rank)
+
+    def step(self) -> None:
+        self.epoch += 1
+

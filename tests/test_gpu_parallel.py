@@ -73,3 +73,51 @@ def test_tp_two_ranks_on_one_gpu():
     np.testing.assert_array_equal(np.concatenate([res[0][3], res[1][3]], 1), ref.kept)
     np.testing.assert_array_equal(np.concatenate([res[0][4], res[1][4]], 1), ref.regrown)
     assert res[0][5] == rep[:2]
+
+
+def _shard_nets(wg, wu, wd, b, world, dtype):
+    import paper_2507_03117_b200 as bs
+    from paper_2507_03117_b200 import parallel
+    return [bs.SparseMlp(*(bs.MaskedMatrix.dense_init(m, b, dtype) for m in (
+        parallel.column_shard(wg, b, r, world), parallel.column_shard(wu, b, r, world),
+        parallel.row_shard(wd, b, r, world)))) for r in range(world)]
+
+
+@pytest.mark.parametrize("world,m,dtype", [(2, 300, torch.bfloat16), (4, 1024, torch.bfloat16),
+                                           (2, 256, torch.float32), (8, 128, torch.bfloat16)])
+def test_fused_tp_allreduce_virtual_ranks(world, m, dtype):
+    """The fused down-projection + all-reduce (blast_tp_mlp_forward)
+    with `world` virtual ranks on one device: every rank's output is the same bits, equal to
+    the sum of the ranks' partial outputs in rank order, and matches the unsharded forward;
+    a second epoch (the other half of the double-buffered receive area) gives the same."""
+    import oracle
+    import paper_2507_03117_b200 as bs
+    from paper_2507_03117_b200 import parallel
+    e, h, b = 512, 2048, 64
+    rng = np.random.default_rng(world * 100 + m)
+    wg, wu, wd = oracle.mlp_init(e, h, rng)
+    for w in (wg, wu, wd):  # 85 % block sparsity so lines hold few blocks
+        keep = rng.random((w.shape[0] // b, w.shape[1] // b)) < 0.15
+        w *= np.kron(keep, np.ones((b, b), np.float32))
+    x = torch.from_numpy(rng.standard_normal((m, e)).astype(np.float32)).cuda().to(dtype)
+    nets = _shard_nets(wg, wu, wd, b, world, dtype)
+    group = parallel.FusedTPGroup.local(world, m, e, b, dtype)
+    # reference: each rank's partial y (its shards alone, unfused), summed in rank order in fp32
+    parts = [bs.mlp_forward(x, n, save_activations=False)[0].float() for n in nets]
+    ref = parts[0]
+    for p in parts[1:]:
+        ref = ref + p
+    full = bs.SparseMlp(*(bs.MaskedMatrix.dense_init(w, b, dtype) for w in (wg, wu, wd)))
+    y_full, _ = bs.mlp_forward(x, full, save_activations=False)
+    for epoch in range(2):
+        for r in range(world):
+            group.forward(x, nets[r], r)
+        ys = [group.wait(r).clone() for r in range(world)]
+        torch.cuda.synchronize()
+        for r in range(1, world):
+            assert torch.equal(ys[r], ys[0])
+        tol = 1e-4 if dtype == torch.float32 else 2e-2
+        assert oracle.max_norm_rel(ys[0].float().cpu().numpy(), ref.cpu().numpy()) <= tol
+        assert oracle.max_norm_rel(ys[0].float().cpu().numpy(),
+                                   y_full.float().cpu().numpy()) <= tol
+        group.step()
