@@ -3,7 +3,8 @@ forward: column-parallel gate/up, row-parallel down, NCCL all-
 partial Y.
 
     python tools/tp_bench.py                 # one GPU: every TP degree's rank-0 shard, timed
-    torchrun --nproc-per-node N tools/tp_bench.py --tp  # N GPUs: real TP with the all-reduce
+    python tools/tp_bench.py --fused         # one GPU: fused down + all-reduce, virtual ranks
+    torchrun --nproc-per-node N tools/tp_bench.py --tp [--fused]  # N GPUs: real TP
 
 On one GPU the script times the shard a rank of an n-way TP group computes (h/n hidden
 columns, exact-k uniform masks per shard) for n = 1, 2, 4, 8, reports per-rank tokens/s and
@@ -67,7 +68,38 @@ def single_gpu(tokens):
         del net
 
 
-def multi_gpu(tokens):
+def single_gpu_fused(tokens):
+    """All ranks of an n-way group on one device (FusedTPGroup.local): the fused forward of
+    every rank back to back vs the same shards' plain forwards; the difference is the cost of
+    the fused epilogue (fp32 partial tiles to the owner, arrival counters, the last arriver's
+    rank-order sum written to every rank's output), exchange bandwidth being local HBM here."""
+    x = torch.randn(tokens, D, device="cuda").bfloat16()
+    for world in (2, 4, 8):
+        nets = [shard_net(r, world) for r in range(world)]
+        group = parallel.FusedTPGroup.local(world, tokens, D, B)
+
+        def plain():
+            for n in nets:
+                bs.mlp_forward(x, n, save_activations=False)
+
+        def fused():
+            for r, n in enumerate(nets):
+                group.forward(x, n, r)
+            for r in range(world):
+                group.wait(r)
+            group.step()
+
+        t_plain, t_fused = timed(plain), timed(fused)
+        print(json.dumps({
+            "config": "cfg4 TP, fused down + all-reduce, all ranks on one B200", "tp": world,
+            "tokens": tokens, "ms_all_ranks_plain": t_plain, "ms_all_ranks_fused": t_fused,
+            "fused_overhead_per_rank_ms": (t_fused - t_plain) / world,
+            "partial_bytes_per_rank": tokens * D * 4}), flush=True)
+        del nets, group
+        torch.cuda.empty_cache()
+
+
+def multi_gpu(tokens, fused=False):
     import torch.distributed as dist
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -88,7 +120,17 @@ def multi_gpu(tokens):
         dist.all_reduce(compute())
 
     res = {}
-    for name, fn in (("compute_ms", compute), ("allreduce_ms", reduce), ("forward_ms", both)):
+    cases = [("compute_ms", compute), ("allreduce_ms", reduce), ("forward_ms", both)]
+    if fused:
+        group = parallel.FusedTPGroup.symmetric(dist.group.WORLD, tokens, D, B)
+
+        def fused_fwd():
+            group.forward(x, net, rank)
+            group.wait(rank)
+            group.step()
+
+        cases.append(("fused_forward_ms", fused_fwd))
+    for name, fn in cases:
         dist.barrier()
         t = torch.tensor([timed(fn)], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -106,8 +148,11 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--tp", action="store_true", help="real TP under torchrun")
     ap.add_argument("--tokens", type=int, default=8192)
+    ap.add_argument("--fused", action="store_true", help="fused down + all-reduce")
     a = ap.parse_args()
     if a.tp:
-        multi_gpu(a.tokens)
+        multi_gpu(a.tokens, a.fused)
+    elif a.fused:
+        single_gpu_fused(a.tokens)
     else:
         single_gpu(a.tokens)
