@@ -7,12 +7,13 @@ any compute function raises, and every compute call needs CUDA tensors.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import torch
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libblast_b200.so"
+LIB_PATH = Path(os.environ["BLAST_LIB"]) if os.environ.get("BLAST_LIB") else _HERE / "libblast_b200.so"  # BLAST_LIB: A/B builds (dev)
 
 F32, BF16, F64 = 0, 1, 2
 ACT = {"none": 0, "relu": 1, "gelu": 2, "silu": 3}

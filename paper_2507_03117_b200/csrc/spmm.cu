@@ -20,6 +20,10 @@ struct EngineCall {
   int64_t a_cols = 0;  // columns (and row pitch) of the A sources
   const void* a0 = nullptr;
   const void* a1 = nullptr;
+  // F32: activations already split into tf32 hi (a0 / a1) and lo parts (e.g. G written split by
+  // the gate+up epilogue); when null the engine splits a0 / a1 itself
+  const void* a0_lo = nullptr;
+  const void* a1_lo = nullptr;
   const void* w0 = nullptr;
   const void* w0_hi = nullptr;  // F32: 3xTF32 operands (K-major image of the blocks)
   const void* w0_lo = nullptr;
@@ -35,6 +39,8 @@ struct EngineCall {
   void* out0 = nullptr;
   void* out1 = nullptr;
   void* out2 = nullptr;
+  void* out3 = nullptr;  // F32 gated fwd: G hi / lo split (SpmmParams::out3 / out4)
+  void* out4 = nullptr;
   const void* in0 = nullptr;
   const void* in1 = nullptr;
   int64_t ld_out = 0;
@@ -119,6 +125,8 @@ static SpmmParams make_params(const EngineCall& c) {
   p.out0 = c.out0;
   p.out1 = c.out1;
   p.out2 = c.out2;
+  p.out3 = c.out3;
+  p.out4 = c.out4;
   p.in0 = c.in0;
   p.in1 = c.in1;
   p.ld_out = c.ld_out;
@@ -240,16 +248,22 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
 }
 
 // Compile-time guard: does this configuration have >= 2 pipeline stages?
+// (NPASS = 3: split-K stages of one 128-byte K atom, accumulator pairs; two-matrix products
+// only in the sequential layout, one panel + one block per stage)
 template <int B, int ELT, int NPASS, int NMAT, bool SUM>
 constexpr bool tc_fits() {
+  constexpr bool sk = NPASS == 3;
   constexpr int rowb = B * ELT;
-  constexpr int a_tile = (128 * rowb + 1023) / 1024 * 1024;
-  constexpr int b_tile = (B * rowb + 1023) / 1024 * 1024;
-  constexpr int ncopy = NPASS == 3 ? 2 : 1;
-  constexpr int na = SUM ? NMAT : 1;
-  constexpr int stage = na * ncopy * a_tile + NMAT * ncopy * b_tile;
+  constexpr int krow = sk ? (rowb < 128 ? rowb : 128) : rowb;  // bytes of K per stage row
+  constexpr int a_tile = (128 * krow + 1023) / 1024 * 1024;
+  constexpr int b_tile = (B * krow + 1023) / 1024 * 1024;
+  constexpr int ncopy = sk ? 2 : 1;
+  constexpr int na = (SUM && !sk) ? NMAT : 1;
+  constexpr int nw = sk ? 1 : NMAT;
+  constexpr int stage = na * ncopy * a_tile + nw * ncopy * b_tile;
   constexpr int nacc = SUM ? 1 : NMAT;
-  return (200 * 1024) / stage >= 2 && 2 * nacc * B <= 512;
+  constexpr int accw = sk ? 2 * B : B;
+  return (200 * 1024) / stage >= 2 && 2 * nacc * accw <= 512 && (!sk || 2 * B <= 256);
 }
 
 // Staged (TMA-store) output for out0: bf16 outputs whose rows are 16-byte aligned, when
@@ -339,7 +353,13 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
         return launch_tc<B, ELT, NPASS, 1, false, (ELT == 4), EPI_STORE, OutT>(c, a0lo, a1lo, st);
       }
     } else if (c.nmat == 2 && c.epi == EPI_GATED_FWD) {
-      if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
+      if constexpr (NPASS == 3) {
+        // 3xTF32 gate+up: sequential layout (all gate blocks of the line, then all up blocks),
+        // split-K stages, accumulator pairs (the plan flags carry per-line block counts)
+        if constexpr (tc_fits<B, ELT, NPASS, 2, false>())
+          if (c.a_cols / B < 0x7fff)
+            return launch_tc<B, ELT, NPASS, 2, false, true, EPI_GATED_FWD, OutT, 0, 1, 2>(c, a0lo, a1lo, st);
+      } else if constexpr (tc_fits<B, ELT, NPASS, 2, false>()) {
         if constexpr (staged_fits<B, ELT, NPASS, 2, false, 2>())
           if (use_staged<B, ELT, NPASS, 2, false>(c) && c.m >= 256 && wide_tiles())
             return (split_stages() == 2 && seq_gate_up_pays<B>(c))
@@ -381,6 +401,11 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
           return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT, SO>(c, a0lo, a1lo, st);
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD, OutT>(c, a0lo, a1lo, st);
+    } else if (c.nmat == 2 && c.sumacc && c.epi == EPI_STORE && NPASS == 3) {
+      // 3xTF32 dX = dA Wg^T + dB Wu^T: sequential layout into one accumulator pair
+      if constexpr (NPASS == 3 && tc_fits<B, ELT, NPASS, 2, true>())
+        if (c.a_cols / B < 0x7fff)
+          return launch_tc<B, ELT, NPASS, 2, true, true, EPI_STORE, OutT, 0, 1, 2>(c, a0lo, a1lo, st);
     } else if (c.nmat == 2 && c.sumacc && c.epi == EPI_STORE) {
       // dX = dA Wg^T + dB Wu^T in one accumulator, staged (TMA-store) output. 256-token items
       // with the sequential layout (all dA blocks of the line, then all dB blocks; one panel +
@@ -392,7 +417,7 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (staged_fits<B, ELT, NPASS, 2, true>())
         if (use_staged<B, ELT, NPASS, 2, true>(c))
           return launch_tc<B, ELT, NPASS, 2, true, true, EPI_STORE, OutT, SO>(c, a0lo, a1lo, st);
-      if constexpr (tc_fits<B, ELT, NPASS, 2, true>())
+      if constexpr (NPASS != 3 && tc_fits<B, ELT, NPASS, 2, true>())
         return launch_tc<B, ELT, NPASS, 2, true, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
     }
   }
@@ -460,23 +485,25 @@ int run_engine(const EngineCall& c_in, cudaStream_t st) {
       int r = dispatch_tc<__nv_bfloat16, 2, 1>(c_in, nullptr, nullptr, st);
       if (r >= 0) return r;
     } else {
-      // 3xTF32: split the activations into hi/lo; weights carry their own split.
-      // (kind::tf32 reads B K-major, so forward products use transposed block copies)
+      // 3xTF32: split the activations into hi/lo (unless the caller passes them split);
+      // weights carry their own split (kind::tf32 reads B K-major, so forward products use
+      // transposed block copies)
       const bool w_split = c_in.w0_hi && c_in.w0_lo && (c_in.nmat == 1 || (c_in.w1_hi && c_in.w1_lo));
-      if (w_split && c_in.block <= 64) {
+      if (w_split) {
         const int64_t n = c_in.m * c_in.a_cols;
         Scratch s0, s1;
-        const int na = c_in.sumacc ? 2 : 1;
-        if (!s0.alloc(sizeof(float) * 2 * n, st)) return cuda_status(cudaGetLastError(), "scratch");
-        if (na == 2 && !s1.alloc(sizeof(float) * 2 * n, st))
-          return cuda_status(cudaGetLastError(), "scratch");
         EngineCall c = c_in;
-        float* h0 = s0.as<float>();
-        blast_split_tf32(static_cast<const float*>(c_in.a0), h0, h0 + n, n, st);
-        c.a0 = h0;
-        const void* lo0 = h0 + n;
-        const void* lo1 = nullptr;
-        if (na == 2) {
+        const void* lo0 = c_in.a0_lo;
+        const void* lo1 = c_in.a1_lo;
+        if (!lo0) {
+          if (!s0.alloc(sizeof(float) * 2 * n, st)) return cuda_status(cudaGetLastError(), "scratch");
+          float* h0 = s0.as<float>();
+          blast_split_tf32(static_cast<const float*>(c_in.a0), h0, h0 + n, n, st);
+          c.a0 = h0;
+          lo0 = h0 + n;
+        }
+        if (c_in.sumacc && !lo1) {
+          if (!s1.alloc(sizeof(float) * 2 * n, st)) return cuda_status(cudaGetLastError(), "scratch");
           float* h1 = s1.as<float>();
           blast_split_tf32(static_cast<const float*>(c_in.a1), h1, h1 + n, n, st);
           c.a1 = h1;
@@ -484,6 +511,10 @@ int run_engine(const EngineCall& c_in, cudaStream_t st) {
         }
         int r = dispatch_tc<float, 4, 3>(c, lo0, lo1, st);
         if (r >= 0) return r;
+        if (c_in.a0_lo || c_in.a1_lo) {
+          set_error("pre-split fp32 activations need the tensor-core engine");
+          return BLAST_EUNSUPPORTED;
+        }
       }
     }
   }
@@ -624,6 +655,13 @@ __global__ void gated_fwd_kernel(const T* a, const T* b, T* g, int64_t n) {
 }
 }  // namespace blast
 
+namespace blast {
+static bool f32_fused_ok(const void* x, int64_t e, const blast_bcsc_t* gate, const blast_bcsc_t* up);
+static int gate_up_impl(const void* x, int64_t m, const blast_bcsc_t* gate, const blast_bcsc_t* up,
+                        const blast_mlp_plan_t* plan, void* gated, void* gate_pre, void* up_out,
+                        void* g_hi, void* g_lo, cudaStream_t st);
+}  // namespace blast
+
 extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* gate,
                                  const blast_bcsc_t* up, const blast_bcsc_t* down,
                                  const blast_mlp_plan_t* plan, void* y, void* gate_pre,
@@ -639,12 +677,43 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
   if (m <= 0) return BLAST_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t elt = bytes_of(gate->dtype);
+  if (plan && plan->gu_step_ptr && f32_fused_ok(x, e, gate, up) && down->tf32_fwd_hi &&
+      down->tf32_fwd_lo) {
+    // fp32: the gate+up epilogue writes G already split into tf32 hi / lo (the down
+    // projection's 3xTF32 operands; G itself only when the caller asked for it)
+    Scratch ss;
+    if (!ss.alloc(2 * sizeof(float) * m * h, st)) return cuda_status(cudaGetLastError(), "scratch G");
+    float* g_hi = ss.as<float>();
+    float* g_lo = g_hi + m * h;
+    int r = gate_up_impl(x, m, gate, up, plan, gated, gate_pre, up_out, g_hi, g_lo, st);
+    if (r) return r;
+    EngineCall c;
+    c.dtype = BLAST_F32;
+    c.block = b;
+    c.m = m;
+    c.a_cols = h;
+    c.a0 = g_hi;
+    c.a0_lo = g_lo;
+    c.w0 = down->values;
+    c.w0_hi = down->tf32_fwd_hi;
+    c.w0_lo = down->tf32_fwd_lo;
+    c.nnzb0 = down->nnzb;
+    c.n_lines = cdiv(down->cols, b);
+    c.n_valid = down->cols;
+    c.step_ptr = down->fwd_step_ptr;
+    c.steps = down->fwd_steps;
+    c.flags = down->fwd_flags;
+    c.out0 = y;
+    c.ld_out = down->cols;
+    c.reverse_tiles = true;
+    return run_engine(c, st);
+  }
   Scratch sg;
   if (!gated) {
     if (!sg.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch G");
     gated = sg.ptr;
   }
-  int r = blast_mlp_gate_up(x, m, gate, up, plan, gated, gate_pre, up_out, stream);
+  int r = gate_up_impl(x, m, gate, up, plan, gated, gate_pre, up_out, nullptr, nullptr, st);
   if (r) return r;
   // gate+up wrote G tile by tile in order: read it back last tile first, while the most
   // recently written rows are still in L2
@@ -734,6 +803,89 @@ extern "C" int blast_tp_wait(const uint32_t* done, uint32_t target, void* stream
   return check_launch("tp_wait");
 }
 
+namespace blast {
+// fp32 gate+up through the fused 3xTF32 engine (sequential layout, accumulator pairs):
+// b in {16, 32, 64} (the two accumulator pairs fit TMEM twice), transposed tf32 block images
+static bool f32_fused_ok(const void* x, int64_t e, const blast_bcsc_t* gate, const blast_bcsc_t* up) {
+  const int b = gate->block;
+  return gate->dtype == BLAST_F32 && (b == 16 || b == 32 || b == 64) && gate->tf32_fwd_hi &&
+         gate->tf32_fwd_lo && up->tf32_fwd_hi && up->tf32_fwd_lo && aligned16(x) &&
+         (e * 4) % 16 == 0 && e / b < 0x7fff;
+}
+
+// G = silu(X Wg) * (X Wu) (mlp.py:111-113). g_hi / g_lo (fp32, optional): G also written as
+// its tf32 hi / lo split for a 3xTF32 down projection; `gated` may then be null.
+static int gate_up_impl(const void* x, int64_t m, const blast_bcsc_t* gate, const blast_bcsc_t* up,
+                        const blast_mlp_plan_t* plan, void* gated, void* gate_pre, void* up_out,
+                        void* g_hi, void* g_lo, cudaStream_t st) {
+  const int64_t e = gate->rows, h = gate->cols;
+  const int b = gate->block;
+  const int dt = gate->dtype;
+  const size_t elt = bytes_of(dt);
+  int r;
+  const bool fused = plan && plan->gu_step_ptr &&
+                     (dt == BLAST_BF16 || f32_fused_ok(x, e, gate, up));
+  if (!fused && !gated) {
+    set_error("gate_up: output buffer required");
+    return BLAST_EINVAL;
+  }
+  if (fused) {
+    EngineCall c;
+    c.dtype = dt;
+    c.block = b;
+    c.nmat = 2;
+    c.epi = EPI_GATED_FWD;
+    c.m = m;
+    c.a_cols = e;
+    c.a0 = x;
+    c.w0 = gate->values;
+    c.w0_hi = gate->tf32_fwd_hi;
+    c.w0_lo = gate->tf32_fwd_lo;
+    c.nnzb0 = gate->nnzb;
+    c.w1 = up->values;
+    c.w1_hi = up->tf32_fwd_hi;
+    c.w1_lo = up->tf32_fwd_lo;
+    c.nnzb1 = up->nnzb;
+    c.n_lines = cdiv(h, b);
+    c.n_valid = h;
+    c.step_ptr = plan->gu_step_ptr;
+    c.steps = plan->gu_steps;
+    c.flags = plan->gu_flags;
+    c.out0 = gated;
+    c.out1 = gate_pre;
+    c.out2 = up_out;
+    c.ld_out = h;
+    if (dt == BLAST_F32) {
+      c.out3 = g_hi;
+      c.out4 = g_lo;
+    }
+    return run_engine(c, st);
+  }
+  Scratch sa, sb;
+  if (!gate_pre) {
+    if (!sa.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch a");
+    gate_pre = sa.ptr;
+  }
+  if (!up_out) {
+    if (!sb.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch b");
+    up_out = sb.ptr;
+  }
+  if ((r = blast_bspmm(x, m, gate, BLAST_ACT_NONE, gate_pre, st))) return r;
+  if ((r = blast_bspmm(x, m, up, BLAST_ACT_NONE, up_out, st))) return r;
+  const int64_t n = m * h;
+  const int grid = static_cast<int>(std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 16));
+  if (dt == BLAST_BF16)
+    gated_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(gate_pre), static_cast<const __nv_bfloat16*>(up_out),
+        static_cast<__nv_bfloat16*>(gated), n);
+  else
+    gated_fwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(gate_pre),
+                                                  static_cast<const float*>(up_out),
+                                                  static_cast<float*>(gated), n);
+  return check_launch("gated_fwd");
+}
+}  // namespace blast
+
 extern "C" int blast_mlp_gate_up(const void* x, int64_t m, const blast_bcsc_t* gate,
                                  const blast_bcsc_t* up, const blast_mlp_plan_t* plan,
                                  void* gated, void* gate_pre, void* up_out, void* stream) {
@@ -749,60 +901,8 @@ extern "C" int blast_mlp_gate_up(const void* x, int64_t m, const blast_bcsc_t* g
     set_error("gate_up: output buffer required");
     return BLAST_EINVAL;
   }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int dt = gate->dtype;
-  const size_t elt = bytes_of(dt);
-  int r;
-  const bool fused = dt == BLAST_BF16 && plan && plan->gu_step_ptr;
-  if (fused) {
-    EngineCall c;
-    c.dtype = dt;
-    c.block = b;
-    c.nmat = 2;
-    c.epi = EPI_GATED_FWD;
-    c.m = m;
-    c.a_cols = e;
-    c.a0 = x;
-    c.w0 = gate->values;
-    c.nnzb0 = gate->nnzb;
-    c.w1 = up->values;
-    c.nnzb1 = up->nnzb;
-    c.n_lines = cdiv(h, b);
-    c.n_valid = h;
-    c.step_ptr = plan->gu_step_ptr;
-    c.steps = plan->gu_steps;
-    c.flags = plan->gu_flags;
-    c.out0 = gated;
-    c.out1 = gate_pre;
-    c.out2 = up_out;
-    c.ld_out = h;
-    r = run_engine(c, st);
-    if (r) return r;
-  } else {
-    Scratch sa, sb;
-    if (!gate_pre) {
-      if (!sa.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch a");
-      gate_pre = sa.ptr;
-    }
-    if (!up_out) {
-      if (!sb.alloc(elt * m * h, st)) return cuda_status(cudaGetLastError(), "scratch b");
-      up_out = sb.ptr;
-    }
-    if ((r = blast_bspmm(x, m, gate, BLAST_ACT_NONE, gate_pre, stream))) return r;
-    if ((r = blast_bspmm(x, m, up, BLAST_ACT_NONE, up_out, stream))) return r;
-    const int64_t n = m * h;
-    const int grid = static_cast<int>(std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 16));
-    if (dt == BLAST_BF16)
-      gated_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(gate_pre), static_cast<const __nv_bfloat16*>(up_out),
-          static_cast<__nv_bfloat16*>(gated), n);
-    else
-      gated_fwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(gate_pre),
-                                                    static_cast<const float*>(up_out),
-                                                    static_cast<float*>(gated), n);
-    if ((r = check_launch("gated_fwd"))) return r;
-  }
-  return BLAST_OK;
+  return gate_up_impl(x, m, gate, up, plan, gated, gate_pre, up_out, nullptr, nullptr,
+                      static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int blast_mlp_backward_dgrad(const void* dy, int64_t m, const void* gate_pre,

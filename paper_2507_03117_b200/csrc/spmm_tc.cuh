@@ -60,6 +60,8 @@ struct SpmmParams {
   void* out0;  // Y | G | dA
   void* out1;  // saved gate_pre (fwd) | dB (bwd)
   void* out2;  // saved up_out (fwd)
+  void* out3;  // fp32 gated fwd: G's tf32 hi part (the down projection's A operand); optional
+  void* out4;  // fp32 gated fwd: G's lo part (with out3)
   const void* in0;  // bwd: gate_pre
   const void* in1;  // bwd: up_out
   int64_t ld_out;   // row stride (elements) of every out*/in* array
@@ -191,10 +193,23 @@ struct TcCfg {
   static constexpr int MMA_K = 32 / ELT;                  // 16 (bf16) / 8 (tf32)
   static constexpr int KSL = B / MMA_K;                   // MMAs per block along K
   static constexpr int NCOPY = NPASS == 3 ? 2 : 1;        // hi / lo operand copies
+  // 3xTF32 (fp32): a stage carries ONE swizzle atom of K (32 fp32) of the hi and lo copies of
+  // the panel and of the block, so a 64-wide block is NATOM stages of 48 KB instead of one
+  // 96 KB stage (four in flight instead of two). Per K slice one N = 2B MMA multiplies A_hi
+  // by [W_hi; W_lo] (adjacent in smem) into an accumulator pair and one N = B MMA adds
+  // A_lo * W_hi to the pair's second half; the epilogue sums the pair (hi*hi and the cross
+  // terms accumulate separately).
+  static constexpr bool SK = NPASS == 3;
+  static constexpr int KPS = SK ? 1 : NATOM;              // K atoms per stage
+  static constexpr int SPS = SK ? NATOM : 1;              // stages per step (stored block)
+  static constexpr int KSL_ST = KSL / SPS;                // MMA K slices per stage
+  static constexpr int ACC_W = SK ? 2 * B : B;            // TMEM columns per accumulator
   static constexpr int NA = (SUMACC && !SPLIT) ? NMAT : 1;  // distinct A panels per stage
   static constexpr int round1k(int x) { return (x + 1023) / 1024 * 1024; }
-  static constexpr int A_TILE = round1k(TROWS * ROWB);
-  static constexpr int B_TILE = round1k(B * ROWB);
+  static constexpr int A_BYTES = TROWS * SW * KPS;        // one copy of a stage's panel
+  static constexpr int B_BYTES = B * SW * KPS;            // one copy of a stage's block
+  static constexpr int A_TILE = round1k(A_BYTES);
+  static constexpr int B_TILE = round1k(B_BYTES);
   static constexpr int WSLOTS = SPLIT ? 1 : NMAT;           // weight blocks per stage
   static constexpr int STAGE = NA * NCOPY * A_TILE + WSLOTS * NCOPY * B_TILE;
 #ifndef BLAST_ONE_OUTBUF_1MAT
@@ -216,7 +231,7 @@ struct TcCfg {
   static constexpr int STAGES_RAW = SMEM_BUDGET / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int NACC = SUMACC ? 1 : NMAT;
-  static constexpr int HALF_ACC = NACC * B;               // TMEM columns per 128-row half
+  static constexpr int HALF_ACC = NACC * ACC_W;           // TMEM columns per 128-row half
   static constexpr int ACC_STRIDE = TM * HALF_ACC;        // TMEM columns per accumulator stage
   static constexpr int TMEM_COLS_RAW = 2 * ACC_STRIDE;
   static constexpr int TMEM_COLS = TMEM_COLS_RAW <= 32    ? 32
@@ -226,6 +241,9 @@ struct TcCfg {
                                                           : 512;
   static constexpr uint32_t IDESC =
       make_idesc(BM, B, ELT == 2 ? 1u : 2u, 0u, B_KMAJOR ? 0u : 1u);
+  static constexpr uint32_t IDESC_PAIR = make_idesc(BM, 2 * B, 2u, 0u, 0u);  // SK: N = 2B
+  static_assert(!SK || (ELT == 4 && B_KMAJOR && 2 * B <= 256 && SW == ROWB / NATOM),
+                "split-K stages: fp32, K-major blocks");
   // barriers + tmem slot live after the stages
   static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE + STAGING + BAR_BYTES + 1024;  // +1024 alignment slack
@@ -426,10 +444,26 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
         else
           g[i] = gated_fwd(v0[i], v1[i]);
       }
-      if constexpr (STG_SW > 0)
+      if constexpr (STG_SW > 0) {
         stage_chunk16<OutT, STG_SW>(stg, trow, tcol, g);
-      else
-        store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
+      } else {
+        if (p.out0) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
+        if constexpr (sizeof(OutT) == 4) {
+          // fp32: G also leaves as its 3xTF32 hi / lo split, the down projection's operands
+          if (p.out3) {
+            float lo[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float v = g[i];
+              const float hi = isfinite(v) ? __uint_as_float(__float_as_uint(v) & 0xFFFFE000u) : v;
+              lo[i] = isfinite(v) ? __fsub_rn(v, hi) : 0.0f;
+              g[i] = hi;
+            }
+            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out3) + off, g, valid, vec_ok);
+            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out4) + off, lo, valid, vec_ok);
+          }
+        }
+      }
     }
   } else if constexpr (EPI == EPI_GATED_FWD_SAVE) {
     // G, a, b into three staged tiles (rows / columns outside the tensor clipped by TMA)
@@ -514,7 +548,7 @@ constexpr int kEpiWarpsT = 8;  // epilogue warps of both engines (named barrier 
 // `tacc` is the TMEM address of accumulator 0 for this warp's lane quarter; row0 / col0 are
 // the tile's first output row / column. Staging buffers alternate per tile (`stg`); the TMA
 // store issued from a buffer two tiles ago must have finished reading it.
-template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW, int NBUF = 2>
+template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW, int NBUF = 2, int ACC_W = B>
 __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t tacc, int row0,
                                                  int col0, int flags, uint8_t* stg, int half,
                                                  uint32_t q, uint32_t lane, uint32_t etid,
@@ -529,21 +563,39 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
   const bool row_ok = row < p.m;
   constexpr int NCH = B / 16;
   constexpr bool kTwoAcc = EPI == EPI_GATED_FWD || EPI == EPI_GATED_FWD_SAVE;
+  // ACC_W = 2B: every accumulator is a pair (hi*hi in columns [0, B), the 3xTF32 cross terms
+  // in [B, 2B)) summed here
+  constexpr bool kPair = ACC_W == 2 * B;
   const bool acc0_init = SUMACC ? ((flags & 3) != 0) : ((flags & 1) != 0);
   // this warp's 16-column chunks are c = half, half + 2, ...; the TMEM loads of two chunks
   // (both accumulators when gated) are issued before one wait
 #pragma unroll 1
   for (int c0 = half; c0 < NCH; c0 += 4) {
     uint32_t r0[2][16], r1[2][16];
+    [[maybe_unused]] uint32_t p0[kPair ? 2 : 1][16], p1[kPair && kTwoAcc ? 2 : 1][16];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int c = c0 + 2 * k;
       if (c < NCH) {
         tmem_ld16_nowait(tacc + c * 16, r0[k]);
-        if (kTwoAcc) tmem_ld16_nowait(tacc + B + c * 16, r1[k]);
+        if (kTwoAcc) tmem_ld16_nowait(tacc + ACC_W + c * 16, r1[k]);
+        if constexpr (kPair) {
+          tmem_ld16_nowait(tacc + B + c * 16, p0[k]);
+          if constexpr (kTwoAcc) tmem_ld16_nowait(tacc + ACC_W + B + c * 16, p1[k]);
+        }
       }
     }
     tmem_wait_ld();
+    if constexpr (kPair) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          r0[k][i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[k][i]), __uint_as_float(p0[k][i])));
+          if constexpr (kTwoAcc)
+            r1[k][i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[k][i]), __uint_as_float(p1[k][i])));
+        }
+    }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int c = c0 + 2 * k;
@@ -604,7 +656,7 @@ __device__ __forceinline__ float4 ld_volatile_f4(const float* p) {
 // No CTA ever waits on another GPU inside the kernel, so ranks overlap the exchange with
 // their own remaining tiles; consumers wait for done[rank] (blast_tp_wait) before reading y.
 // The TMEM reads come first; `release` frees the accumulator stage right after them.
-template <int B, typename OutT>
+template <int B, typename OutT, int ACC_W = B>
 __device__ __noinline__ void epi_tp_tile(const SpmmParams& p, uint32_t tacc, int t128, int j,
                                          int flags, int half, uint32_t q, uint32_t lane,
                                          uint32_t etid, bool release, uint64_t* acc_empty,
@@ -621,7 +673,15 @@ __device__ __noinline__ void epi_tp_tile(const SpmmParams& p, uint32_t tacc, int
 #pragma unroll
   for (int k = 0; k < (NCH + 1) / 2; ++k) {
     const int c = half + 2 * k;
-    if (c < NCH) tmem_ld16(tacc + c * 16, v[k]);
+    if (c < NCH) {
+      tmem_ld16(tacc + c * 16, v[k]);
+      if constexpr (ACC_W == 2 * B) {  // 3xTF32 accumulator pair
+        float w[16];
+        tmem_ld16(tacc + B + c * 16, w);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[k][i] = __fadd_rn(v[k][i], w[i]);
+      }
+    }
   }
   if (release) {
     tc_fence_before();
@@ -758,9 +818,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   constexpr int IN_ST = in_staged<EPI, OUT_ELT>();
   using C = TcCfg<B, ELT, NPASS, NMAT, SUMACC, B_KMAJOR, OUT_ELT, TM, IN_ST, SPLIT,
                   staged_outputs<EPI>()>;
-  static_assert(!SPLIT || (NMAT == 2 && NPASS == 1 &&
+  static_assert(!SPLIT || (NMAT == 2 && (NPASS == 1 || SPLIT == 2) &&
                            (SPLIT == 2) == use_waiter<NMAT, TM, SPLIT>()),
                 "split stages: gate+up products only");
+  static_assert(!C::SK || NMAT == 1 || SPLIT == 2, "3xTF32 two-matrix products: sequential layout");
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
 #ifdef BLAST_WAIT_COUNTERS
   const long long t_kernel0 = clock64();
@@ -869,31 +930,41 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             const int4 st = cur.get(s);
             const int kb = pass == 0 ? st.y : st.z;
             if (kb < 0) continue;
-            if ((n++ & 1u) != mine) {
-              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-              continue;
-            }
-            wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
-            if (elect_one()) {
-              uint8_t* sbase = smem + stage * C::STAGE;
-              if (kDiagSwitches && (p.skip_epilogue & 2)) {  // diagnosis: stale operands
-                mbar_arrive(&full[stage]);
-              } else {
-                mbar_expect_tx(&full[stage], C::TROWS * C::ROWB + B * C::ROWB);
-#pragma unroll
-                for (int at = 0; at < C::NATOM; ++at)
-                  tma_load_2d(sbase + at * C::TROWS * C::SW,
-                              (SUMACC && pass == 1) ? &mapA1 : &mapA0, &full[stage],
-                              st.x * B + at * C::SWE, t * C::TROWS);
-                const CUtensorMap* mw = pass == 0 ? &mapW0 : &mapW1;
-#pragma unroll
-                for (int at = 0; at < C::NATOM; ++at)
-                  tma_load_2d_hint(sbase + C::A_TILE + at * B * C::SW, mw, &full[stage],
-                                   at * C::SWE, kb * B, pol_w);
+#pragma unroll 1
+            for (int sa = 0; sa < C::SPS; ++sa) {  // SK: one stage per K atom of the block
+              if ((n++ & 1u) != mine) {
+                if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                continue;
               }
+              wc.wait(0, &empty[stage], phase ^ 1, dbg_on);
+              if (elect_one()) {
+                uint8_t* sbase = smem + stage * C::STAGE;
+                if (kDiagSwitches && (p.skip_epilogue & 2)) {  // diagnosis: stale operands
+                  mbar_arrive(&full[stage]);
+                } else {
+                  mbar_expect_tx(&full[stage], C::NCOPY * (C::A_BYTES + C::B_BYTES));
+                  const bool a1 = SUMACC && pass == 1;
+#pragma unroll
+                  for (int c = 0; c < C::NCOPY; ++c)
+#pragma unroll
+                    for (int at = 0; at < C::KPS; ++at)
+                      tma_load_2d(sbase + c * C::A_TILE + at * C::TROWS * C::SW,
+                                  c == 0 ? (a1 ? &mapA1 : &mapA0) : (a1 ? &mapA1lo : &mapA0lo),
+                                  &full[stage], st.x * B + (C::SK ? sa : at) * C::SWE,
+                                  t * C::TROWS);
+#pragma unroll
+                  for (int c = 0; c < C::NCOPY; ++c)
+#pragma unroll
+                    for (int at = 0; at < C::KPS; ++at)
+                      tma_load_2d_hint(sbase + C::NCOPY * C::A_TILE + c * C::B_TILE + at * B * C::SW,
+                                       c == 0 ? (pass == 0 ? &mapW0 : &mapW1)
+                                              : (pass == 0 ? &mapW0lo : &mapW1lo),
+                                       &full[stage], (C::SK ? sa : at) * C::SWE, kb * B, pol_w);
+                }
+              }
+              __syncwarp();
+              if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             }
-            __syncwarp();
-            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
         }
       }
@@ -920,6 +991,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         uint32_t meta = step_recipe<NMAT, SUMACC, kMergeP && !SPLIT>(make_int4(st.x, kb[0], kb[1], 0),
                                                                      init0, init1);
         if (SPLIT && s + 1 == s1 && part + 1 == nparts) meta |= kMetaLast;
+#pragma unroll 1
+        for (int sa = 0; sa < C::SPS; ++sa) {  // SK: one stage per K atom of the block(s)
         if ((n++ & 1u) != mine) {
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           continue;
@@ -929,10 +1002,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           uint32_t bytes = 0;
 #pragma unroll
           for (int a = 0; a < C::NA; ++a)
-            if (!SUMACC || kb[a] >= 0) bytes += C::NCOPY * (C::TROWS * C::ROWB);
+            if (!SUMACC || kb[a] >= 0) bytes += C::NCOPY * C::A_BYTES;
 #pragma unroll
           for (int mm = 0; mm < NMAT; ++mm)
-            if (kb[mm] >= 0) bytes += C::NCOPY * (B * C::ROWB);
+            if (kb[mm] >= 0) bytes += C::NCOPY * C::B_BYTES;
           if (!use_waiter<NMAT, TM, SPLIT>()) stage_meta[stage] = meta;
           if (kDiagSwitches && (p.skip_epilogue & 2)) {  // diagnosis: stale operands
             mbar_arrive(&full[stage]);
@@ -951,9 +1024,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             for (int c = 0; c < C::NCOPY; ++c) {
               uint8_t* dst = sbase + (a * C::NCOPY + c) * C::A_TILE;
 #pragma unroll
-              for (int at = 0; at < C::NATOM; ++at)
+              for (int at = 0; at < C::KPS; ++at)
                 tma_load_2d(dst + at * C::TROWS * C::SW, c == 0 ? mh : ml, &full[stage],
-                            st.x * B + at * C::SWE, t * C::TROWS);
+                            st.x * B + (C::SK ? sa : at) * C::SWE, t * C::TROWS);
             }
           }
 #pragma unroll
@@ -966,15 +1039,16 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             for (int c = 0; c < C::NCOPY; ++c) {
               uint8_t* dst = sbase + C::NA * C::NCOPY * C::A_TILE + (slot * C::NCOPY + c) * C::B_TILE;
 #pragma unroll
-              for (int at = 0; at < C::NATOM; ++at) {
+              for (int at = 0; at < C::KPS; ++at) {
                 tma_load_2d_hint(dst + at * B * C::SW, c == 0 ? mh : ml, &full[stage],
-                                 at * C::SWE, kb[mm] * B, pol_w);
+                                 (C::SK ? sa : at) * C::SWE, kb[mm] * B, pol_w);
               }
             }
           }
         }
         __syncwarp();
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
         }
       }
     }
@@ -1006,6 +1080,23 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         return ((byte_k / C::SW) * B * C::SW + (byte_k % C::SW)) >> 4;
       }
       return (static_cast<uint32_t>(ks) * C::MMA_K * C::SW) >> 4;
+    };
+    // One stage's MMAs for one 128-row half into accumulator `d` (init: accumulate into it).
+    // bf16 / tf32: KSL_ST K slices of N = B. SK (3xTF32): per K slice A_hi x [W_hi; W_lo]
+    // (N = 2B) into the pair (d, d + B), then A_lo x W_hi into d + B.
+    auto issue_stage = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t init) {
+#pragma unroll
+      for (int ks = 0; ks < C::KSL_ST; ++ks) {
+        const uint32_t acc_flag = (init | ks) ? 1u : 0u;
+        if constexpr (C::SK) {
+          mma_tf32(d, ad + a_koff(ks), bd + b_koff(ks), C::IDESC_PAIR, acc_flag);
+          mma_tf32(d + B, ad + (C::A_TILE >> 4) + a_koff(ks), bd + b_koff(ks), C::IDESC, 1u);
+        } else if constexpr (ELT == 4) {
+          mma_tf32(d, ad + a_koff(ks), bd + b_koff(ks), C::IDESC, acc_flag);
+        } else {
+          mma_f16(d, ad + a_koff(ks), bd + b_koff(ks), C::IDESC, acc_flag);
+        }
+      }
     };
     constexpr bool kWaiter = use_waiter<NMAT, TM, SPLIT>();
     uint32_t stage = 0, phase = 0, it = 0;
@@ -1047,28 +1138,29 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           // SUMACC (dX = dA Wg^T + dB Wu^T): both passes accumulate into one accumulator
           const uint32_t sel = (!SUMACC && i >= n0) ? 1u : 0u;
           const uint32_t init = SUMACC ? (i != 0 ? 1u : 0u) : ((i != 0 && i != n0) ? 1u : 0u);
-          named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
-          tc_fence_after();
-          const long long ti0 = dbg_on ? clock64() : 0;
-          if (elect_one()) {
-            const uint32_t soff = (stage * C::STAGE) >> 4;
-            const uint64_t bb = b_desc0 + soff;
+#pragma unroll 1
+          for (int sa = 0; sa < C::SPS; ++sa) {  // SK: the block's K atoms, one stage each
+            named_bar_sync(kBarStage + stage, 64);  // warp 2 saw full[stage]
+            tc_fence_after();
+            const long long ti0 = dbg_on ? clock64() : 0;
+            if (elect_one()) {
+              const uint32_t soff = (stage * C::STAGE) >> 4;
+              const uint64_t bb = b_desc0 + soff;
 #pragma unroll
-            for (int h = 0; h < TM; ++h) {
-              const uint64_t ad = a_desc0 + soff + ((h * C::BM * C::SW) >> 4);
-              const uint32_t d = d_base + h * C::HALF_ACC + sel * B;
-#pragma unroll
-              for (int ks = 0; ks < C::KSL; ++ks)
-                mma_f16(d, ad + a_koff(ks), bb + b_koff(ks), C::IDESC, (init | ks) ? 1u : 0u);
+              for (int h = 0; h < TM; ++h) {
+                const uint64_t ad = a_desc0 + soff + ((h * C::BM * C::SW) >> 4);
+                const uint32_t d = d_base + h * C::HALF_ACC + sel * C::ACC_W;
+                issue_stage(d, ad, bb, (init | (sa != 0 ? 1u : 0u)));
+              }
+              mma_commit(&empty[stage]);
             }
-            mma_commit(&empty[stage]);
+            __syncwarp();
+            if (dbg_on) {
+              wc.acc[6] += static_cast<unsigned long long>(clock64() - ti0);
+              wc.acc[7] += 1;
+            }
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
-          if (dbg_on) {
-            wc.acc[6] += static_cast<unsigned long long>(clock64() - ti0);
-            wc.acc[7] += 1;
-          }
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         if (elect_one()) mma_commit(&tmem_full[as]);
         __syncwarp();
@@ -1113,6 +1205,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
             else meta |= init1 ? kMetaAccSecond : 0u;
           }
         }
+#pragma unroll 1
+        for (int sa = 0; sa < C::SPS; ++sa) {  // SK (single-matrix): one stage per K atom
         if constexpr (NMAT == 1 || kBallot) {
           if constexpr (kWaiter) {
             const long long tw0 = dbg_on ? clock64() : 0;
@@ -1128,6 +1222,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           meta = ld_shared_u32(&stage_meta[stage]);  // the producer's recipe
           if (SPLIT) done = (meta & kMetaLast) != 0;
         }
+        if (sa != 0) meta |= kMetaAccFirst | kMetaAccSecond;  // later K atoms accumulate
         const long long ti0 = dbg_on ? clock64() : 0;
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
@@ -1149,27 +1244,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
                 if (!(meta & (mm == 0 ? kMetaHas0 : kMetaHas1))) continue;
                 const int acc_i = SUMACC ? 0 : mm;
                 const int a_i = SUMACC ? mm : 0;
-                const uint32_t d = dh + acc_i * B;
-                const uint64_t a_hi = ad + ((a_i * C::NCOPY * C::A_TILE) >> 4);
-                const uint64_t a_lo = a_hi + (C::A_TILE >> 4);
-                const uint64_t b_hi = bd + (((SPLIT ? 0 : mm) * C::NCOPY * C::B_TILE) >> 4);
-                const uint64_t b_lo = b_hi + (C::B_TILE >> 4);
                 const uint32_t init =
                     (meta & (mm == 0 ? kMetaAccFirst : kMetaAccSecond)) ? 1u : 0u;
-#pragma unroll
-                for (int ks = 0; ks < C::KSL; ++ks) {
-                  const uint32_t acc_flag = (init | ks) ? 1u : 0u;
-                  if constexpr (NPASS == 3) {
-                    // small cross terms first, then the hi*hi product
-                    mma_tf32(d, a_lo + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
-                    mma_tf32(d, a_hi + a_koff(ks), b_lo + b_koff(ks), C::IDESC, 1u);
-                    mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, 1u);
-                  } else if constexpr (ELT == 4) {
-                    mma_tf32(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
-                  } else {
-                    mma_f16(d, a_hi + a_koff(ks), b_hi + b_koff(ks), C::IDESC, acc_flag);
-                  }
-                }
+                issue_stage(dh + acc_i * C::ACC_W, ad + ((a_i * C::NCOPY * C::A_TILE) >> 4),
+                            bd + (((SPLIT ? 0 : mm) * C::NCOPY * C::B_TILE) >> 4), init);
               }
             }
           }
@@ -1181,6 +1259,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
           wc.acc[7] += 1;
         }
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
       }
       if (elect_one()) mma_commit(&tmem_full[as]);
       __syncwarp();
@@ -1203,6 +1282,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       } else {
         n_steps = __ldg(&p.step_ptr[j + 1]) - __ldg(&p.step_ptr[j]);
       }
+      n_steps *= C::SPS;  // SK: one stage per K atom of every block
       wc.wait(3, &tmem_empty[as], (use & 1) ^ 1, dbg_on);
       named_bar_arrive(kBarAcc + as, 64);
       for (int s = 0; s < n_steps; ++s) {
@@ -1264,7 +1344,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         if (p.tp.n > 0) {  // fused TP all-reduce of the row-parallel down projection
 #pragma unroll 1
           for (int h = 0; h < TM; ++h)
-            epi_tp_tile<B, OutT>(p, tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE +
+            epi_tp_tile<B, OutT, C::ACC_W>(p, tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE +
                                         h * C::HALF_ACC,
                                  t * TM + h, j, flags, half, q, lane, etid, h == TM - 1,
                                  &tmem_empty[as], reinterpret_cast<volatile int*>(in_full + 2));
@@ -1277,7 +1357,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         const uint32_t tacc =
             tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
         const int row0 = t * C::TROWS + h * C::BM;
-        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS>(
+        epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS, C::ACC_W>(
             p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
             IN_ST ? in_staging + ((it & 1) * IN_ST * TM + h) * C::OUT_TILE : nullptr,
             C::OUT_TILE, TM * C::OUT_TILE);

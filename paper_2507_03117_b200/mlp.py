@@ -198,6 +198,8 @@ def mlp_forward(x, mlp: SparseMlp, save_activations: bool = True, out=None,
     a = b = None
     if save_activations:
         a, b, g = (torch.empty(m, h, dtype=dt, device=A.DEVICE) for _ in range(3))
+    elif dt == torch.float32:
+        g = None  # fp32: the library keeps G as its tf32 hi / lo split in pooled scratch
     else:
         g = mlp.workspace(m)
     if m:
