@@ -224,7 +224,9 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   // chip-wide L2 -> SM feed, which an even split cannot raise, so it keeps round robin.
   // Decode-size products (fewer than two items per CTA) balance the gate+up product too:
   // cfg3 shape at 95 %, 128 tokens, graph replay 18.6 -> 16.7 us (profiles/r02/decode_ab.txt).
-  if (NMAT == 1 || items < 2 * static_cast<int64_t>(num_sms()))
+  // 3xTF32 gate+up (cfg0 fp32: per-CTA ends spread over 22.5 of 104.6 us with round robin) is
+  // balanced as well: its 48 KB stages make it latency- rather than L2-feed-bound
+  if (NMAT == 1 || NPASS == 3 || items < 2 * static_cast<int64_t>(num_sms()))
     p.sched = balanced_schedule(c.step_ptr, c.flags, p.n_lines, p.n_tok_tiles, grid, SPLIT == 2,
                                 st, &p.sched_rows);
   dbg_begin(st);

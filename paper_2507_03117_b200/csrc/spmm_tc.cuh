@@ -330,10 +330,35 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int ks) {
                     8u * SW, swizzle_layout_code(SW));
 }
 
-template <typename OutT>
+#ifndef BLAST_V8
+#define BLAST_V8 1
+#endif
+// V8: 256-bit stores when 32-byte aligned. Not used in the out-of-line TP epilogue
+// (epi_tp_tile): there the 256-bit store of a pointer loaded from the local copy of the
+// parameters wrote wrong data (tests/test_gpu_parallel.py virtual ranks), the 128-bit path
+// is correct.
+template <typename OutT, bool V8 = true>
 __device__ __forceinline__ void store_chunk16(OutT* dst, const float (&v)[16], int valid,
                                               bool vec_ok) {
-  if (vec_ok && valid >= 16) {
+  if (V8 && BLAST_V8 && vec_ok && valid >= 16 && (reinterpret_cast<uintptr_t>(dst) & 31u) == 0) {
+    // whole 32-byte sectors per thread and instruction (row-strided tiles: one row per lane)
+    if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        st_global_v8(dst + 8 * i, __float_as_uint(v[8 * i]), __float_as_uint(v[8 * i + 1]),
+                     __float_as_uint(v[8 * i + 2]), __float_as_uint(v[8 * i + 3]),
+                     __float_as_uint(v[8 * i + 4]), __float_as_uint(v[8 * i + 5]),
+                     __float_as_uint(v[8 * i + 6]), __float_as_uint(v[8 * i + 7]));
+    } else {
+      uint32_t w[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        __nv_bfloat162 pr = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+        w[h] = *reinterpret_cast<uint32_t*>(&pr);
+      }
+      st_global_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+    }
+  } else if (vec_ok && valid >= 16) {
     if constexpr (sizeof(OutT) == 4) {
       float4* d = reinterpret_cast<float4*>(dst);
 #pragma unroll
@@ -359,7 +384,22 @@ __device__ __forceinline__ void store_chunk16(OutT* dst, const float (&v)[16], i
 }
 template <typename T>
 __device__ __forceinline__ void load_chunk16(const T* src, float (&v)[16], int valid, bool vec_ok) {
-  if (vec_ok && valid >= 16) {
+  if (BLAST_V8 && vec_ok && valid >= 16 && (reinterpret_cast<uintptr_t>(src) & 31u) == 0) {
+    uint32_t w[sizeof(T) == 4 ? 2 : 1][8];
+#pragma unroll
+    for (int i = 0; i < (sizeof(T) == 4 ? 2 : 1); ++i) ld_global_v8(src + 8 * i * (sizeof(T) == 4 ? 1 : 2), w[i]);
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(w[i / 8][i % 8]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[0][h]));
+        v[2 * h] = f.x;
+        v[2 * h + 1] = f.y;
+      }
+    }
+  } else if (vec_ok && valid >= 16) {
     if constexpr (sizeof(T) == 4) {
       const float4* s = reinterpret_cast<const float4*>(src);
 #pragma unroll
@@ -737,7 +777,7 @@ __device__ __noinline__ void epi_tp_tile(const SpmmParams& p, uint32_t tacc, int
       const int valid = p.n_valid - col;
       const int64_t off = static_cast<int64_t>(row) * p.ld_out + col;
       for (int r = 0; r < n; ++r)
-        store_chunk16<OutT>(reinterpret_cast<OutT*>(tp.y[r]) + off, s, valid,
+        store_chunk16<OutT, false>(reinterpret_cast<OutT*>(tp.y[r]) + off, s, valid,
                             (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0);
     }
   }

@@ -1,0 +1,12 @@
+"""Quick timing of bench extras without the full bench: python tools/extras_quick.py cfg0 decode ..."""
+import sys, json
+sys.path.insert(0, ".")
+import torch, bench
+import paper_2507_03117_b200 as bs
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
+hbm, tf, _ = bench.load_peaks()
+for what in sys.argv[1:] or ["cfg0", "decode"]:
+    if what == "cfg0":
+        print(json.dumps(bench.extra_cfg0_fp32(bs, flush, tf, 20, 0)))
+    elif what == "decode":
+        print(json.dumps(bench.extra_decode(bs, flush, hbm, 50, 0)))
