@@ -53,7 +53,8 @@ def cfg3_sweep():
     dense_ms = timed(lambda: F.linear(F.silu(F.linear(x, wg)) * F.linear(x, wu), wd))
     del wg, wu, wd
     peak = bench.load_peaks()[1]
-    for b in (16, 32, 64, 128):
+    blocks = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else (16, 32, 64, 128)
+    for b in blocks:
         for s in (0.5, 0.7, 0.8, 0.9, 0.95):
             ws = bench.make_weights(d, h, b, s, 0)
             net = bs.SparseMlp.from_caches(*[bs.from_host(w, torch.bfloat16) for w in ws])

@@ -23,7 +23,8 @@ def run(e, h, b, s, m, dt):
         print(f"e={e} h={h} b={b} m={m} {dt} save={save}: y {err:.2e} g {gerr:.2e}", flush=True)
 
 for dt in (torch.bfloat16, torch.float32):
-    for (e, h, b, s, m) in [(256, 512, 64, 0.5, 200), (512, 1024, 64, 0.75, 512), (256, 512, 32, 0.5, 256)]:
+    for (e, h, b, s, m) in [(256, 512, 64, 0.5, 200), (512, 1024, 64, 0.75, 512), (256, 512, 32, 0.5, 256),
+                            (1024, 2048, 16, 0.9, 512), (1024, 2048, 32, 0.9, 300), (1024, 2048, 16, 0.8, 1000)]:
         run(e, h, b, s, m, dt)
 
 print("single products:")
