@@ -47,9 +47,23 @@ __global__ void __launch_bounds__(256) block_norms_kernel(const T* __restrict__ 
       constexpr int VW = 16 / sizeof(T);
       const int per_row = b / VW;
       const int total = b * per_row;
-      for (int e = lane; e < total; e += 32) {
-        const int ii = e / per_row, jj = (e - ii * per_row) * VW;
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(src + (i0 + ii) * cols + j0 + jj));
+      // U loads in flight per lane before their FMAs (the products are still accumulated in
+      // ascending e, so the sum is bitwise the one-load-at-a-time loop's)
+      constexpr int U = 8;
+      for (int e0 = lane; e0 < total; e0 += 32 * U) {
+        uint4 qs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + 32 * u;
+          if (e < total) {
+            const int ii = e / per_row, jj = (e - ii * per_row) * VW;
+            qs[u] = __ldg(reinterpret_cast<const uint4*>(src + (i0 + ii) * cols + j0 + jj));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+        if (e0 + 32 * u >= total) break;
+        const uint4 q = qs[u];
         if constexpr (sizeof(T) == 8) {
           const double d0 = __hiloint2double(static_cast<int>(q.y), static_cast<int>(q.x));
           const double d1 = __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z));
@@ -68,6 +82,7 @@ __global__ void __launch_bounds__(256) block_norms_kernel(const T* __restrict__ 
             acc = fma((double)f.x, (double)f.x, acc);
             acc = fma((double)f.y, (double)f.y, acc);
           }
+        }
         }
       }
     } else {
@@ -232,6 +247,34 @@ __global__ void __launch_bounds__(1024) topk_kernel(const double* __restrict__ n
 // the 64-bit norm key, then over the column-major index among exact ties. No
 // grid barriers and no scratch; blockIdx.x selects one of two independent grids
 // (the weight and gradient selections of generate_masks run in one launch).
+// one warp scans the 256 bins (8 per lane) and names the bucket holding the krem-th key:
+// its index, the count of keys in lower buckets and its own count
+__device__ __forceinline__ void topk_pick_bucket(const unsigned int* hist, unsigned int krem,
+                                                 unsigned int* bucket, unsigned int* below_out,
+                                                 unsigned int* count) {
+  unsigned int local[8], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    local[j] = hist[threadIdx.x * 8 + j];
+    sum += local[j];
+  }
+  unsigned int incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (threadIdx.x >= static_cast<unsigned int>(o)) incl += t;
+  }
+  unsigned int below = incl - sum;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (below < krem && krem <= below + local[j]) {
+      *bucket = threadIdx.x * 8 + j;
+      *below_out = below;
+      *count = local[j];
+    }
+    below += local[j];
+  }
+}
+
 constexpr int kTopkSmemMax = 24576;
 
 __global__ void __launch_bounds__(1024) topk_smem_kernel(const double* __restrict__ norms0,
@@ -245,66 +288,115 @@ __global__ void __launch_bounds__(1024) topk_smem_kernel(const double* __restric
   const double* norms = blockIdx.x == 0 ? norms0 : norms1;
   uint8_t* keep = blockIdx.x == 0 ? keep0 : keep1;
   const int n = static_cast<int>(gr * gc);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = norm_key(norms[i]);
-  uint64_t pre1 = 0;
+  // 8 independent loads in flight per thread (the norms come from L2 / HBM)
+  for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      v[u] = i < n ? __ldg(&norms[i]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n) keys[i] = norm_key(v[u]);
+    }
+  }
+  __shared__ unsigned int sel_count;
+  __shared__ uint64_t red_and[32], red_or[32];
+  // bits common to every key: the radix passes start below them (block norms of similar
+  // magnitude share sign, exponent and the top mantissa bits)
+  {
+    uint64_t ka = ~0ull, ko = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      ka &= keys[i];
+      ko |= keys[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ka &= __shfl_xor_sync(0xffffffffu, ka, o);
+      ko |= __shfl_xor_sync(0xffffffffu, ko, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red_and[threadIdx.x >> 5] = ka;
+      red_or[threadIdx.x >> 5] = ko;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int nw = static_cast<int>(blockDim.x >> 5);
+      ka = threadIdx.x < nw ? red_and[threadIdx.x] : ~0ull;
+      ko = threadIdx.x < nw ? red_or[threadIdx.x] : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ka &= __shfl_xor_sync(0xffffffffu, ka, o);
+        ko |= __shfl_xor_sync(0xffffffffu, ko, o);
+      }
+      if (threadIdx.x == 0) {
+        red_and[0] = ka;
+        red_or[0] = ko;
+      }
+    }
+    __syncthreads();
+  }
+  const uint64_t kdiff = red_and[0] ^ red_or[0];
+  int top = kdiff ? 64 - __clzll(static_cast<long long>(kdiff)) : 0;  // bits [top, 64) common
+  uint64_t pre1 = top >= 64 ? 0ull : (top == 0 ? red_and[0] : (red_and[0] >> top) << top);
   uint32_t pre2 = 0;
   unsigned int krem = static_cast<unsigned int>(k);
-  // 8 passes over K1, then 2 over lin (n <= 24576 < 2^16)
-  for (int pass = 0; pass < 10; ++pass) {
-    const bool on_lin = pass >= 8;
-    const int sh = on_lin ? (9 - pass) * 8 : (7 - pass) * 8;
+  uint64_t thr_all = 0;  // early exit: every key <= thr_all is selected (no tie-break needed)
+  bool early = false;
+  // digits of <= 8 bits over K1 from the highest differing bit, then 2 passes over lin among
+  // exact ties (n <= 24576 < 2^16); stops as soon as the bucket holding the k-th key is
+  // selected whole (it holds exactly the keys still needed)
+  while (top > 0 && !early) {
+    const int sh = top > 8 ? top - 8 : 0;
+    const int w = top - sh;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
       const uint64_t k1 = keys[idx];
-      unsigned int digit;
-      if (!on_lin) {
-        const int top = sh + 8;
-        if (top < 64 && (k1 >> top) != (pre1 >> top)) continue;
-        digit = static_cast<unsigned int>((k1 >> sh) & 0xFF);
-      } else {
-        if (k1 != pre1) continue;
-        const int r = idx / static_cast<int>(gc), c = idx - r * static_cast<int>(gc);
-        const uint32_t lin = static_cast<uint32_t>(c * gr + r);
-        const int top = sh + 8;
-        if (top < 16 && (lin >> top) != (pre2 >> top)) continue;
-        digit = (lin >> sh) & 0xFF;
-      }
-      atomicAdd(&hist[digit], 1u);
+      if (top < 64 && (k1 >> top) != (pre1 >> top)) continue;
+      const unsigned int digit = static_cast<unsigned int>((k1 >> sh) & ((1ull << w) - 1));
+      // warp-aggregated: keys of similar norms share digits
+      const unsigned int peers = __match_any_sync(__activemask(), digit);
+      if ((threadIdx.x & 31) == static_cast<unsigned int>(__ffs(peers) - 1))
+        atomicAdd(&hist[digit], static_cast<unsigned int>(__popc(peers)));
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // one warp scans the 256 bins, 8 per lane
-      unsigned int local[8], sum = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        local[j] = hist[threadIdx.x * 8 + j];
-        sum += local[j];
-      }
-      unsigned int incl = sum;
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (threadIdx.x >= o) incl += t;
-      }
-      unsigned int below = incl - sum;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (below < krem && krem <= below + local[j]) {
-          sel_bucket = threadIdx.x * 8 + j;
-          sel_below = below;
-        }
-        below += local[j];
-      }
-    }
+    if (threadIdx.x < 32) topk_pick_bucket(hist, krem, &sel_bucket, &sel_below, &sel_count);
     __syncthreads();
     krem -= sel_below;
-    if (!on_lin) pre1 |= static_cast<uint64_t>(sel_bucket) << sh;
-    else pre2 |= static_cast<uint32_t>(sel_bucket) << sh;
+    pre1 |= static_cast<uint64_t>(sel_bucket) << sh;
+    if (sel_count == krem) {  // the whole bucket is selected: done
+      thr_all = sh ? (pre1 | ((uint64_t(1) << sh) - 1)) : pre1;
+      early = true;
+    }
+    top = sh;
+    __syncthreads();
+  }
+  // exact ties on K1 (pre1 is the k-th key): two 8-bit passes over the column-major index
+  for (int lp = 0; lp < 2 && !early; ++lp) {
+    const int sh = (1 - lp) * 8;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      if (keys[idx] != pre1) continue;
+      const int r = idx / static_cast<int>(gc), c = idx - r * static_cast<int>(gc);
+      const uint32_t lin = static_cast<uint32_t>(c * gr + r);
+      if (lp == 1 && (lin >> 8) != (pre2 >> 8)) continue;
+      atomicAdd(&hist[(lin >> sh) & 0xFF], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) topk_pick_bucket(hist, krem, &sel_bucket, &sel_below, &sel_count);
+    __syncthreads();
+    krem -= sel_below;
+    pre2 |= static_cast<uint32_t>(sel_bucket) << sh;
     __syncthreads();
   }
   for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
     const uint64_t k1 = keys[idx];
-    bool kp = k1 < pre1;
-    if (k1 == pre1) {
+    bool kp = early ? k1 <= thr_all : k1 < pre1;
+    if (!early && k1 == pre1) {
       const int r = idx / static_cast<int>(gc), c = idx - r * static_cast<int>(gc);
       kp = static_cast<uint32_t>(c * gr + r) <= pre2;
     }
@@ -491,12 +583,32 @@ __global__ void __launch_bounds__(256) apply_mask_gather_vec4_kernel(
     const int32_t* __restrict__ kmap, float4* masked, V* values) {
   const int64_t n4 = rows * cols4;
   const int64_t bb = static_cast<int64_t>(b) * b;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / cols4, col = (i - row * cols4) * 4;
-    const int64_t r = row / b, c = col / b;
+  // 4 independent 16-byte loads in flight per thread; 32-bit index arithmetic when it fits
+  constexpr int U = 4;
+  const bool small = n4 < (int64_t(1) << 31);
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x * U + threadIdx.x; i0 < n4;
+       i0 += (int64_t)gridDim.x * blockDim.x * U) {
+    float4 vs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * (int64_t)blockDim.x < n4) vs[u] = __ldg(&x[i0 + u * (int64_t)blockDim.x]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + u * (int64_t)blockDim.x;
+    if (i >= n4) break;
+    int64_t row, col;
+    if (small) {
+      const uint32_t q = static_cast<uint32_t>(i) / static_cast<uint32_t>(cols4);
+      row = q;
+      col = (static_cast<uint32_t>(i) - q * static_cast<uint32_t>(cols4)) * 4;
+    } else {
+      row = i / cols4;
+      col = (i - row * cols4) * 4;
+    }
+    const int64_t r = static_cast<uint32_t>(row) / static_cast<uint32_t>(b);
+    const int64_t c = static_cast<uint32_t>(col) / static_cast<uint32_t>(b);
     const int64_t cell = r * gc + c;
-    const float4 v = __ldg(&x[i]);
+    const float4 v = vs[u];
     float4 m = v;
     if (mode != 0) {
       const bool surv = kept[cell] != 0 || (mode == 2 && regrown[cell] != 0);
@@ -517,6 +629,7 @@ __global__ void __launch_bounds__(256) apply_mask_gather_vec4_kernel(
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
         *reinterpret_cast<uint2*>(values + off) = pk;
       }
+    }
     }
   }
 }
@@ -760,7 +873,7 @@ extern "C" int blast_apply_mask_gather(const void* dense, int64_t rows, int64_t 
   const bool vec = dtype == BLAST_F32 && cols % 4 == 0 && block % 4 == 0 && aligned16(dense) &&
                    (!masked_out || aligned16(masked_out)) && aligned16(values);
   if (vec) {
-    const int g4 = grid_for(n / 4, 256, 32);
+    const int g4 = grid_for(cdiv(n / 4, 4), 256, 32);
     if (values_dtype == BLAST_F32)
       apply_mask_gather_vec4_kernel<float><<<g4, 256, 0, st>>>(
           static_cast<const float4*>(dense), rows, cols / 4, block, gc, kept, regrown, mode, kmap,

@@ -8,5 +8,8 @@ hbm, tf, _ = bench.load_peaks()
 for what in sys.argv[1:] or ["cfg0", "decode"]:
     if what == "cfg0":
         print(json.dumps(bench.extra_cfg0_fp32(bs, flush, tf, 20, 0)))
+    elif what == "prune":
+        import paper_2507_03117_b200._lib as L
+        print(json.dumps(bench.extra_prune_refresh(bs, L, flush, hbm, 20)))
     elif what == "decode":
         print(json.dumps(bench.extra_decode(bs, flush, hbm, 50, 0)))
