@@ -92,6 +92,8 @@ extern "C" int blast_mlp_forward_host(const void* x_host, int64_t m, const blast
   // the exposed head (copy-in alone) and tail (compute + copy-out alone)
   std::vector<int64_t> bounds{0};
   if (!chunk_tokens && m > 2 * chunk) {
+    // (first / last chunk 512 tokens at cfg3: 1.796 ms vs 1.804 (384), 1.846 (256), 1.858
+    // (128); profiles/r02/e2e_pipeline.txt)
     const int64_t half = std::max<int64_t>(128, chunk / 3 / 128 * 128);
     bounds.push_back(half);
     while (m - bounds.back() > half + chunk) bounds.push_back(bounds.back() + chunk);
@@ -101,10 +103,14 @@ extern "C" int blast_mlp_forward_host(const void* x_host, int64_t m, const blast
   }
   bounds.push_back(m);
   const int64_t n_chunks = static_cast<int64_t>(bounds.size()) - 1;
-  // three X and Y slots: copy-in may run two chunks ahead of the copy-out, so neither
-  // DMA direction waits on the other through a shared slot
-  const int slots = static_cast<int>(std::min<int64_t>(n_chunks, 3));
+  // X and Y slots: one per chunk while both fit 1 GiB (every copy-in is queued back to back
+  // with no slot dependency), else three (copy-in may run two chunks ahead of the copy-out,
+  // so neither DMA direction waits on the other through a shared slot)
   const size_t row_bytes = elt * e;
+  const int slots = static_cast<int>(
+      2 * static_cast<size_t>(n_chunks) * chunk * row_bytes <= (size_t(1) << 30)
+          ? n_chunks
+          : std::min<int64_t>(n_chunks, 3));
 
   Scratch sx, sy, sg;
   if (!sx.alloc(slots * chunk * row_bytes, st) || !sy.alloc(slots * chunk * row_bytes, st) ||
@@ -132,6 +138,20 @@ extern "C" int blast_mlp_forward_host(const void* x_host, int64_t m, const blast
     return rc;
   };
   std::vector<cudaEvent_t> ev_comp(n_chunks), ev_out(n_chunks);
+  // BLAST_PIPE_TRACE=1 (diagnosis): per-chunk copy-in / compute / copy-out spans to stderr
+  static const bool trace = [] {
+    const char* e = getenv("BLAST_PIPE_TRACE");
+    return e && e[0] == '1';
+  }();
+  std::vector<cudaEvent_t> tr;
+  auto tmark = [&](cudaStream_t s) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    tr.push_back(e);
+  };
+  tmark(st);
   const char* xh = static_cast<const char*>(x_host);
   char* yh = static_cast<char*>(y_host);
   for (int64_t c = 0; c < n_chunks; ++c) {
@@ -145,22 +165,41 @@ extern "C" int blast_mlp_forward_host(const void* x_host, int64_t m, const blast
     if (!ev_in || !ev_comp[c] || !ev_out[c]) return join(cuda_status(cudaGetLastError(), "event"));
     // copy-in: the X slot is free once chunk c-slots' compute has consumed it
     if (c >= slots) cudaStreamWaitEvent(cs->in, ev_comp[c - slots], 0);
+    tmark(cs->in);
     cudaError_t ce = cudaMemcpyAsync(xd, xh + r0 * row_bytes, mc * row_bytes,
                                      cudaMemcpyHostToDevice, cs->in);
     if (ce != cudaSuccess) return join(cuda_status(ce, "copy-in"));
     cudaEventRecord(ev_in, cs->in);
+    tmark(cs->in);
     // compute: needs the chunk's X, and the Y slot drained by chunk c-slots' copy-out
     cudaStreamWaitEvent(st, ev_in, 0);
     if (c >= slots) cudaStreamWaitEvent(st, ev_out[c - slots], 0);
+    tmark(st);
     int r = blast_mlp_forward(xd, mc, gate, up, down, plan, yd, nullptr, nullptr, sg.ptr, st);
     if (r) return join(r);
     cudaEventRecord(ev_comp[c], st);
+    tmark(st);
     // copy-out
     cudaStreamWaitEvent(cs->out, ev_comp[c], 0);
+    tmark(cs->out);
     ce = cudaMemcpyAsync(yh + r0 * row_bytes, yd, mc * row_bytes, cudaMemcpyDeviceToHost,
                          cs->out);
     if (ce != cudaSuccess) return join(cuda_status(ce, "copy-out"));
     cudaEventRecord(ev_out[c], cs->out);
+    tmark(cs->out);
+  }
+  if (trace) {
+    const int rc = join(check_launch("mlp_forward_host"));
+    cudaStreamSynchronize(st);
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      float t[6];
+      for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&t[k], tr[0], tr[1 + 6 * c + k]);
+      fprintf(stderr, "[blast pipe] chunk %lld (%lld tok): in %7.1f-%7.1f  mlp %7.1f-%7.1f  out %7.1f-%7.1f us\n",
+              (long long)c, (long long)(bounds[c + 1] - bounds[c]), t[0] * 1e3, t[1] * 1e3,
+              t[2] * 1e3, t[3] * 1e3, t[4] * 1e3, t[5] * 1e3);
+    }
+    for (cudaEvent_t e : tr) cudaEventDestroy(e);
+    return rc;
   }
   // the caller's stream passes this point only after the last copy-out
   return join(check_launch("mlp_forward_host"));
