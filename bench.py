@@ -74,6 +74,21 @@ def make_weights(d, h, b, s, seed):
             synth_bcsc(h, d, b, s, rng, 0.5 / np.sqrt(h)))
 
 
+L2_FEED_TBS = 17.96  # max chip L2 -> SM rate, 1-D bulk copies (tools/mma_probe.cu P5, profiles/r01/mma_probe.txt)
+
+
+def l2_feed_roof(weights, m, ms_per_step):
+    """L2 -> shared-memory bytes of the forward (activation panel + weight block per stored
+    block and 256-token tile) against the measured chip feed rate."""
+    tiles = -(-m // 256)
+    b = weights[0].block
+    panel, blk = 256 * b * 2, b * b * 2
+    nbytes = sum(len(w.block_row_idx) for w in weights) * tiles * (panel + blk)
+    ms = nbytes / (L2_FEED_TBS * 1e12) * 1e3
+    return {"bytes_per_step": nbytes, "peak_tbs": L2_FEED_TBS, "ms_at_peak": ms,
+            "frac": ms / ms_per_step, "peak_source": "tools/mma_probe.cu P5 (bulk L2->smem)"}
+
+
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -536,7 +551,12 @@ def run_blast(args):
             "frac": max(flops_total / (tf_peak * 1e12), step_bytes / (hbm_peak * 1e9))
             / (ms_per_step * 1e-3),
             "achieved_tflops": flops_total / (ms_per_step * 1e-3) / 1e12,
-            "kernel_ms": {"gate_up": t_gu * 1e3, "down": t_dn * 1e3}},
+            "kernel_ms": {"gate_up": t_gu * 1e3, "down": t_dn * 1e3},
+            # the binding on-chip limit: every stored block reads its
+            # 256-token activation panel and the block itself from L2 into shared memory
+            # (no panel reuse at this sparsity); ncu counts exactly these bytes
+            # (l1tex__m_xbar2l1tex_read_bytes, profiles/r02/ncu_full_cfg3_summary.txt)
+            "l2_feed": l2_feed_roof(weights, m, ms_per_step)},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": m * D * 2,
                 "d2h_bytes_per_step": m * D * 2,
                 "path": "pinned host x -> mlp_forward (public API, chunked H2D/MLP/D2H "

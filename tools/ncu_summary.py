@@ -15,6 +15,11 @@ KEYS = [
     ("dram__bytes_read.sum", "dram rd"),
     ("dram__bytes_write.sum", "dram wr"),
     ("smsp__issue_inst0.avg.pct_of_peak_sustained_active", "issue idle%"),
+    ("lts__t_sectors_srcunit_tex.avg.pct_of_peak_sustained_elapsed", "l2 tag (tex)%"),
+    ("lts__t_sectors_srcunit_tex.max.pct_of_peak_sustained_elapsed", "l2 tag max%"),
+    ("lts__t_sectors_srcunit_ltcfabric.avg.pct_of_peak_sustained_elapsed", "l2 fabric%"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "tc smem rd%"),
+    ("derived__lts__lts2xbar_bytes.sum.per_second", "l2->xbar B/s"),
 ]
 
 
