@@ -226,7 +226,11 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   // cfg3 shape at 95 %, 128 tokens, graph replay 18.6 -> 16.7 us (profiles/r02/decode_ab.txt).
   // 3xTF32 gate+up (cfg0 fp32: per-CTA ends spread over 22.5 of 104.6 us with round robin) is
   // balanced as well: its 48 KB stages make it latency- rather than L2-feed-bound
-  if (NMAT == 1 || NPASS == 3 || items < 2 * static_cast<int64_t>(num_sms()))
+#ifndef BLAST_LPT_SUMACC
+#define BLAST_LPT_SUMACC 1
+#endif
+  if (NMAT == 1 || NPASS == 3 || (BLAST_LPT_SUMACC && SUM) ||
+      items < 2 * static_cast<int64_t>(num_sms()))
     p.sched = balanced_schedule(c.step_ptr, c.flags, p.n_lines, p.n_tok_tiles, grid, SPLIT == 2,
                                 st, &p.sched_rows);
   dbg_begin(st);

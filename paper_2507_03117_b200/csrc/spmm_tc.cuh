@@ -217,8 +217,14 @@ struct TcCfg {
 #endif
   // single-buffered output staging buys a fifth 40 KB stage (gate+up SPLIT layouts; with
   // BLAST_ONE_OUTBUF_1MAT also the 256-token single-matrix products)
+#ifndef BLAST_ONE_OUTBUF_BWD2
+#define BLAST_ONE_OUTBUF_BWD2 1
+#endif
   static constexpr int OUT_BUFS =
-      (SPLIT || (BLAST_ONE_OUTBUF_1MAT && NMAT == 1 && TM == 2 && IN_ST == 0 && B >= 64)) ? 1 : 2;
+      (SPLIT || (BLAST_ONE_OUTBUF_1MAT && NMAT == 1 && TM == 2 && IN_ST == 0 && B >= 64) ||
+       (BLAST_ONE_OUTBUF_BWD2 && IN_ST == 2))
+          ? 1
+          : 2;
   static constexpr int OUT_ROWB = B * OUT_ELT;                          // bytes of an output tile row
   static constexpr int OUT_SW = OUT_ROWB < 128 ? OUT_ROWB : 128;
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;

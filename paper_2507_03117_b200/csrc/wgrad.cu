@@ -34,9 +34,12 @@ struct WgradParams {
   int64_t gr;
 };
 
+// Tokens per pipeline stage (the K of one handshake): 128 -> 8 MMAs per stage (round 1: 64).
+constexpr int kWgTK = 128;
+
 template <int B>
 struct WgCfg {
-  static constexpr int TK = 64;                 // tokens per stage
+  static constexpr int TK = kWgTK;              // tokens per stage
   static constexpr int ATOM = TK * 128;         // one [TK x 64 bf16] swizzle-128 atom
   static constexpr int A_TILE = 2 * ATOM;       // 128 output rows
   static constexpr int NB_ATOM = B / 64;
@@ -47,6 +50,9 @@ struct WgCfg {
   static constexpr uint32_t IDESC = make_idesc(128, B, 1u, 1u, 1u);
   static constexpr int SMEM_BYTES = STAGES * STAGE + 256 + 1024;
 };
+
+constexpr uint32_t kWgBarAcc = 2;    // + accumulator stage (2 ids)
+constexpr uint32_t kWgBarStage = 4;  // + ring stage (<= 8 ids)
 
 template <int B>
 __global__ void __launch_bounds__(256, 1)
@@ -128,19 +134,22 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    // MN-major operands: K slice kk = 16 token rows (2 KB); LBO = 64-wide atom stride
+    // MN-major operands: K slice kk = 16 token rows (2 KB); LBO = 64-wide atom stride.
+    // The MMA warp waits on named barriers released by the waiter warp (3): an mbarrier wait
+    // or shared-memory read in this warp queues behind its own in-flight MMAs (DESIGN.md
+    // section 3, tools/mma_probe.cu P8).
     const uint64_t a_desc0 = make_sdesc(smem_u32(smem), C::ATOM, 1024, 2);
     const uint64_t b_desc0 = make_sdesc(smem_u32(smem) + C::A_TILE, C::ATOM, 1024, 2);
-    uint32_t stage = 0, phase = 0, it = 0;
+    uint32_t stage = 0, it = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-      const uint32_t as = it & 1, use = it >> 1;
+      const uint32_t as = it & 1;
       int k0, k1;
       krange(w, k0, k1);
-      mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+      named_bar_sync(kWgBarAcc + as, 64);  // warp 3 saw tmem_empty[as]
       tc_fence_after();
       const uint32_t d = tmem_base + as * B;
       for (int ks = k0; ks < k1; ++ks) {
-        mbar_wait(&full[stage], phase);
+        named_bar_sync(kWgBarStage + stage, 64);  // warp 3 saw full[stage]
         tc_fence_after();
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
@@ -152,10 +161,25 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           mma_commit(&empty[stage]);
         }
         __syncwarp();
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == C::STAGES) stage = 0;
       }
       if (elect_one()) mma_commit(&tmem_full[as]);
       __syncwarp();
+    }
+  } else if (warp == 3) {
+    // barrier waiter: mirrors the MMA warp's sequence
+    uint32_t stage = 0, phase = 0, it = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+      const uint32_t as = it & 1, use = it >> 1;
+      int k0, k1;
+      krange(w, k0, k1);
+      mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+      named_bar_arrive(kWgBarAcc + as, 64);
+      for (int ks = k0; ks < k1; ++ks) {
+        mbar_wait(&full[stage], phase);
+        named_bar_arrive(kWgBarStage + stage, 64);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
     }
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;
@@ -450,7 +474,7 @@ static int block_wgrad_impl(const void* a, const void* d, int64_t m, int64_t row
     }
     p.n_items = static_cast<int32_t>((nsel + gc + per_item - 1) / per_item);
     // split-K when the blocks cannot fill the GPU (e.g. GPT-2 small at 90%: ~60 blocks)
-    const int ksteps = static_cast<int>(cdiv(m, 64));
+    const int ksteps = static_cast<int>(cdiv(m, kWgTK));
     int n_split = 1;
     if (p.n_items < 2 * num_sms() && ksteps >= 8)
       n_split = std::min<int>({static_cast<int>(cdiv(2 * num_sms(), p.n_items)), ksteps / 4, 32});
