@@ -105,7 +105,7 @@ static void dbg_end(const char* name, cudaStream_t st, int ctas) {
 static SpmmParams make_params(const EngineCall& c) {
   SpmmParams p{};
   p.dbg = dbg_buffer();
-  {
+  if constexpr (kDiagSwitches) {  // diagnosis builds only (-DBLAST_DIAG_SWITCHES=1)
     static int skip = -1;
     if (skip < 0) {
       const char* e = getenv("BLAST_SKIP_EPILOGUE");

@@ -78,7 +78,7 @@ struct SpmmParams {
   blast_tp_t tp;            // tp.n > 0: fused down-projection + all-reduce epilogue (epi_tp_tile)
 };
 
-// BLAST_SKIP_EPILOGUE's "skip operand loads" switch (diagnosis) is compiled in only on request
+// BLAST_SKIP_EPILOGUE (diagnosis: skip epilogues / operand loads) is compiled in only on request
 #ifndef BLAST_DIAG_SWITCHES
 #define BLAST_DIAG_SWITCHES 0  // 0.3472 vs 0.3485 ms per cfg3 step with it in (same box)
 #endif
@@ -1380,7 +1380,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
       if constexpr (IN_ST) mbar_wait(&in_full[it & 1], (it >> 1) & 1);
-      if (p.skip_epilogue & 1) {  // diagnosis: release the accumulator unread
+      if (kDiagSwitches && (p.skip_epilogue & 1)) {  // diagnosis: release the accumulator unread
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[as]);
