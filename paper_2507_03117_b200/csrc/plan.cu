@@ -136,18 +136,41 @@ __global__ void plan_fill_kernel(const int32_t* kmap0, const int32_t* kmap1, int
   if (lane == 0) flags[line] = f | (min(n0, 0x7fff) << 2) | (min(n1, 0x7fff) << 17);
 }
 
-__global__ void split_tf32_kernel(const float* x, float* hi, float* lo, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = x[i];
-    float h = v, l = 0.0f;
-    if (isfinite(v)) {
-      h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-      l = __fsub_rn(v, h);
-    }
-    hi[i] = h;
-    lo[i] = l;
+__device__ __forceinline__ void tf32_split1(float v, float& h, float& l) {
+  h = v;
+  l = 0.0f;
+  if (isfinite(v)) {
+    h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    l = __fsub_rn(v, h);
   }
+}
+// 16-byte vectors, 4 per thread in flight (scalar tail for n % 4 or unaligned buffers)
+__global__ void split_tf32_kernel(const float* x, float* hi, float* lo, int64_t n) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) |
+                     reinterpret_cast<uintptr_t>(lo)) & 15u) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n4; i0 += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * stride < n4) v[u] = __ldg(x4 + i0 + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n4) break;
+      float4 h, l;
+      tf32_split1(v[u].x, h.x, l.x);
+      tf32_split1(v[u].y, h.y, l.y);
+      tf32_split1(v[u].z, h.z, l.z);
+      tf32_split1(v[u].w, h.w, l.w);
+      reinterpret_cast<float4*>(hi)[i] = h;
+      reinterpret_cast<float4*>(lo)[i] = l;
+    }
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    tf32_split1(x[i], hi[i], lo[i]);
 }
 
 // hi/lo split of every block, once as stored (rt) and once transposed (fwd)
