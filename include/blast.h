@@ -123,7 +123,8 @@ int blast_kmap_from_bcsc(const int64_t* col_ptr, const int32_t* row_idx, int64_t
 int blast_build_plan(const int32_t* kmap0, const int32_t* kmap1, int64_t grid_rows,
                      int64_t grid_cols, int by_rows, int32_t* step_ptr, int32_t* steps,
                      int32_t* flags, void* stream);
-/* 3xTF32 operand split: hi = x with the low 13 mantissa bits cleared, lo = x - hi. */
+/* 3xTF32 operand split: hi = x with the low 13 mantissa bits cleared, lo = x - hi. hi may be
+ * NULL: the engine passes the raw x as the hi operand (kind::tf32 reads it truncated). */
 int blast_split_tf32(const float* x, float* hi, float* lo, int64_t n, void* stream);
 /* 3xTF32 weight operands of an F32 BCSC: split values[nnzb][b][b] into hi/lo, once as
  * stored (rt_*) and once with every block transposed (fwd_*): kind::tf32 reads B K-major. */

@@ -146,6 +146,7 @@ __device__ __forceinline__ void tf32_split1(float v, float& h, float& l) {
 }
 // 16-byte vectors, 4 per thread in flight (scalar tail for n % 4 or unaligned buffers)
 __global__ void split_tf32_kernel(const float* x, float* hi, float* lo, int64_t n) {
+  // hi may be null (lo only: the raw x serves as the hi operand)
   const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) |
                      reinterpret_cast<uintptr_t>(lo)) & 15u) == 0;
   const int64_t n4 = vec ? n / 4 : 0;
@@ -165,12 +166,16 @@ __global__ void split_tf32_kernel(const float* x, float* hi, float* lo, int64_t 
       tf32_split1(v[u].y, h.y, l.y);
       tf32_split1(v[u].z, h.z, l.z);
       tf32_split1(v[u].w, h.w, l.w);
-      reinterpret_cast<float4*>(hi)[i] = h;
+      if (hi) reinterpret_cast<float4*>(hi)[i] = h;
       reinterpret_cast<float4*>(lo)[i] = l;
     }
   }
-  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    tf32_split1(x[i], hi[i], lo[i]);
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float h, l;
+    tf32_split1(x[i], h, l);
+    if (hi) hi[i] = h;
+    lo[i] = l;
+  }
 }
 
 // hi/lo split of every block, once as stored (rt) and once transposed (fwd)

@@ -501,19 +501,17 @@ int run_engine(const EngineCall& c_in, cudaStream_t st) {
         EngineCall c = c_in;
         const void* lo0 = c_in.a0_lo;
         const void* lo1 = c_in.a1_lo;
+        // the raw activation is the hi operand: kind::tf32 reads fp32 truncated to tf32,
+        // bitwise equal to a pre-split hi copy (tools/probe_tf32_trunc.py); only lo is built
         if (!lo0) {
-          if (!s0.alloc(sizeof(float) * 2 * n, st)) return cuda_status(cudaGetLastError(), "scratch");
-          float* h0 = s0.as<float>();
-          blast_split_tf32(static_cast<const float*>(c_in.a0), h0, h0 + n, n, st);
-          c.a0 = h0;
-          lo0 = h0 + n;
+          if (!s0.alloc(sizeof(float) * n, st)) return cuda_status(cudaGetLastError(), "scratch");
+          blast_split_tf32(static_cast<const float*>(c_in.a0), nullptr, s0.as<float>(), n, st);
+          lo0 = s0.ptr;
         }
         if (c_in.sumacc && !lo1) {
-          if (!s1.alloc(sizeof(float) * 2 * n, st)) return cuda_status(cudaGetLastError(), "scratch");
-          float* h1 = s1.as<float>();
-          blast_split_tf32(static_cast<const float*>(c_in.a1), h1, h1 + n, n, st);
-          c.a1 = h1;
-          lo1 = h1 + n;
+          if (!s1.alloc(sizeof(float) * n, st)) return cuda_status(cudaGetLastError(), "scratch");
+          blast_split_tf32(static_cast<const float*>(c_in.a1), nullptr, s1.as<float>(), n, st);
+          lo1 = s1.ptr;
         }
         int r = dispatch_tc<float, 4, 3>(c, lo0, lo1, st);
         if (r >= 0) return r;
@@ -687,10 +685,12 @@ extern "C" int blast_mlp_forward(const void* x, int64_t m, const blast_bcsc_t* g
       down->tf32_fwd_lo) {
     // fp32: the gate+up epilogue writes G already split into tf32 hi / lo (the down
     // projection's 3xTF32 operands; G itself only when the caller asked for it)
+    // G itself is the hi operand (kind::tf32 truncates); only its lo part is extra
     Scratch ss;
-    if (!ss.alloc(2 * sizeof(float) * m * h, st)) return cuda_status(cudaGetLastError(), "scratch G");
-    float* g_hi = ss.as<float>();
-    float* g_lo = g_hi + m * h;
+    if (!ss.alloc((gated ? 1 : 2) * sizeof(float) * m * h, st))
+      return cuda_status(cudaGetLastError(), "scratch G");
+    float* g_lo = ss.as<float>();
+    float* g_hi = gated ? static_cast<float*>(gated) : g_lo + m * h;
     int r = gate_up_impl(x, m, gate, up, plan, gated, gate_pre, up_out, g_hi, g_lo, st);
     if (r) return r;
     EngineCall c;

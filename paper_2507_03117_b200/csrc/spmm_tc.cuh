@@ -60,8 +60,8 @@ struct SpmmParams {
   void* out0;  // Y | G | dA
   void* out1;  // saved gate_pre (fwd) | dB (bwd)
   void* out2;  // saved up_out (fwd)
-  void* out3;  // fp32 gated fwd: G's tf32 hi part (the down projection's A operand); optional
-  void* out4;  // fp32 gated fwd: G's lo part (with out3)
+  void* out3;  // fp32 gated fwd: G for the down projection's hi operand when out0 is null
+  void* out4;  // fp32 gated fwd: G's 3xTF32 lo part (G - tf32(G)), the down's lo operand
   const void* in0;  // bwd: gate_pre
   const void* in1;  // bwd: up_out
   int64_t ld_out;   // row stride (elements) of every out*/in* array
@@ -496,16 +496,15 @@ __device__ __forceinline__ void epilogue_chunk(const SpmmParams& p, float (&v0)[
         if (p.out0) store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out0) + off, g, valid, vec_ok);
         if constexpr (sizeof(OutT) == 4) {
           // fp32: G also leaves as its 3xTF32 hi / lo split, the down projection's operands
-          if (p.out3) {
+          if (p.out4) {  // lo part only: G itself (out0 / out3) is the hi operand
             float lo[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float v = g[i];
-              const float hi = isfinite(v) ? __uint_as_float(__float_as_uint(v) & 0xFFFFE000u) : v;
-              lo[i] = isfinite(v) ? __fsub_rn(v, hi) : 0.0f;
-              g[i] = hi;
+              lo[i] = isfinite(v) ? __fsub_rn(v, __uint_as_float(__float_as_uint(v) & 0xFFFFE000u)) : 0.0f;
             }
-            store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out3) + off, g, valid, vec_ok);
+            if (p.out3 && p.out3 != p.out0)
+              store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out3) + off, g, valid, vec_ok);
             store_chunk16<OutT>(reinterpret_cast<OutT*>(p.out4) + off, lo, valid, vec_ok);
           }
         }
