@@ -157,6 +157,21 @@ def _pinned_counts() -> torch.Tensor:
     return buf
 
 
+_MASK_SCRATCH = {}
+
+
+def _mask_scratch(gr: int, gc: int):
+    """Per (device, grid) fp64 norm grids [2, gr, gc] and device counts of generate_masks
+    (stream-ordered reuse: the refresh synchronises before returning)."""
+    key = (torch.cuda.current_device(), gr, gc)
+    buf = _MASK_SCRATCH.get(key)
+    if buf is None:
+        buf = (torch.empty(2, gr, gc, dtype=torch.float64, device=A.DEVICE),
+               torch.empty(2, dtype=torch.int64, device=A.DEVICE))
+        _MASK_SCRATCH[key] = buf
+    return buf
+
+
 def generate_masks(w_dense, g_dense, b: int, s: float, iteration: int = 0):
     """kept = top-k(|W| block norms), regrown = top-k(|G| block norms) minus kept
     (pruner.py:128-157). One library call (blast_generate_masks): a fused norm pass over W
@@ -173,14 +188,14 @@ def generate_masks(w_dense, g_dense, b: int, s: float, iteration: int = 0):
     gr, gc = -(-rows // b), -(-cols // b)
     total = gr * gc
     k = _k_of(s, total)
-    nw = torch.empty(gr, gc, dtype=torch.float64, device=A.DEVICE)
-    ng = torch.empty_like(nw)
-    kept = torch.empty(gr, gc, dtype=torch.uint8, device=A.DEVICE)
-    regrown = torch.empty_like(kept)
-    counts = torch.empty(2, dtype=torch.int64, device=A.DEVICE)
+    # norm grids and device counts are scratch, reused across refreshes of this grid shape;
+    # kept / regrown are returned, so they come from one fresh allocation
+    nrm, counts = _mask_scratch(gr, gc)
+    grids = torch.empty(2, gr, gc, dtype=torch.uint8, device=A.DEVICE)
+    kept, regrown = grids[0], grids[1]
     counts_h = _pinned_counts()
     L.check(L.load().blast_generate_masks(w.data_ptr(), _norm_code(w), g.data_ptr(), _norm_code(g),
-                                          rows, cols, b, k, nw.data_ptr(), ng.data_ptr(),
+                                          rows, cols, b, k, nrm[0].data_ptr(), nrm[1].data_ptr(),
                                           kept.data_ptr(), regrown.data_ptr(), counts.data_ptr(),
                                           counts_h.data_ptr(), L.stream()), "generate_masks")
     n_kept, n_regrown = int(counts_h[0]), int(counts_h[1])
