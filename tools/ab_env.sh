@@ -1,9 +1,7 @@
 #!/bin/bash
-# Same-box A/B of an environment switch on the cfg3 forward (tools/diag_time.py), alternating
-# runs: tools/ab_env.sh VAR VALUE_A VALUE_B [sparsity]
-var=$1; a=$2; b=$3; sp=${4:-0.9}
-for i in 1 2 3; do
-  for v in $a $b; do
-    echo -n "$var=$v: "; env $var=$v python tools/diag_time.py $sp
-  done
-done
+# Same-box A/B of an engine environment switch on the decode extra and the cfg3 bench:
+#   bash tools/ab_env.sh VAR        (runs VAR=1 and VAR=0 alternately, three rounds)
+v=$1
+for r in 1 2 3; do for x in 1 0; do
+  echo -n "$v=$x decode: "; env $v=$x python tools/extras_quick.py decode | python -c "import json,sys; print(round(json.loads(sys.stdin.read())['us'],2), 'us')"
+done; done
