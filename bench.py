@@ -205,13 +205,17 @@ def extra_train_step(bs, net, x, world, flush, tf_peak, iters):
     n = [w.cache.nnzb for w in net.matrices()]
     b = net.block
 
+    from paper_2507_03117_b200 import parallel
+
     def step():
         _, acts = bs.mlp_forward(x, net)
-        grads = bs.mlp_backward(dy, acts, net, grad_mode="active")
-        if world > 1:
-            for g in grads[1:]:
-                dist.all_reduce(g)
-                g.div_(world)
+        if world == 1:
+            return bs.mlp_backward(dy, acts, net, grad_mode="active")
+        # data-parallel: each weight gradient's NCCL all-reduce overlaps the rest of the
+        # backward (dWdown first); wait() orders the averaged gradients on this stream
+        red = parallel.OverlappedGradAllReduce()
+        grads = bs.mlp_backward(dy, acts, net, grad_mode="active", grad_ready=red)
+        red.wait()
         return grads
 
     ms = _ev_median(step, iters, flush)
@@ -224,7 +228,8 @@ def extra_train_step(bs, net, x, world, flush, tf_peak, iters):
     return {"ms_per_step": ms, "tokens_per_s": world * m / (ms * 1e-3),
             "flops_per_step": flops, "achieved_tflops": ach, "frac": ach / tf_peak,
             "grad_mode": "active (stored blocks)",
-            "dp_allreduce": "NCCL all-reduce of the stored-block gradients" if world > 1 else None,
+            "dp_allreduce": ("NCCL all-reduce of the stored-block gradients, overlapped with the "
+                             "backward (parallel.OverlappedGradAllReduce)") if world > 1 else None,
             "path": "mlp_forward(save_activations=True) + mlp_backward(grad_mode='active')"}
 
 

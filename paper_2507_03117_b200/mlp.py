@@ -243,13 +243,19 @@ def _wgrad(a: torch.Tensor, d: torch.Tensor, rows: int, cols: int, w: BlockSpars
     return out
 
 
-def mlp_backward(dy, acts: MlpActivations, mlp: SparseMlp, grad_mode: str = "full"):
+def mlp_backward(dy, acts: MlpActivations, mlp: SparseMlp, grad_mode: str = "full",
+                 grad_ready=None):
     """Exact gradients at the saved activations (mlp.py:118-143).
 
     Returns (dX, dWgate, dWup, dWdown). ``grad_mode="full"`` gives the
     reference's dense float32 weight gradients over the whole grid (needed for
     regrowth and the global-norm clip); ``grad_mode="active"`` gives float32
     [nnzb, b, b] gradients of the stored blocks only, in each cache's BCSC order.
+
+    ``grad_ready(i, grad)`` (optional, device path) is called as soon as weight gradient i
+    (1 gate, 2 up, 3 down: its index in the returned tuple) has been enqueued on the current
+    stream, so a data-parallel all-reduce can overlap the rest of the backward
+    (parallel.OverlappedGradAllReduce). dWdown needs only G and dY and is computed first.
     """
     if acts is None:
         raise ValueError("missing saved activations: run mlp_forward first")
@@ -266,16 +272,20 @@ def mlp_backward(dy, acts: MlpActivations, mlp: SparseMlp, grad_mode: str = "ful
     dx = torch.empty(m, e, dtype=dt, device=A.DEVICE)
     da = torch.empty(m, h, dtype=dt, device=A.DEVICE)
     db = torch.empty(m, h, dtype=dt, device=A.DEVICE)
+    full = grad_mode == "full"
+    ready = grad_ready if grad_ready is not None else (lambda i, t: None)
+    d_down = _wgrad(g, dyt, h, e, mlp.down.cache, full)
+    ready(3, d_down)
     if m:
         dg, du, dd = (mat.cache.desc() for mat in mlp.matrices())
         plan = mlp.plan()
         L.check(L.load().blast_mlp_backward_dgrad(
             dyt.data_ptr(), m, a.data_ptr(), b.data_ptr(), C.byref(dg), C.byref(du), C.byref(dd),
             C.byref(plan), dx.data_ptr(), da.data_ptr(), db.data_ptr(), L.stream()), "mlp_backward")
-    full = grad_mode == "full"
     d_gate = _wgrad(x, da, e, h, mlp.gate.cache, full)
+    ready(1, d_gate)
     d_up = _wgrad(x, db, e, h, mlp.up.cache, full)
-    d_down = _wgrad(g, dyt, h, e, mlp.down.cache, full)
+    ready(2, d_up)
     if host:
         return tuple(A.to_host(t) for t in (dx, d_gate, d_up, d_down))
     return dx, d_gate, d_up, d_down

@@ -129,6 +129,45 @@ def allreduce_mean_(tensors, group=None) -> None:
         t.div_(world)
 
 
+class OverlappedGradAllReduce:
+    """Data-parallel gradient averaging overlapped with the backward:
+    pass as ``mlp_backward(..., grad_ready=reducer)``. Each weight gradient's all-reduce is
+    enqueued on a side stream as soon as the gradient is ready (dWdown first, while the data
+    gradient and the other weight gradients still run); ``wait()`` makes the current stream
+    wait for all of them and divides by the world size. CPU tensors (gloo) reduce
+    synchronously, with the same result."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.pending = []
+        self.stream = None
+
+    def __call__(self, index: int, grad: torch.Tensor) -> None:
+        if self.world == 1:
+            return
+        if not grad.is_cuda or _host_staged(self.group):
+            _all_reduce_sum_(grad, self.group)
+            self.pending.append((None, grad))
+            return
+        if self.stream is None:
+            self.stream = torch.cuda.Stream()
+        ready = torch.cuda.Event()
+        ready.record()
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(ready)
+            grad.record_stream(self.stream)
+            work = dist.all_reduce(grad, group=self.group, async_op=True)
+        self.pending.append((work, grad))
+
+    def wait(self) -> None:
+        for work, grad in self.pending:
+            if work is not None:
+                work.wait()  # the current stream waits for the collective
+            grad.div_(self.world)
+        self.pending.clear()
+
+
 @dataclass
 class TPShardedMlp:
     """One rank's shard of a gated sparse MLP: gate/up column shards, down row shard.

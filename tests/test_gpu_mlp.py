@@ -280,3 +280,25 @@ def test_graphed_forward_equals_eager(m):
         assert torch.equal(y_graph, y_eager)
     with pytest.raises(ValueError, match="captured for"):
         fwd(torch.zeros(m + 1, 512, device="cuda", dtype=torch.bfloat16))
+
+
+def test_backward_grad_ready_hook_order_and_bits():
+    """mlp_backward(grad_ready=...) reports dWdown first (it needs only G and dY), then dWgate
+    and dWup, and the gradients are bitwise those of the call without a hook (the hook only
+    lets a data-parallel all-reduce overlap the rest of the backward)."""
+    import bench
+    ws = bench.make_weights(512, 1024, 64, 0.75, 3)
+    net = bs.SparseMlp.from_caches(*[bs.from_host(w, torch.bfloat16) for w in ws])
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(384, 512, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(384, 512, device="cuda", generator=g).bfloat16()
+    _, acts = bs.mlp_forward(x, net)
+    ref = bs.mlp_backward(dy, acts, net, grad_mode="active")
+    seen = []
+    got = bs.mlp_backward(dy, acts, net, grad_mode="active",
+                          grad_ready=lambda i, t: seen.append((i, t.data_ptr())))
+    torch.cuda.synchronize()
+    assert [i for i, _ in seen] == [3, 1, 2]
+    assert [p for _, p in seen] == [got[3].data_ptr(), got[1].data_ptr(), got[2].data_ptr()]
+    for r, o in zip(ref, got):
+        assert torch.equal(r, o)

@@ -163,6 +163,24 @@ def test_dp_gradient_average():
         np.testing.assert_allclose(out[1], np.arange(5) * 1.5)
 
 
+def _dp_overlapped(rank, world):
+    # the backward's hook order (dWdown first), then wait(): same averages as allreduce_mean_
+    red = parallel.OverlappedGradAllReduce()
+    t = [torch.full((3, 4), float(rank + 1)), torch.arange(5, dtype=torch.float32) * (rank + 1),
+         torch.full((2, 2), 10.0 * (rank + 1))]
+    for i in (2, 0, 1):
+        red(i + 1, t[i])
+    red.wait()
+    return [x.numpy() for x in t]
+
+
+def test_dp_overlapped_gradient_average():
+    for out in run_world(_dp_overlapped):
+        np.testing.assert_array_equal(out[0], np.full((3, 4), 1.5))
+        np.testing.assert_allclose(out[1], np.arange(5) * 1.5)
+        np.testing.assert_array_equal(out[2], np.full((2, 2), 15.0))
+
+
 def test_shard_ranges_and_roofline_helpers():
     assert parallel.shard_range(448, 3, 8) == (168, 224)
     with pytest.raises(ValueError):
