@@ -938,6 +938,12 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     // those of odd steps, so the per-step issue latency is overlapped. One elected
     // lane issues each copy.
     const uint64_t pol_w = policy_evict_last();
+    // sequential gate+up / dX panels: L2 evict_last like the weights (X and W stay resident
+    // against the streamed G stores; cfg3 0.3382-0.3390 vs 0.3396-0.3402 ms, tools/ab_lib.sh)
+#ifndef BLAST_A_POLICY
+#define BLAST_A_POLICY 2
+#endif
+    const uint64_t pol_a = BLAST_A_POLICY == 2 ? policy_evict_last() : policy_evict_normal();
     const uint32_t mine = warp == 0 ? 0u : 1u;
     uint32_t stage = 0, phase = 0, n = 0;
     constexpr bool kMergeP = (NMAT == 2) && !SUMACC && !B_KMAJOR && (2 * B <= 256) &&
@@ -993,10 +999,10 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
                   for (int c = 0; c < C::NCOPY; ++c)
 #pragma unroll
                     for (int at = 0; at < C::KPS; ++at)
-                      tma_load_2d(sbase + c * C::A_TILE + at * C::TROWS * C::SW,
-                                  c == 0 ? (a1 ? &mapA1 : &mapA0) : (a1 ? &mapA1lo : &mapA0lo),
-                                  &full[stage], st.x * B + (C::SK ? sa : at) * C::SWE,
-                                  t * C::TROWS);
+                      tma_load_2d_hint(sbase + c * C::A_TILE + at * C::TROWS * C::SW,
+                                       c == 0 ? (a1 ? &mapA1 : &mapA0) : (a1 ? &mapA1lo : &mapA0lo),
+                                       &full[stage], st.x * B + (C::SK ? sa : at) * C::SWE,
+                                       t * C::TROWS, pol_a);
 #pragma unroll
                   for (int c = 0; c < C::NCOPY; ++c)
 #pragma unroll
