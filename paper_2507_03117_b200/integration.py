@@ -19,7 +19,7 @@ from __future__ import annotations
 import torch
 from torch import nn
 
-from . import bcsc
+from . import bcsc, ops
 from .bcsc import BlockMask, BlockSparseMatrix
 from .kernels import bspmm_act_save, bspmm_fused, bspmm_rt, bspmm_rt_act_grad, column_sums
 from .mlp import SparseMlp, _wgrad, mlp_backward, mlp_forward
@@ -42,19 +42,21 @@ def _bcsc_param(w: BlockSparseMatrix) -> nn.Parameter:
 
 
 class _GatedFn(torch.autograd.Function):
+    # through the dispatcher-visible ops (ops.py): traceable by torch.compile / export
     @staticmethod
-    def forward(ctx, x2d, net: SparseMlp, vg, vu, vd):
-        y, acts = mlp_forward(x2d, net, save_activations=True)
-        ctx.net = net
-        ctx.acts = acts
+    def forward(ctx, x2d, handle: int, vg, vu, vd):
+        y, a, b, g = torch.ops.blast.mlp_forward_train(x2d, handle)
+        ctx.save_for_backward(x2d, a, b, g)
+        ctx.handle = handle
+        ctx.dtypes = (vg.dtype, vu.dtype, vd.dtype)
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        dx, dwg, dwu, dwd = mlp_backward(dy.contiguous(), ctx.acts, ctx.net, grad_mode="active")
-        net = ctx.net
-        return (dx, None, dwg.to(net.gate.cache.values.dtype), dwu.to(net.up.cache.values.dtype),
-                dwd.to(net.down.cache.values.dtype))
+        x2d, a, b, g = ctx.saved_tensors
+        dx, dwg, dwu, dwd = torch.ops.blast.mlp_backward(dy.contiguous(), x2d, a, b, g, ctx.handle)
+        tg, tu, td = ctx.dtypes
+        return dx, None, dwg.to(tg), dwu.to(tu), dwd.to(td)
 
 
 class SparseGatedMLP(nn.Module):
@@ -63,6 +65,7 @@ class SparseGatedMLP(nn.Module):
     def __init__(self, gate: BlockSparseMatrix, up: BlockSparseMatrix, down: BlockSparseMatrix):
         super().__init__()
         self.net = SparseMlp.from_caches(gate, up, down)
+        self.handle = ops.register(self.net)
         self.gate_values = _bcsc_param(gate)
         self.up_values = _bcsc_param(up)
         self.down_values = _bcsc_param(down)
@@ -80,9 +83,9 @@ class SparseGatedMLP(nn.Module):
         shape = x.shape
         x2d = x.reshape(-1, shape[-1]).to(self.gate_values.dtype).contiguous()
         if torch.is_grad_enabled() and (x.requires_grad or self.gate_values.requires_grad):
-            y = _GatedFn.apply(x2d, self.net, self.gate_values, self.up_values, self.down_values)
+            y = _GatedFn.apply(x2d, self.handle, self.gate_values, self.up_values, self.down_values)
         else:
-            y, _ = mlp_forward(x2d, self.net, save_activations=False)
+            y = torch.ops.blast.mlp_forward(x2d, self.handle)
         return y.reshape(*shape[:-1], y.shape[-1]).to(x.dtype)
 
 
