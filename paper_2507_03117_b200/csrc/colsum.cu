@@ -26,23 +26,38 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
 #pragma unroll
   for (int i = 0; i < V; ++i) acc[i] = 0.0f;
   const bool vec = (c0 + V <= n) && (n % V == 0);
-  for (int64_t r = r0 + g; r < r1; r += kCsRowGroups) {
-    const T* row = x + r * n;
-    if (vec) {
-      const uint4 w = __ldcs(reinterpret_cast<const uint4*>(row + c0));
-      if constexpr (sizeof(T) == 2) {
-        const uint32_t h[4] = {w.x, w.y, w.z, w.w};
+  // U rows' loads in flight per thread, added in row order (same sums as one row at a time)
+  constexpr int U = 8;
+  auto add = [&](const uint4& w) {
+    if constexpr (sizeof(T) == 2) {
+      const uint32_t h[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h[i]));
-          acc[2 * i] += f.x;
-          acc[2 * i + 1] += f.y;
-        }
-      } else {
-        acc[0] += __uint_as_float(w.x); acc[1] += __uint_as_float(w.y);
-        acc[2] += __uint_as_float(w.z); acc[3] += __uint_as_float(w.w);
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h[i]));
+        acc[2 * i] += f.x;
+        acc[2 * i + 1] += f.y;
       }
     } else {
+      acc[0] += __uint_as_float(w.x); acc[1] += __uint_as_float(w.y);
+      acc[2] += __uint_as_float(w.z); acc[3] += __uint_as_float(w.w);
+    }
+  };
+  if (vec) {
+    for (int64_t rb = r0 + g; rb < r1; rb += static_cast<int64_t>(kCsRowGroups) * U) {
+      uint4 w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = rb + static_cast<int64_t>(u) * kCsRowGroups;
+        if (r < r1) w[u] = __ldcs(reinterpret_cast<const uint4*>(x + r * n + c0));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (rb + static_cast<int64_t>(u) * kCsRowGroups < r1) add(w[u]);
+    }
+  }
+  for (int64_t r = r0 + g; !vec && r < r1; r += kCsRowGroups) {
+    const T* row = x + r * n;
+    {
 #pragma unroll
       for (int i = 0; i < V; ++i)
         if (c0 + i < n) {
@@ -70,7 +85,15 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int64_t spli
   const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (c >= n) return;
   float s = 0.0f;
-  for (int64_t k = 0; k < splits; ++k) s += part[k * n + c];  // split order
+  int64_t k = 0;
+  for (; k + 8 <= splits; k += 8) {  // 8 loads in flight, added in split order
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = part[(k + u) * n + c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; k < splits; ++k) s += part[k * n + c];  // split order
   out[c] = s;
 }
 
