@@ -34,3 +34,17 @@ def test_world_size_must_match_gpus():
                             capture_output=True, text=True, timeout=120, cwd=ROOT,
                             env={**__import__("os").environ, "WORLD_SIZE": "1", "RANK": "0"})
     assert env_ok.returncode != 0 and "WORLD_SIZE" in (env_ok.stderr + env_ok.stdout)
+
+
+def test_l2_feed_roof_counts_panel_and_block_bytes():
+    """The bench line's L2-feed roof: every stored block reads its 256-token activation panel
+    and the block itself (cfg3: 5.64 GB per 8192-token step, the ncu xbar2l1tex bytes)."""
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+    ws = bench.make_weights(4096, 14336, 64, 0.9, 0)
+    r = bench.l2_feed_roof(ws, 8192, 0.34)
+    nnzb = sum(len(w.block_row_idx) for w in ws)
+    assert nnzb == 3 * 1434
+    assert r["bytes_per_step"] == nnzb * 32 * (256 * 64 * 2 + 64 * 64 * 2) == 5638717440
+    assert abs(r["ms_at_peak"] - 5638717440 / 17.96e12 * 1e3) < 1e-9
+    assert abs(r["frac"] - r["ms_at_peak"] / 0.34) < 1e-12
