@@ -294,7 +294,7 @@ constexpr bool staged_fits() {
   constexpr int na = SUM ? NMAT : 1;
   constexpr int stage = na * a_tile + NMAT * b_tile;
   constexpr int nout = IN_ST == 2 ? 2 : 1;
-  constexpr int staging = (2 * nout + 2 * IN_ST * TM) * ((128 * B * 2 + 1023) / 1024 * 1024);
+  constexpr int staging = (2 * nout + 2 * IN_ST) * ((128 * B * 2 + 1023) / 1024 * 1024);
   return (232448 - 1024 - 512 - staging) / stage >= 3;
 }
 // gate+up stage layout (TcCfg SPLIT) for the 256-token staged product:
@@ -329,6 +329,15 @@ static bool wide_tiles() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("BLAST_WIDE_TILES");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+// 256-token items for the two-input gating backward (EPI_GATED_BWD2); BLAST_WIDE_BWD2=0 disables.
+static bool wide_bwd2() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_WIDE_BWD2");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -391,7 +400,11 @@ static int dispatch_b(const EngineCall& c, const void* a0lo, const void* a1lo, c
       if constexpr (tc_fits<B, ELT, NPASS, 1, false>())
         return launch_tc<B, ELT, NPASS, 1, false, true, EPI_STORE, OutT>(c, a0lo, a1lo, st);
     } else if (c.nmat == 1 && c.epi == EPI_GATED_BWD && c.in1) {
-      // gating backward (dA, dB): a, b in and dA, dB out through staged TMA tiles
+      // gating backward (dA, dB): a, b in and dA, dB out through staged TMA tiles; 256-token
+      // items (the weight blocks read once per 256 tokens) with 3 x 40 KB stages
+      if constexpr (B == 64 && ELT == 2 && NPASS == 1)
+        if (use_staged<B, ELT, NPASS, 1, false>(c) && c.m >= 256 && wide_tiles() && wide_bwd2())
+          return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD2, OutT, SO, 2>(c, a0lo, a1lo, st);
       if constexpr (staged_fits<B, ELT, NPASS, 1, false, 1, 2>())
         if (use_staged<B, ELT, NPASS, 1, false>(c))
           return launch_tc<B, ELT, NPASS, 1, false, true, EPI_GATED_BWD2, OutT, SO>(c, a0lo, a1lo, st);

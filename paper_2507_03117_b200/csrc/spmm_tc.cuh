@@ -230,7 +230,8 @@ struct TcCfg {
   static constexpr int OUT_NATOM = OUT_ELT ? OUT_ROWB / OUT_SW : 0;
   static constexpr int OUT_TILE = OUT_ELT ? round1k(BM * OUT_ROWB) : 0;
   static constexpr int NOUT = NOUT_;                                // staged outputs per tile
-  static constexpr int IN_STAGING = IN_ST * 2 * TM * OUT_TILE;      // [2 bufs][IN_ST][TM] tiles
+  // staged inputs per 128-row half, double-buffered across halves: [2 bufs][IN_ST] tiles
+  static constexpr int IN_STAGING = IN_ST * 2 * OUT_TILE;
   static constexpr int STAGING = OUT_BUFS * NOUT * OUT_TILE + IN_STAGING;
   // 227 KB opt-in maximum minus barriers, alignment slack and the output staging
   static constexpr int SMEM_BUDGET = OUT_ELT ? 232448 - 1024 - 512 - STAGING : 200 * 1024;
@@ -884,7 +885,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   // producer before its expect_tx arrive (release), read after the full wait (acquire)
   uint32_t* stage_meta = tmem_slot + 4;
   uint64_t* in_full = reinterpret_cast<uint64_t*>(stage_meta + 8);  // [2] staged in0 landed
-  uint8_t* in_staging = staging + C::OUT_BUFS * C::NOUT * C::OUT_TILE;  // [2][IN_ST][TM][OUT_TILE]
+  uint8_t* in_staging = staging + C::OUT_BUFS * C::NOUT * C::OUT_TILE;  // [2][IN_ST][OUT_TILE]
 
   const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);
   const uint32_t lane = lane_id();
@@ -1352,39 +1353,43 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
     const uint64_t pol_out = policy_evict_first();
     uint32_t it = 0;
     const bool vec_ok = (p.ld_out * static_cast<int64_t>(sizeof(OutT))) % 16 == 0;
+    [[maybe_unused]] auto load_in = [&](int itm, int h, uint32_t buf) {
+      const int tt = tile_of(itm), jj = itm % p.n_lines;
+      mbar_expect_tx(&in_full[buf], IN_ST * C::BM * C::OUT_ROWB);
+#pragma unroll
+      for (int i = 0; i < IN_ST; ++i)
+#pragma unroll
+        for (int a = 0; a < C::OUT_NATOM; ++a)
+          tma_load_2d(in_staging + (buf * IN_ST + i) * C::OUT_TILE + a * (C::BM * C::OUT_SW),
+                      i == 0 ? &mapI : &mapI1, &in_full[buf], jj * B + a * (C::OUT_SW / OUT_ELT),
+                      tt * C::TROWS + h * C::BM);
+    };
     for (int k = 0, item = item_at(p, 0, n_items); item < n_items;
          item = item_at(p, ++k, n_items), ++it) {
       const int t = tile_of(item);
       const int j = item % p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
       const int flags = __ldg(&p.line_flags[j]);
-      if constexpr (IN_ST) {
-        // in0 tiles one item ahead: this item's were requested during the previous item (or
-        // here for the first); the buffer of the next one was last read by the previous item,
-        // whose reads all precede its final barrier
-        auto load_in = [&](int itm, uint32_t buf) {
-          const int tt = tile_of(itm), jj = itm % p.n_lines;
-          mbar_expect_tx(&in_full[buf], IN_ST * TM * C::BM * C::OUT_ROWB);
-#pragma unroll
-          for (int i = 0; i < IN_ST; ++i)
-#pragma unroll
-            for (int h = 0; h < TM; ++h)
-#pragma unroll
-              for (int a = 0; a < C::OUT_NATOM; ++a)
-                tma_load_2d(in_staging + ((buf * IN_ST + i) * TM + h) * C::OUT_TILE +
-                                a * (C::BM * C::OUT_SW),
-                            i == 0 ? &mapI : &mapI1, &in_full[buf],
-                            jj * B + a * (C::OUT_SW / OUT_ELT), tt * C::TROWS + h * C::BM);
-        };
-        if (etid == 0) {
-          if (it == 0) load_in(item, 0);
+      // in0 (and in1) tiles per 128-row half, one half ahead (the half after `seq` goes to
+      // buffer (seq + 1) & 1, last read by half seq - 1, whose reads all precede its final
+      // barrier): the first half of the first item and the half after this item's first are
+      // requested before the accumulator wait, later ones at the top of the half loop.
+      [[maybe_unused]] auto load_after = [&](uint32_t seq, int h) {
+        if (h + 1 < TM) {
+          load_in(item, h + 1, (seq + 1) & 1);
+        } else {
           const int nxt = item_at(p, k + 1, n_items);
-          if (nxt < n_items) load_in(nxt, (it + 1) & 1);
+          if (nxt < n_items) load_in(nxt, 0, (seq + 1) & 1);
+        }
+      };
+      if constexpr (IN_ST) {
+        if (etid == 0) {
+          if (it == 0) load_in(item, 0, 0u);
+          load_after(it * TM, 0);
         }
       }
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
       tc_fence_after();
-      if constexpr (IN_ST) mbar_wait(&in_full[it & 1], (it >> 1) & 1);
       if (kDiagSwitches && (p.skip_epilogue & 1)) {  // diagnosis: release the accumulator unread
         tc_fence_before();
         __syncwarp();
@@ -1404,14 +1409,19 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       }
 #pragma unroll
       for (int h = 0; h < TM; ++h) {
+        const uint32_t seq = it * TM + h;  // half sequence number of this CTA
+        if constexpr (IN_ST) {
+          if (etid == 0 && h > 0) load_after(seq, h);
+          mbar_wait(&in_full[seq & 1], (seq >> 1) & 1);
+        }
         uint8_t* stg = staging + ((it * TM + h) % C::OUT_BUFS) * C::NOUT * C::OUT_TILE;
         const uint32_t tacc =
             tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
         const int row0 = t * C::TROWS + h * C::BM;
         epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS, C::ACC_W>(
             p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
-            IN_ST ? in_staging + ((it & 1) * IN_ST * TM + h) * C::OUT_TILE : nullptr,
-            C::OUT_TILE, TM * C::OUT_TILE);
+            IN_ST ? in_staging + (seq & 1) * IN_ST * C::OUT_TILE : nullptr,
+            C::OUT_TILE, C::OUT_TILE);
         if (h == TM - 1) {  // every TMEM read of this accumulator stage is done
           tc_fence_before();
           __syncwarp();
