@@ -57,26 +57,26 @@ static unsigned long long* dbg_buffer() {
   if (on < 0) {
     const char* e = getenv("BLAST_DEBUG_COUNTERS");
     on = (e && e[0] == '1') ? 1 : 0;
-    // [0, 8): summed role counters; [8, 8 + 2 * 1024): per-CTA start / end globaltimer
-    if (on && cudaMalloc(&buf, (8 + 2048) * sizeof(unsigned long long)) != cudaSuccess) on = 0;
+    // [0, kDbgSlots): summed role counters; then 2 * 1024 per-CTA start / end globaltimer
+    if (on && cudaMalloc(&buf, (kDbgSlots + 2048) * sizeof(unsigned long long)) != cudaSuccess) on = 0;
   }
   return on ? buf : nullptr;
 }
 static void dbg_begin(cudaStream_t st) {
-  if (auto* b = dbg_buffer()) cudaMemsetAsync(b, 0, (8 + 2048) * sizeof(unsigned long long), st);
+  if (auto* b = dbg_buffer()) cudaMemsetAsync(b, 0, (kDbgSlots + 2048) * sizeof(unsigned long long), st);
 }
 static void dbg_end(const char* name, cudaStream_t st, int ctas) {
   auto* b = dbg_buffer();
   if (!b) return;
-  static unsigned long long h[8 + 2048];
+  static unsigned long long h[kDbgSlots + 2048];
   cudaMemcpyAsync(h, b, sizeof(h), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   const double n = ctas > 0 ? ctas : 1;
-  if (ctas > 0 && ctas <= 1024 && h[8] != 0) {  // per-CTA spans (globaltimer, ns)
+  if (ctas > 0 && ctas <= 1024 && h[kDbgSlots] != 0) {  // per-CTA spans (globaltimer, ns)
     unsigned long long t0 = ~0ull, t1 = 0, e0 = ~0ull;
     double sum = 0, mx = 0;
     for (int i = 0; i < ctas; ++i) {
-      const unsigned long long a = h[8 + 2 * i], z = h[8 + 2 * i + 1];
+      const unsigned long long a = h[kDbgSlots + 2 * i], z = h[kDbgSlots + 2 * i + 1];
       t0 = std::min(t0, a);
       t1 = std::max(t1, z);
       e0 = std::min(e0, z);
@@ -84,22 +84,23 @@ static void dbg_end(const char* name, cudaStream_t st, int ctas) {
       mx = std::max(mx, double(z - a));
     }
     unsigned long long s1 = 0;
-    for (int i = 0; i < ctas; ++i) s1 = std::max(s1, h[8 + 2 * i]);
+    for (int i = 0; i < ctas; ++i) s1 = std::max(s1, h[kDbgSlots + 2 * i]);
     fprintf(stderr,
             "[blast dbg] %s span %.1f us: CTA starts within %.1f us, ends within %.1f us, "
             "per-CTA avg %.1f max %.1f us\n",
             name, (t1 - t0) * 1e-3, (s1 - t0) * 1e-3, (t1 - e0) * 1e-3, sum / ctas * 1e-3, mx * 1e-3);
     if (getenv("BLAST_DEBUG_CTAS")) {
       fprintf(stderr, "[blast dbg] per-CTA end (us after first start):");
-      for (int i = 0; i < ctas; ++i) fprintf(stderr, " %.1f", (h[8 + 2 * i + 1] - t0) * 1e-3);
+      for (int i = 0; i < ctas; ++i) fprintf(stderr, " %.1f", (h[kDbgSlots + 2 * i + 1] - t0) * 1e-3);
       fprintf(stderr, "\n");
     }
   }
   fprintf(stderr,
           "[blast dbg] %s ctas=%d per-CTA cycles: prod.wait_empty=%.0f cta.total=%.0f "
           "mma.wait_full=%.0f mma.wait_acc=%.0f mma.loop=%.0f epi.wait_acc=%.0f mma.issue=%.0f "
-          "mma.steps=%.0f\n",
-          name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n);
+          "mma.steps=%.0f epi.wait_in=%.0f epi.tile=%.0f\n",
+          name, ctas, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n, h[6] / n, h[7] / n,
+          h[8] / n, h[9] / n);
 }
 
 static SpmmParams make_params(const EngineCall& c) {

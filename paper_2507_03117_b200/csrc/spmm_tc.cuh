@@ -115,8 +115,11 @@ __device__ __forceinline__ void add_bias16(float (&v)[16], const float* bias, in
 // 0 producer waits on empty, 1 producer waits on resident-weight release,
 // 2 MMA waits on full, 3 MMA waits on accumulator release, 4 MMA waits on
 // resident weights, 5 epilogue waits on accumulator, 6 epilogue busy, 7 MMA steps.
+// diagnosis counters (BLAST_WAIT_COUNTERS builds): kDbgSlots summed role counters, then the
+// per-CTA start / end globaltimer pairs
+constexpr int kDbgSlots = 10;
 struct WaitClock {
-  unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long acc[kDbgSlots] = {};
   __device__ __forceinline__ void wait(int slot, uint64_t* bar, uint32_t parity, bool on) {
     if (!on) {
       mbar_wait(bar, parity);
@@ -128,7 +131,7 @@ struct WaitClock {
   }
   __device__ __forceinline__ void flush(unsigned long long* dbg) {
     if (!dbg || lane_id() != 0) return;
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < kDbgSlots; ++i)
       if (acc[i]) atomicAdd(&dbg[i], acc[i]);
   }
 };
@@ -600,14 +603,52 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
                                                  uint32_t q, uint32_t lane, uint32_t etid,
                                                  bool vec_ok, const uint8_t* in_stg = nullptr,
                                                  int out1_off = 0, int in1_off = 0) {
-  if constexpr (OUT_SW > 0) {
-    if (etid == 0) bulk_wait_group_read<NBUF - 1>();
-    named_bar_sync(1, kEpiWarpsT * 32);
-  }
   const int trow = static_cast<int>(q * 32 + lane);
   const int row = row0 + trow;
   const bool row_ok = row < p.m;
   constexpr int NCH = B / 16;
+  if constexpr (EPI == EPI_GATED_BWD2 && NCH <= 4 && ACC_W == B) {
+    // Gating backward: accumulator, staged inputs and the math for all of this thread's
+    // chunks (c = half, half + 2) first, so they overlap the previous tile's TMA store still
+    // reading the (single) output staging buffer; only the staging writes wait for it.
+    const bool acc0_init = (flags & 1) != 0;
+    uint32_t r[2][16];
+    float da[2][16], db[2][16];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (half + 2 * k < NCH) tmem_ld16_nowait(tacc + (half + 2 * k) * 16, r[k]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int c = half + 2 * k;
+      if (c >= NCH) break;
+      float a[16], b[16];
+      unstage_chunk16<OutT, OUT_SW>(in_stg, trow, c * 16, a);
+      unstage_chunk16<OutT, OUT_SW>(in_stg + in1_off, trow, c * 16, b);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float g = acc0_init ? __uint_as_float(r[k][i]) : 0.0f;
+        if constexpr (sizeof(OutT) == 2)
+          gated_bwd_fast(g, a[i], b[i], da[k][i], db[k][i]);
+        else
+          gated_bwd(g, a[i], b[i], da[k][i], db[k][i]);
+      }
+    }
+    if (etid == 0) bulk_wait_group_read<NBUF - 1>();
+    named_bar_sync(1, kEpiWarpsT * 32);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int c = half + 2 * k;
+      if (c >= NCH) break;
+      stage_chunk16<OutT, OUT_SW>(stg, trow, c * 16, da[k]);
+      stage_chunk16<OutT, OUT_SW>(stg + out1_off, trow, c * 16, db[k]);
+    }
+    return;
+  }
+  if constexpr (OUT_SW > 0) {
+    if (etid == 0) bulk_wait_group_read<NBUF - 1>();
+    named_bar_sync(1, kEpiWarpsT * 32);
+  }
   constexpr bool kTwoAcc = EPI == EPI_GATED_FWD || EPI == EPI_GATED_FWD_SAVE;
   // ACC_W = 2B: every accumulator is a pair (hi*hi in columns [0, B), the 3xTF32 cross terms
   // in [B, 2B)) summed here
@@ -871,7 +912,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
   static_assert(OUT_ELT == 0 || OUT_ELT == static_cast<int>(sizeof(OutT)), "staged output type");
 #ifdef BLAST_WAIT_COUNTERS
   const long long t_kernel0 = clock64();
-  if (p.dbg && threadIdx.x == 0) p.dbg[8 + 2 * blockIdx.x] = globaltimer_ns();
+  if (p.dbg && threadIdx.x == 0) p.dbg[kDbgSlots + 2 * blockIdx.x] = globaltimer_ns();
 #endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1412,12 +1453,13 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         const uint32_t seq = it * TM + h;  // half sequence number of this CTA
         if constexpr (IN_ST) {
           if (etid == 0 && h > 0) load_after(seq, h);
-          mbar_wait(&in_full[seq & 1], (seq >> 1) & 1);
+          wc.wait(8, &in_full[seq & 1], (seq >> 1) & 1, dbg_on);
         }
         uint8_t* stg = staging + ((it * TM + h) % C::OUT_BUFS) * C::NOUT * C::OUT_TILE;
         const uint32_t tacc =
             tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
         const int row0 = t * C::TROWS + h * C::BM;
+        const long long te0 = dbg_on ? clock64() : 0;
         epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS, C::ACC_W>(
             p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
             IN_ST ? in_staging + (seq & 1) * IN_ST * C::OUT_TILE : nullptr,
@@ -1430,6 +1472,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT, C::NOUT>(&mapO, &mapO1, &mapO2, stg,
                                                                   C::OUT_TILE, row0, j * B, etid,
                                                                   pol_out);
+        if (dbg_on) wc.acc[9] += static_cast<unsigned long long>(clock64() - te0);
       }
     }
     if constexpr (OUT_ELT > 0) {
@@ -1440,7 +1483,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 #ifdef BLAST_WAIT_COUNTERS
   if (warp == 4 && dbg_on) {
     wc.acc[1] += static_cast<unsigned long long>(clock64() - t_kernel0);
-    if (lane == 0) p.dbg[8 + 2 * blockIdx.x + 1] = globaltimer_ns();
+    if (lane == 0) p.dbg[kDbgSlots + 2 * blockIdx.x + 1] = globaltimer_ns();
   }
 #endif
   if (warp <= 2 || warp == 4) wc.flush(p.dbg);
