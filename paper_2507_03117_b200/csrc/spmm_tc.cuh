@@ -597,17 +597,27 @@ constexpr int kEpiWarpsT = 8;  // epilogue warps of both engines (named barrier 
 // `tacc` is the TMEM address of accumulator 0 for this warp's lane quarter; row0 / col0 are
 // the tile's first output row / column. Staging buffers alternate per tile (`stg`); the TMA
 // store issued from a buffer two tiles ago must have finished reading it.
-template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW, int NBUF = 2, int ACC_W = B>
+struct EpiNoOp {
+  __device__ __forceinline__ void operator()() const {}
+};
+// Gating backward with the reordered tile (epi_tile_compute): every staged-input read of the
+// tile precedes its staging barrier, after which `after_inputs` may refill the input buffer.
+template <int B, int EPI, int ACC_W>
+constexpr bool early_inputs() { return EPI == EPI_GATED_BWD2 && B / 16 <= 4 && ACC_W == B; }
+
+template <int B, int EPI, typename OutT, bool SUMACC, int OUT_SW, int NBUF = 2, int ACC_W = B,
+          typename AfterInputs = EpiNoOp>
 __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t tacc, int row0,
                                                  int col0, int flags, uint8_t* stg, int half,
                                                  uint32_t q, uint32_t lane, uint32_t etid,
                                                  bool vec_ok, const uint8_t* in_stg = nullptr,
-                                                 int out1_off = 0, int in1_off = 0) {
+                                                 int out1_off = 0, int in1_off = 0,
+                                                 AfterInputs after_inputs = AfterInputs{}) {
   const int trow = static_cast<int>(q * 32 + lane);
   const int row = row0 + trow;
   const bool row_ok = row < p.m;
   constexpr int NCH = B / 16;
-  if constexpr (EPI == EPI_GATED_BWD2 && NCH <= 4 && ACC_W == B) {
+  if constexpr (early_inputs<B, EPI, ACC_W>()) {
     // Gating backward: accumulator, staged inputs and the math for all of this thread's
     // chunks (c = half, half + 2) first, so they overlap the previous tile's TMA store still
     // reading the (single) output staging buffer; only the staging writes wait for it.
@@ -636,6 +646,7 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
     }
     if (etid == 0) bulk_wait_group_read<NBUF - 1>();
     named_bar_sync(1, kEpiWarpsT * 32);
+    if (etid == 0) after_inputs();  // every thread has read this tile's staged inputs
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int c = half + 2 * k;
@@ -1411,22 +1422,19 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
       const int j = item % p.n_lines;
       const uint32_t as = it & 1, use = it >> 1;
       const int flags = __ldg(&p.line_flags[j]);
-      // in0 (and in1) tiles per 128-row half, one half ahead (the half after `seq` goes to
-      // buffer (seq + 1) & 1, last read by half seq - 1, whose reads all precede its final
-      // barrier): the first half of the first item and the half after this item's first are
-      // requested before the accumulator wait, later ones at the top of the half loop.
-      [[maybe_unused]] auto load_after = [&](uint32_t seq, int h) {
-        if (h + 1 < TM) {
-          load_in(item, h + 1, (seq + 1) & 1);
-        } else {
-          const int nxt = item_at(p, k + 1, n_items);
-          if (nxt < n_items) load_in(nxt, 0, (seq + 1) & 1);
-        }
+      // in0 (and in1) tiles per 128-row half, two buffers indexed by the half's sequence
+      // number: the first two halves are requested up front, half seq + 2 as soon as every
+      // thread has read half seq's inputs (mid-tile for the reordered gating backward, after
+      // the tile's store barrier otherwise).
+      [[maybe_unused]] auto load_half = [&](uint32_t seq) {
+        const int kk = static_cast<int>(seq / TM), hh = static_cast<int>(seq % TM);
+        const int itm = item_at(p, kk, n_items);
+        if (itm < n_items) load_in(itm, hh, seq & 1);
       };
       if constexpr (IN_ST) {
-        if (etid == 0) {
-          if (it == 0) load_in(item, 0, 0u);
-          load_after(it * TM, 0);
+        if (etid == 0 && it == 0) {
+          load_half(0);
+          load_half(1);
         }
       }
       wc.wait(5, &tmem_full[as], use & 1, dbg_on);
@@ -1451,10 +1459,11 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
 #pragma unroll
       for (int h = 0; h < TM; ++h) {
         const uint32_t seq = it * TM + h;  // half sequence number of this CTA
-        if constexpr (IN_ST) {
-          if (etid == 0 && h > 0) load_after(seq, h);
-          wc.wait(8, &in_full[seq & 1], (seq >> 1) & 1, dbg_on);
-        }
+        if constexpr (IN_ST) wc.wait(8, &in_full[seq & 1], (seq >> 1) & 1, dbg_on);
+        constexpr bool kEarly = IN_ST && early_inputs<B, EPI, C::ACC_W>();
+        auto refill = [&]() {
+          if constexpr (IN_ST) load_half(seq + 2);
+        };
         uint8_t* stg = staging + ((it * TM + h) % C::OUT_BUFS) * C::NOUT * C::OUT_TILE;
         const uint32_t tacc =
             tmem_base + ((q * 32u) << 16) + as * C::ACC_STRIDE + h * C::HALF_ACC;
@@ -1463,7 +1472,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         epi_tile_compute<B, EPI, OutT, SUMACC, C::OUT_SW, C::OUT_BUFS, C::ACC_W>(
             p, tacc, row0, j * B, flags, stg, half, q, lane, etid, vec_ok,
             IN_ST ? in_staging + (seq & 1) * IN_ST * C::OUT_TILE : nullptr,
-            C::OUT_TILE, C::OUT_TILE);
+            C::OUT_TILE, C::OUT_TILE, [&]() {
+              if constexpr (kEarly) refill();
+            });
         if (h == TM - 1) {  // every TMEM read of this accumulator stage is done
           tc_fence_before();
           __syncwarp();
@@ -1472,6 +1483,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap mapO, const __grid_constant__
         epi_tile_store<C::OUT_SW, C::OUT_NATOM, OUT_ELT, C::NOUT>(&mapO, &mapO1, &mapO2, stg,
                                                                   C::OUT_TILE, row0, j * B, etid,
                                                                   pol_out);
+        if (!kEarly && etid == 0) refill();  // the store barrier ordered every input read
         if (dbg_on) wc.acc[9] += static_cast<unsigned long long>(clock64() - te0);
       }
     }
