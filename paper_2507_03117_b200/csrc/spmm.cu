@@ -1,6 +1,11 @@
 // Host dispatch of the block-sparse engine and the C-ABI product entry points:
 // blast_bspmm (kernels.py:86/127), blast_bspmm_rt (kernels.py:143),
 // blast_mlp_forward (mlp.py:102), blast_mlp_backward_dgrad (mlp.py:118-142).
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
 #include "host.hpp"
 #include "spmm_simt.cuh"
 #include "spmm_tc.cuh"
@@ -151,6 +156,19 @@ const int32_t* balanced_schedule(const int32_t* step_ptr, const int32_t* flags, 
                                  int n_tiles, int grid, bool seq_gu, cudaStream_t st,
                                  int* rows_out);
 
+// 0/1 switch read once per name from the environment (default `dflt`)
+static bool env_flag(const char* name, int dflt) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, int>> seen;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& kv : seen)
+    if (kv.first == name) return kv.second != 0;
+  const char* e = getenv(name);
+  const int v = e ? (e[0] == '1') : dflt;
+  seen.emplace_back(name, v);
+  return v != 0;
+}
+
 template <int B, int ELT, int NPASS, int NMAT, bool SUM, bool BK, int EPI, typename OutT,
           int OUT_ELT = 0, int TM = 1, int SPLIT = 0>
 static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cudaStream_t st) {
@@ -227,10 +245,15 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   // cfg3 shape at 95 %, 128 tokens, graph replay 18.6 -> 16.7 us (profiles/r02/decode_ab.txt).
   // 3xTF32 gate+up (cfg0 fp32: per-CTA ends spread over 22.5 of 104.6 us with round robin) is
   // balanced as well: its 48 KB stages make it latency- rather than L2-feed-bound
+  // The training gate+up (G, a and b written) is balanced too: its per-item HBM writes make the
+  // round-robin tail long (CTA ends spread over 47.7 us); LPT 310 -> 294 us, training step
+  // 1.331 -> 1.315 ms same box (tools/ab_lpt_save.sh; BLAST_LPT_SAVE=0 disables). The same
+  // schedule for the inference gate+up stays neutral (tools/ab_lpt_gu.sh, round 2).
 #ifndef BLAST_LPT_SUMACC
 #define BLAST_LPT_SUMACC 1
 #endif
   if (NMAT == 1 || NPASS == 3 || (BLAST_LPT_SUMACC && SUM) ||
+      (EPI == EPI_GATED_FWD_SAVE && env_flag("BLAST_LPT_SAVE", 1)) ||
       items < 2 * static_cast<int64_t>(num_sms()))
     p.sched = balanced_schedule(c.step_ptr, c.flags, p.n_lines, p.n_tok_tiles, grid, SPLIT == 2,
                                 st, &p.sched_rows);
