@@ -5,10 +5,10 @@
 // reference's dense gradient, needed at mask refresh for regrowth norms and by
 // the global-norm clip, trainer.py:365-384) -> dense [rows, cols].
 //
-// Tensor-core path (bf16, b in {64, 128}): one item = 128 output rows of one
-// block column c: two blocks of that column for b = 64 (they share the D
-// panel), one block for b = 128. Both operands are MN-major (A^T and D are read
-// straight from the row-major activations), K = tokens in 64-token stages.
+// Tensor-core path (bf16, b in {64, 128}): one item = up to NACC x 128 output rows of one
+// block column c: up to 2 * NACC consecutive stored blocks of that column for b = 64 (all
+// share the D panel, loaded once per stage), one block for b = 128. Both operands are
+// MN-major (A^T and D are read straight from the row-major activations), K = tokens.
 #include "host.hpp"
 #include "scan.cuh"
 #include "spmm_tc.cuh"
@@ -20,7 +20,7 @@ struct WgradParams {
   int64_t rows, cols;
   int32_t n_items;              // upper bound (grid sizing)
   const int64_t* n_items_dev;   // exact count, on device
-  const int4* items;   // {c, s0, s1, 0}: block column, first/second block slot (-1 none)
+  const int4* items;   // {c, s0, n, 0}: block column, first slot, n consecutive slots
   const int32_t* row_of;  // slot -> block row (row_idx); nullptr in dense mode (slot = row)
   float* out_blocks;   // [nnzb, b, b] (selected mode)
   float* dense_out;    // [rows, cols]  (dense mode)
@@ -34,22 +34,34 @@ struct WgradParams {
   int64_t gr;
 };
 
-// Tokens per pipeline stage (the K of one handshake): 128 -> 8 MMAs per stage (round 1: 64).
-constexpr int kWgTK = 128;
+// Accumulators (128 output rows each) per b = 64 item: 2 -> four blocks of one column share
+// each D panel load (L2 -> smem bytes per block and 128 tokens: 20 KB instead of 24 KB for
+// block pairs). b = 128: one block (one accumulator) per item.
+#ifndef BLAST_WG_NACC
+#define BLAST_WG_NACC 2
+#endif
+constexpr int kWgNacc64 = BLAST_WG_NACC;
 
 template <int B>
 struct WgCfg {
-  static constexpr int TK = kWgTK;              // tokens per stage
+  static constexpr int NACC = B == 64 ? kWgNacc64 : 1;
+  // tokens per pipeline stage (the K of one handshake): 8 MMAs per stage
+  static constexpr int TK = 128 / NACC >= 64 ? 128 / NACC : 64;
+  static constexpr int PER_ITEM = B == 64 ? 2 * NACC : 1;  // stored blocks per item
   static constexpr int ATOM = TK * 128;         // one [TK x 64 bf16] swizzle-128 atom
-  static constexpr int A_TILE = 2 * ATOM;       // 128 output rows
+  static constexpr int A_TILE = 2 * NACC * ATOM;  // NACC x 128 output rows
   static constexpr int NB_ATOM = B / 64;
   static constexpr int B_TILE = NB_ATOM * ATOM;
   static constexpr int STAGE = A_TILE + B_TILE;
   static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
-  static constexpr int TMEM_COLS = 2 * B <= 128 ? 128 : 256;
+  static constexpr int ACC_COLS = NACC * B;     // TMEM columns per accumulator stage
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 128 ? 128 : 2 * ACC_COLS <= 256 ? 256 : 512;
   static constexpr uint32_t IDESC = make_idesc(128, B, 1u, 1u, 1u);
   static constexpr int SMEM_BYTES = STAGES * STAGE + 256 + 1024;
+  static_assert(STAGES >= 3 && 2 * ACC_COLS <= 512, "wgrad stage / accumulator budget");
 };
+static int wgrad_per_item(int block) { return block == 64 ? WgCfg<64>::PER_ITEM : WgCfg<128>::PER_ITEM; }
+static int wgrad_tk(int block) { return block == 64 ? WgCfg<64>::TK : WgCfg<128>::TK; }
 
 constexpr uint32_t kWgBarAcc = 2;    // + accumulator stage (2 ids)
 constexpr uint32_t kWgBarStage = 4;  // + ring stage (<= 8 ids)
@@ -93,6 +105,12 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   const uint32_t tmem_base = *tmem_slot;
 
   auto block_row = [&](int slot) -> int { return p.row_of ? p.row_of[slot] : slot; };
+  // k-th work unit of this CTA: round robin over the column-ordered list (-1: past the end)
+  const int G = static_cast<int>(gridDim.x), bx = static_cast<int>(blockIdx.x);
+  auto unit = [&](int k) -> int {
+    const int w = k * G + bx;
+    return w < n_work ? w : -1;
+  };
 
   // token-stage range of a work item (split-K)
   auto krange = [&](int w, int& k0, int& k1) {
@@ -104,26 +122,35 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   if (warp == 0) {
     // whole warp walks the work list; one elected lane issues the copies
     uint32_t stage = 0, phase = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+    for (int k = 0; k * G < n_work; ++k) {
+      const int w = unit(k);
+      if (w < 0) continue;
       const int4 it = __ldg(&p.items[w / p.n_split]);
       const int c = it.x;
-      const int r0 = block_row(it.y);
-      const int r1 = it.z >= 0 ? block_row(it.z) : r0;
+      const int n = it.z;  // stored blocks of the item (consecutive slots from it.y)
+      // lane i holds the block row of the item's i-th block
+      const int my_r = static_cast<int>(lane) < n ? block_row(it.y + static_cast<int>(lane)) : 0;
+      int rows[C::PER_ITEM];
+#pragma unroll
+      for (int i = 0; i < C::PER_ITEM; ++i) rows[i] = __shfl_sync(0xffffffffu, my_r, i);
       int k0, k1;
       krange(w, k0, k1);
+      // A atoms: one per block (b = 64), both halves of the block (b = 128)
+      const int n_atoms = B == 64 ? n : 2;
       for (int ks = k0; ks < k1; ++ks) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
-          mbar_expect_tx(&full[stage], C::STAGE);
+          mbar_expect_tx(&full[stage], (n_atoms + C::NB_ATOM) * C::ATOM);
           uint8_t* sa = smem + stage * C::STAGE;
           uint8_t* sb = sa + C::A_TILE;
           const int tok = ks * C::TK;
           if (B == 64) {
-            tma_load_2d(sa, &mapA, &full[stage], r0 * B, tok);
-            tma_load_2d(sa + C::ATOM, &mapA, &full[stage], r1 * B, tok);
+#pragma unroll
+            for (int i = 0; i < C::PER_ITEM; ++i)
+              if (i < n) tma_load_2d(sa + i * C::ATOM, &mapA, &full[stage], rows[i] * B, tok);
           } else {
-            tma_load_2d(sa, &mapA, &full[stage], r0 * B, tok);
-            tma_load_2d(sa + C::ATOM, &mapA, &full[stage], r0 * B + 64, tok);
+            tma_load_2d(sa, &mapA, &full[stage], rows[0] * B, tok);
+            tma_load_2d(sa + C::ATOM, &mapA, &full[stage], rows[0] * B + 64, tok);
           }
 #pragma unroll
           for (int a = 0; a < C::NB_ATOM; ++a)
@@ -141,23 +168,33 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     const uint64_t a_desc0 = make_sdesc(smem_u32(smem), C::ATOM, 1024, 2);
     const uint64_t b_desc0 = make_sdesc(smem_u32(smem) + C::A_TILE, C::ATOM, 1024, 2);
     uint32_t stage = 0, it = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
-      const uint32_t as = it & 1;
+    for (int k = 0; k * G < n_work; ++k) {
+      const int w = unit(k);
+      if (w < 0) continue;
+      const uint32_t as = it++ & 1;
       int k0, k1;
       krange(w, k0, k1);
+      // accumulators in use: one per two blocks (b = 64); an odd last block leaves rows
+      // 64..127 of its accumulator computed from a stale atom and never stored
+      const int n = __ldg(&p.items[w / p.n_split]).z;
+      const int na = B == 64 ? (n + 1) / 2 : 1;
       named_bar_sync(kWgBarAcc + as, 64);  // warp 3 saw tmem_empty[as]
       tc_fence_after();
-      const uint32_t d = tmem_base + as * B;
+      const uint32_t d = tmem_base + as * C::ACC_COLS;
       for (int ks = k0; ks < k1; ++ks) {
         named_bar_sync(kWgBarStage + stage, 64);  // warp 3 saw full[stage]
         tc_fence_after();
         if (elect_one()) {
           const uint32_t soff = (stage * C::STAGE) >> 4;
 #pragma unroll
-          for (int kk = 0; kk < C::TK / 16; ++kk)
-            mma_f16(d, a_desc0 + soff + ((kk * 16 * 128) >> 4),
-                    b_desc0 + soff + ((kk * 16 * 128) >> 4), C::IDESC,
-                    (ks > k0 || kk > 0) ? 1u : 0u);
+          for (int a = 0; a < C::NACC; ++a) {
+            if (a >= na) break;
+#pragma unroll
+            for (int kk = 0; kk < C::TK / 16; ++kk)
+              mma_f16(d + a * B, a_desc0 + soff + ((a * 2 * C::ATOM + kk * 16 * 128) >> 4),
+                      b_desc0 + soff + ((kk * 16 * 128) >> 4), C::IDESC,
+                      (ks > k0 || kk > 0) ? 1u : 0u);
+          }
           mma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -169,8 +206,11 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   } else if (warp == 3) {
     // barrier waiter: mirrors the MMA warp's sequence
     uint32_t stage = 0, phase = 0, it = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+    for (int k = 0; k * G < n_work; ++k) {
+      const int w = unit(k);
+      if (w < 0) continue;
       const uint32_t as = it & 1, use = it >> 1;
+      ++it;
       int k0, k1;
       krange(w, k0, k1);
       mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
@@ -184,25 +224,28 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;
     uint32_t it = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++it) {
+    for (int k = 0; k * G < n_work; ++k) {
+      const int w = unit(k);
+      if (w < 0) continue;
       const int4 itm = __ldg(&p.items[w / p.n_split]);
       const int sp = w % p.n_split;
       int k0, k1;
       krange(w, k0, k1);
       const uint32_t as = it & 1, use = it >> 1;
+      ++it;
       mbar_wait(&tmem_full[as], use & 1);
       tc_fence_after();
       const int lrow = static_cast<int>(q * 32 + lane);  // 0..127
-      int slot, r, li;
-      if (B == 64) {
-        slot = lrow < 64 ? itm.y : itm.z;
-        li = lrow & 63;
-      } else {
-        slot = itm.y;
-        li = lrow;
-      }
-      r = slot >= 0 ? block_row(slot) : -1;
-      const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * B;
+      const int n = itm.z;
+      const int na = B == 64 ? (n + 1) / 2 : 1;
+#pragma unroll 1
+      for (int acc = 0; acc < na; ++acc) {
+      // accumulator acc holds blocks 2 acc (rows 0..63) and 2 acc + 1 (rows 64..127) for b = 64
+      const int bi = B == 64 ? 2 * acc + (lrow >> 6) : 0;
+      const int slot = bi < n ? itm.y + bi : -1;
+      const int li = B == 64 ? (lrow & 63) : lrow;
+      const int r = slot >= 0 ? block_row(slot) : -1;
+      const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_COLS + acc * B;
 #pragma unroll 1
       for (int ch = 0; ch < B / 16; ++ch) {
         float v[16];
@@ -227,6 +270,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           float* dst = p.out_blocks + (static_cast<int64_t>(slot) * B + li) * B + ch * 16;
           store_chunk16<float>(dst, v, 16, true);
         }
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -296,20 +340,23 @@ __global__ void __launch_bounds__(256) wgrad_simt_kernel(const T* __restrict__ A
     }
 }
 
-// items for the tensor-core kernel: per block column, consecutive stored blocks paired
-// (b = 64) or single (b = 128). Dense mode: every block of the grid.
+// items for the tensor-core kernel: per block column, runs of up to per_item consecutive
+// stored blocks (WgCfg::PER_ITEM), in column order, so the items of one column (sharing its
+// D panels) run side by side in the same wave. Dense mode: every block of the grid.
+// (A size-sorted list dealt in snake order balances the CTAs better but puts a column's items
+// in different waves: its D panels are then read from HBM once per item, which costs more;
+// profiles/r02/train_step/wgrad_items.txt.)
 __global__ void wgrad_items_kernel(const int64_t* col_ptr, int64_t gr, int64_t gc, int per_item,
                                    const int64_t* item_ptr, int4* items) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= gc) return;
-  const int64_t lo = col_ptr ? col_ptr[c] : c * gr;  // dense mode: slot = row, lo unused
+  const int64_t lo = col_ptr ? col_ptr[c] : c * gr;  // dense mode: slot = row
   const int64_t hi = col_ptr ? col_ptr[c + 1] : c * gr + gr;
   int64_t out = item_ptr[c];
   for (int64_t s = lo; s < hi; s += per_item) {
-    int s0 = static_cast<int>(col_ptr ? s : s - c * gr);
-    int s1 = -1;
-    if (per_item == 2 && s + 1 < hi) s1 = static_cast<int>(col_ptr ? s + 1 : s + 1 - c * gr);
-    items[out++] = make_int4(static_cast<int>(c), s0, s1, 0);
+    const int s0 = static_cast<int>(col_ptr ? s : s - c * gr);
+    const int n = static_cast<int>(hi - s < per_item ? hi - s : per_item);
+    items[out++] = make_int4(static_cast<int>(c), s0, n, 0);
   }
 }
 __global__ void wgrad_item_count_kernel(const int64_t* col_ptr, int64_t gr, int64_t gc,
@@ -402,7 +449,7 @@ extern "C" int blast_wgrad_plan(const int64_t* col_ptr, int64_t grid_rows, int64
     return BLAST_EINVAL;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int per_item = block == 64 ? 2 : 1;
+  const int per_item = wgrad_per_item(block);
   const int thr = 256, blk = static_cast<int>(cdiv(grid_cols, thr));
   wgrad_item_count_kernel<<<blk, thr, 0, st>>>(col_ptr, grid_rows, grid_cols, per_item, counts);
   offsets_scan_kernel<int64_t><<<1, 1024, 0, st>>>(counts, grid_cols);
@@ -457,7 +504,7 @@ static int block_wgrad_impl(const void* a, const void* d, int64_t m, int64_t row
                   aligned16(d) && m <= INT32_MAX;
   const int64_t* cp = dense ? nullptr : col_ptr;
   if (tc) {
-    const int per_item = block == 64 ? 2 : 1;
+    const int per_item = wgrad_per_item(block);
     Scratch sp, si;
     if (plan_items && plan_counts && !dense) {  // item list cached with the matrix structure
       p.n_items_dev = plan_counts + gc;
@@ -472,9 +519,10 @@ static int block_wgrad_impl(const void* a, const void* d, int64_t m, int64_t row
       p.n_items_dev = sp.as<int64_t>() + gc;
       p.items = si.as<int4>();
     }
-    p.n_items = static_cast<int32_t>((nsel + gc + per_item - 1) / per_item);
+    // upper bound of sum over columns of ceil(blocks / per_item) (grid sizing, split-K choice)
+    p.n_items = static_cast<int32_t>(std::min<int64_t>(nsel, (nsel + gc * (per_item - 1)) / per_item));
     // split-K when the blocks cannot fill the GPU (e.g. GPT-2 small at 90%: ~60 blocks)
-    const int ksteps = static_cast<int>(cdiv(m, kWgTK));
+    const int ksteps = static_cast<int>(cdiv(m, wgrad_tk(block)));
     int n_split = 1;
     if (p.n_items < 2 * num_sms() && ksteps >= 8)
       n_split = std::min<int>({static_cast<int>(cdiv(2 * num_sms(), p.n_items)), ksteps / 4, 32});
