@@ -32,7 +32,21 @@ struct WgradParams {
   float* partial;      // [n_split][n_slots][b][b]
   int64_t n_slots;     // selected blocks, or gr*gc in dense mode (slot = c*gr + r)
   int64_t gr;
+  // tail split (selected mode, n_split = 1): when the last wave would hold few items
+  // (r = items mod grid <= grid / 4), those r items are split along the tokens into
+  // tail_splits(r) parts written as fp32 partials [kWgTailSplit][tail_cap][b][b] and summed in
+  // split order by wgrad_tail_reduce_kernel; nullptr disables.
+  float* tail_partial;
+  int64_t tail_cap;    // partial slots per split (>= grid / 4 * items' blocks)
 };
+
+constexpr int kWgTailSplit = 8;
+// number of parts of each tail item (1: no tail split) for n_items items on a grid of g CTAs
+__host__ __device__ __forceinline__ int wgrad_tail_splits(int n_items, int g) {
+  const int r = n_items % g;
+  if (r == 0 || 4 * r > g) return 1;
+  return g / r < kWgTailSplit ? g / r : kWgTailSplit;
+}
 
 // Accumulators (128 output rows each) per b = 64 item: 2 -> four blocks of one column share
 // each D panel load (L2 -> smem bytes per block and 128 tokens: 20 KB instead of 24 KB for
@@ -80,7 +94,14 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int ksteps = (p.m + C::TK - 1) / C::TK;
-  const int n_work = static_cast<int>(*p.n_items_dev) * p.n_split;
+  const int n_items = static_cast<int>(*p.n_items_dev);
+  const int t_s = (p.tail_partial && p.n_split == 1) ? wgrad_tail_splits(n_items, gridDim.x) : 1;
+  const int t_base = t_s > 1 ? n_items - n_items % static_cast<int>(gridDim.x) : n_items;
+  const int n_work = t_s > 1 ? t_base + (n_items - t_base) * t_s : n_items * p.n_split;
+  // work unit -> item (tail units: t_s per item)
+  auto item_of = [&](int w) -> int {
+    return (t_s > 1 && w >= t_base) ? t_base + (w - t_base) / t_s : w / p.n_split;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapA);
@@ -114,9 +135,16 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
 
   // token-stage range of a work item (split-K)
   auto krange = [&](int w, int& k0, int& k1) {
-    const int sp = w % p.n_split;
-    k0 = sp * p.kps;
-    k1 = min(ksteps, k0 + p.kps);
+    int sp, kps;
+    if (t_s > 1 && w >= t_base) {
+      sp = (w - t_base) % t_s;
+      kps = (ksteps + t_s - 1) / t_s;
+    } else {
+      sp = w % p.n_split;
+      kps = p.kps;
+    }
+    k0 = sp * kps;
+    k1 = min(ksteps, k0 + kps);
   };
 
   if (warp == 0) {
@@ -125,7 +153,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     for (int k = 0; k * G < n_work; ++k) {
       const int w = unit(k);
       if (w < 0) continue;
-      const int4 it = __ldg(&p.items[w / p.n_split]);
+      const int4 it = __ldg(&p.items[item_of(w)]);
       const int c = it.x;
       const int n = it.z;  // stored blocks of the item (consecutive slots from it.y)
       // lane i holds the block row of the item's i-th block
@@ -176,7 +204,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       krange(w, k0, k1);
       // accumulators in use: one per two blocks (b = 64); an odd last block leaves rows
       // 64..127 of its accumulator computed from a stale atom and never stored
-      const int n = __ldg(&p.items[w / p.n_split]).z;
+      const int n = __ldg(&p.items[item_of(w)]).z;
       const int na = B == 64 ? (n + 1) / 2 : 1;
       named_bar_sync(kWgBarAcc + as, 64);  // warp 3 saw tmem_empty[as]
       tc_fence_after();
@@ -227,8 +255,11 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     for (int k = 0; k * G < n_work; ++k) {
       const int w = unit(k);
       if (w < 0) continue;
-      const int4 itm = __ldg(&p.items[w / p.n_split]);
-      const int sp = w % p.n_split;
+      const int4 itm = __ldg(&p.items[item_of(w)]);
+      const bool tail = t_s > 1 && w >= t_base;
+      const int sp = tail ? (w - t_base) % t_s : w % p.n_split;
+      // tail units: partial slot index relative to the first tail item's first block
+      const int64_t tslot0 = tail ? __ldg(&p.items[t_base]).y : 0;
       int k0, k1;
       krange(w, k0, k1);
       const uint32_t as = it & 1, use = it >> 1;
@@ -255,7 +286,10 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
           for (int i = 0; i < 16; ++i) v[i] = 0.0f;
         }
         if (slot < 0) continue;
-        if (p.n_split > 1) {  // fp32 partial, reduced in split order afterwards
+        if (tail) {  // fp32 partial of a tail item, reduced in split order afterwards
+          float* dst = p.tail_partial + ((sp * p.tail_cap + (slot - tslot0)) * B + li) * B + ch * 16;
+          store_chunk16<float>(dst, v, 16, true);
+        } else if (p.n_split > 1) {  // fp32 partial, reduced in split order afterwards
           const int64_t flat = p.dense_out ? static_cast<int64_t>(itm.x) * p.gr + r : slot;
           float* dst = p.partial + ((sp * p.n_slots + flat) * B + li) * B + ch * 16;
           store_chunk16<float>(dst, v, 16, true);
@@ -385,6 +419,22 @@ __global__ void wgrad_reduce_kernel(const WgradParams p, int b) {
     }
   }
 }
+// tail-split reduction: blocks of the last r items = sum of their t_s partials in split order
+__global__ void wgrad_tail_reduce_kernel(const WgradParams p, int b, int grid) {
+  const int n_items = static_cast<int>(*p.n_items_dev);
+  const int t_s = wgrad_tail_splits(n_items, grid);
+  if (t_s <= 1) return;
+  const int t_base = n_items - n_items % grid;
+  const int64_t s0 = p.items[t_base].y;
+  const int64_t bb = static_cast<int64_t>(b) * b;
+  const int64_t total = (p.n_slots - s0) * bb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = p.tail_partial[i];
+    for (int sp = 1; sp < t_s; ++sp) acc = __fadd_rn(acc, p.tail_partial[sp * p.tail_cap * bb + i]);
+    p.out_blocks[s0 * bb + i] = acc;
+  }
+}
 // simt items: one per (slot, 64x64 sub-tile)
 __global__ void wgrad_simt_items_kernel(const int64_t* col_ptr, int64_t gr, int64_t gc, int tiles,
                                         int4* items) {
@@ -415,6 +465,12 @@ static int launch_wgrad_tc(const void* a, const void* d, const WgradParams& p, c
   const int grid = static_cast<int>(work < num_sms() ? work : num_sms());
   kern<<<grid, 256, C::SMEM_BYTES, st>>>(ma, md, p);
   int rc = check_launch("wgrad_tc");
+  if (rc == BLAST_OK && p.tail_partial) {  // no-op on the device when no tail split happened
+    const int64_t total = std::min<int64_t>(p.n_slots, p.tail_cap) * B * B;
+    const int rg = static_cast<int>(std::min<int64_t>(cdiv(total, 256), (int64_t)num_sms() * 4));
+    wgrad_tail_reduce_kernel<<<rg, 256, 0, st>>>(p, B, grid);
+    rc = check_launch("wgrad_tail_reduce");
+  }
   if (rc == BLAST_OK && p.n_split > 1) {
     const int64_t total = p.n_slots * B * B;
     const int rg = static_cast<int>(std::min<int64_t>(cdiv(total, 256), (int64_t)num_sms() * 8));
@@ -531,11 +587,17 @@ static int block_wgrad_impl(const void* a, const void* d, int64_t m, int64_t row
     p.n_split = static_cast<int32_t>(cdiv(ksteps, p.kps));
     p.n_slots = nsel;
     p.gr = gr;
-    Scratch spart;
+    Scratch spart, stail;
     if (p.n_split > 1) {
       if (!spart.alloc(sizeof(float) * p.n_split * nsel * block * block, st))
         return cuda_status(cudaGetLastError(), "wgrad partials");
       p.partial = spart.as<float>();
+    } else if (!dense && p.n_items >= num_sms()) {
+      // tail split: at most grid / 4 tail items of per_item blocks each
+      p.tail_cap = std::min<int64_t>(nsel, static_cast<int64_t>(num_sms() / 4) * per_item);
+      if (!stail.alloc(sizeof(float) * kWgTailSplit * p.tail_cap * block * block, st))
+        return cuda_status(cudaGetLastError(), "wgrad tail partials");
+      p.tail_partial = stail.as<float>();
     }
     return block == 64 ? launch_wgrad_tc<64>(a, d, p, st) : launch_wgrad_tc<128>(a, d, p, st);
   }
