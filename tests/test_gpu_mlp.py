@@ -302,3 +302,31 @@ def test_backward_grad_ready_hook_order_and_bits():
     assert [p for _, p in seen] == [got[3].data_ptr(), got[1].data_ptr(), got[2].data_ptr()]
     for r, o in zip(ref, got):
         assert torch.equal(r, o)
+
+
+@pytest.mark.parametrize("which", [0, 1, 2])
+def test_stored_block_wgrad_item_layouts(which):
+    """Stored-block weight gradients at the cfg3 mask structures (csrc/wgrad.cu): 4-block items
+    per column, the up mask's 446 items (3 waves of 148 + 2, the last two split along the
+    tokens into fp32 partials) and the down mask's long columns; every stored block against
+    x^T d in fp32 (mlp.py:137-141) and bitwise reproducible."""
+    import bench
+    from paper_2507_03117_b200 import mlp as M
+    rows, cols = (4096, 14336) if which < 2 else (14336, 4096)
+    w = bs.from_host(bench.make_weights(4096, 14336, 64, 0.9, 0)[which], torch.bfloat16)
+    g = torch.Generator(device="cuda").manual_seed(7 + which)
+    m = 256
+    a = torch.randn(m, rows, device="cuda", generator=g).bfloat16()
+    d = torch.randn(m, cols, device="cuda", generator=g).bfloat16()
+    got = M._wgrad(a, d, rows, cols, w, False)
+    assert torch.equal(got, M._wgrad(a, d, rows, cols, w, False))
+    full = a.float().t() @ d.float()
+    cp = w.col_ptr.cpu().numpy()
+    ri = w.block_row_idx.cpu().numpy()
+    ref = torch.empty_like(got)
+    for c in range(len(cp) - 1):
+        for s in range(cp[c], cp[c + 1]):
+            r = int(ri[s])
+            ref[s] = full[r * 64:(r + 1) * 64, c * 64:(c + 1) * 64]
+    err = ((got - ref).abs().max() / ref.abs().max()).item()
+    assert err <= 1e-5, err
