@@ -38,6 +38,12 @@ struct WgradParams {
   // split order by wgrad_tail_reduce_kernel; nullptr disables.
   float* tail_partial;
   int64_t tail_cap;    // partial slots per split (>= grid / 4 * items' blocks)
+  // sweep mode (when every CTA has at most WgCfg::MAX_SWEEP units): a CTA keeps all its
+  // units' accumulators in TMEM and walks the tokens once, stage by stage over its units, so
+  // all CTAs sweep the activations together and each panel is read from HBM about once (one
+  // unit after another, the CTAs restart the sweep per wave and re-read the panels that L2
+  // did not keep: dWdown read 731 MB of DRAM for 300 MB of operands)
+  int32_t sweep_ok;
 };
 
 constexpr int kWgTailSplit = 8;
@@ -69,11 +75,22 @@ struct WgCfg {
   static constexpr int STAGE = A_TILE + B_TILE;
   static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
   static constexpr int ACC_COLS = NACC * B;     // TMEM columns per accumulator stage
-  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 128 ? 128 : 2 * ACC_COLS <= 256 ? 256 : 512;
+  // all 512 columns: the sweep mode keeps up to 512 / ACC_COLS units' accumulators live
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int MAX_SWEEP = 512 / ACC_COLS;
   static constexpr uint32_t IDESC = make_idesc(128, B, 1u, 1u, 1u);
   static constexpr int SMEM_BYTES = STAGES * STAGE + 256 + 1024;
   static_assert(STAGES >= 3 && 2 * ACC_COLS <= 512, "wgrad stage / accumulator budget");
 };
+// BLAST_WG_SWEEP=0 disables the sweep mode (WgradParams::sweep_ok)
+static bool wgrad_sweep_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_WG_SWEEP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 static int wgrad_per_item(int block) { return block == 64 ? WgCfg<64>::PER_ITEM : WgCfg<128>::PER_ITEM; }
 static int wgrad_tk(int block) { return block == 64 ? WgCfg<64>::TK : WgCfg<128>::TK; }
 
@@ -147,45 +164,108 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     k1 = min(ksteps, k0 + kps);
   };
 
+  // sweep mode: this CTA's units are unit(0..n_mine-1), all resident in TMEM
+  const bool sweep = p.sweep_ok && n_work <= C::MAX_SWEEP * G;
+  const int n_mine = sweep ? (n_work - bx + G - 1) / G : 0;
+  int sk0 = 0, sk1 = 0;  // token-stage span of the sweep
+  if (sweep) {
+    sk0 = ksteps;
+    for (int j = 0; j < n_mine; ++j) {
+      int a0, a1;
+      krange(unit(j), a0, a1);
+      sk0 = min(sk0, a0);
+      sk1 = max(sk1, a1);
+    }
+  }
+
+  // the item's block rows: lane i reads the i-th, then every lane holds all (warp-uniform)
+  auto item_rows = [&](const int4& it, int (&rows)[C::PER_ITEM]) {
+    const int my_r = static_cast<int>(lane) < it.z ? block_row(it.y + static_cast<int>(lane)) : 0;
+#pragma unroll
+    for (int i = 0; i < C::PER_ITEM; ++i) rows[i] = __shfl_sync(0xffffffffu, my_r, i);
+  };
+  // one stage of item `it` at token stage ks (elected lane)
+  auto load_stage = [&](uint32_t stage, const int4& it, const int (&rows)[C::PER_ITEM], int ks) {
+    const int n = it.z;
+    // A atoms: one per block (b = 64), both halves of the block (b = 128)
+    const int n_atoms = B == 64 ? n : 2;
+    mbar_expect_tx(&full[stage], (n_atoms + C::NB_ATOM) * C::ATOM);
+    uint8_t* sa = smem + stage * C::STAGE;
+    uint8_t* sb = sa + C::A_TILE;
+    const int tok = ks * C::TK;
+    if (B == 64) {
+#pragma unroll
+      for (int i = 0; i < C::PER_ITEM; ++i)
+        if (i < n) tma_load_2d(sa + i * C::ATOM, &mapA, &full[stage], rows[i] * B, tok);
+    } else {
+      tma_load_2d(sa, &mapA, &full[stage], rows[0] * B, tok);
+      tma_load_2d(sa + C::ATOM, &mapA, &full[stage], rows[0] * B + 64, tok);
+    }
+#pragma unroll
+    for (int a = 0; a < C::NB_ATOM; ++a)
+      tma_load_2d(sb + a * C::ATOM, &mapD, &full[stage], it.x * B + a * 64, tok);
+  };
+  // MMAs of one stage into the accumulators at TMEM column d (elected lane)
+  auto mma_stage = [&](uint32_t stage, uint32_t d, int na, bool first, uint64_t a_desc0,
+                       uint64_t b_desc0) {
+    const uint32_t soff = (stage * C::STAGE) >> 4;
+#pragma unroll
+    for (int a = 0; a < C::NACC; ++a) {
+      if (a >= na) break;
+#pragma unroll
+      for (int kk = 0; kk < C::TK / 16; ++kk)
+        mma_f16(d + a * B, a_desc0 + soff + ((a * 2 * C::ATOM + kk * 16 * 128) >> 4),
+                b_desc0 + soff + ((kk * 16 * 128) >> 4), C::IDESC, (!first || kk > 0) ? 1u : 0u);
+    }
+    mma_commit(&empty[stage]);
+  };
+  // accumulators in use: one per two blocks (b = 64); an odd last block leaves rows 64..127 of
+  // its accumulator computed from a stale atom and never stored
+  auto n_acc = [](int n) { return B == 64 ? (n + 1) / 2 : 1; };
+
   if (warp == 0) {
     // whole warp walks the work list; one elected lane issues the copies
     uint32_t stage = 0, phase = 0;
-    for (int k = 0; k * G < n_work; ++k) {
-      const int w = unit(k);
-      if (w < 0) continue;
-      const int4 it = __ldg(&p.items[item_of(w)]);
-      const int c = it.x;
-      const int n = it.z;  // stored blocks of the item (consecutive slots from it.y)
-      // lane i holds the block row of the item's i-th block
-      const int my_r = static_cast<int>(lane) < n ? block_row(it.y + static_cast<int>(lane)) : 0;
-      int rows[C::PER_ITEM];
+    if (sweep) {
+      int4 its[C::MAX_SWEEP];
+      int rows[C::MAX_SWEEP][C::PER_ITEM], k0s[C::MAX_SWEEP], k1s[C::MAX_SWEEP];
 #pragma unroll
-      for (int i = 0; i < C::PER_ITEM; ++i) rows[i] = __shfl_sync(0xffffffffu, my_r, i);
-      int k0, k1;
-      krange(w, k0, k1);
-      // A atoms: one per block (b = 64), both halves of the block (b = 128)
-      const int n_atoms = B == 64 ? n : 2;
-      for (int ks = k0; ks < k1; ++ks) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (elect_one()) {
-          mbar_expect_tx(&full[stage], (n_atoms + C::NB_ATOM) * C::ATOM);
-          uint8_t* sa = smem + stage * C::STAGE;
-          uint8_t* sb = sa + C::A_TILE;
-          const int tok = ks * C::TK;
-          if (B == 64) {
-#pragma unroll
-            for (int i = 0; i < C::PER_ITEM; ++i)
-              if (i < n) tma_load_2d(sa + i * C::ATOM, &mapA, &full[stage], rows[i] * B, tok);
-          } else {
-            tma_load_2d(sa, &mapA, &full[stage], rows[0] * B, tok);
-            tma_load_2d(sa + C::ATOM, &mapA, &full[stage], rows[0] * B + 64, tok);
-          }
-#pragma unroll
-          for (int a = 0; a < C::NB_ATOM; ++a)
-            tma_load_2d(sb + a * C::ATOM, &mapD, &full[stage], c * B + a * 64, tok);
+      for (int j = 0; j < C::MAX_SWEEP; ++j) {
+        if (j < n_mine) {
+          const int w = unit(j);
+          its[j] = __ldg(&p.items[item_of(w)]);
+          item_rows(its[j], rows[j]);
+          krange(w, k0s[j], k1s[j]);
+        } else {
+          its[j] = make_int4(0, 0, 0, 0);
+          k0s[j] = k1s[j] = 0;
         }
-        __syncwarp();
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      for (int ks = sk0; ks < sk1; ++ks) {
+#pragma unroll
+        for (int j = 0; j < C::MAX_SWEEP; ++j) {
+          if (j >= n_mine || ks < k0s[j] || ks >= k1s[j]) continue;
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (elect_one()) load_stage(stage, its[j], rows[j], ks);
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else {
+      for (int k = 0; k * G < n_work; ++k) {
+        const int w = unit(k);
+        if (w < 0) continue;
+        const int4 it = __ldg(&p.items[item_of(w)]);
+        int rows[C::PER_ITEM];
+        item_rows(it, rows);
+        int k0, k1;
+        krange(w, k0, k1);
+        for (int ks = k0; ks < k1; ++ks) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (elect_one()) load_stage(stage, it, rows, ks);
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -196,65 +276,96 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
     const uint64_t a_desc0 = make_sdesc(smem_u32(smem), C::ATOM, 1024, 2);
     const uint64_t b_desc0 = make_sdesc(smem_u32(smem) + C::A_TILE, C::ATOM, 1024, 2);
     uint32_t stage = 0, it = 0;
-    for (int k = 0; k * G < n_work; ++k) {
-      const int w = unit(k);
-      if (w < 0) continue;
-      const uint32_t as = it++ & 1;
-      int k0, k1;
-      krange(w, k0, k1);
-      // accumulators in use: one per two blocks (b = 64); an odd last block leaves rows
-      // 64..127 of its accumulator computed from a stale atom and never stored
-      const int n = __ldg(&p.items[item_of(w)]).z;
-      const int na = B == 64 ? (n + 1) / 2 : 1;
-      named_bar_sync(kWgBarAcc + as, 64);  // warp 3 saw tmem_empty[as]
-      tc_fence_after();
-      const uint32_t d = tmem_base + as * C::ACC_COLS;
-      for (int ks = k0; ks < k1; ++ks) {
-        named_bar_sync(kWgBarStage + stage, 64);  // warp 3 saw full[stage]
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t soff = (stage * C::STAGE) >> 4;
+    if (sweep) {
+      int nas[C::MAX_SWEEP], k0s[C::MAX_SWEEP], k1s[C::MAX_SWEEP];
 #pragma unroll
-          for (int a = 0; a < C::NACC; ++a) {
-            if (a >= na) break;
-#pragma unroll
-            for (int kk = 0; kk < C::TK / 16; ++kk)
-              mma_f16(d + a * B, a_desc0 + soff + ((a * 2 * C::ATOM + kk * 16 * 128) >> 4),
-                      b_desc0 + soff + ((kk * 16 * 128) >> 4), C::IDESC,
-                      (ks > k0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit(&empty[stage]);
+      for (int j = 0; j < C::MAX_SWEEP; ++j) {
+        nas[j] = 0;
+        k0s[j] = k1s[j] = 0;
+        if (j < n_mine) {
+          const int w = unit(j);
+          nas[j] = n_acc(__ldg(&p.items[item_of(w)]).z);
+          krange(w, k0s[j], k1s[j]);
         }
-        __syncwarp();
-        if (++stage == C::STAGES) stage = 0;
       }
-      if (elect_one()) mma_commit(&tmem_full[as]);
+      tc_fence_after();
+      for (int ks = sk0; ks < sk1; ++ks) {
+#pragma unroll
+        for (int j = 0; j < C::MAX_SWEEP; ++j) {
+          if (j >= n_mine || ks < k0s[j] || ks >= k1s[j]) continue;
+          named_bar_sync(kWgBarStage + stage, 64);  // warp 3 saw full[stage]
+          tc_fence_after();
+          if (elect_one())
+            mma_stage(stage, tmem_base + j * C::ACC_COLS, nas[j], ks == k0s[j], a_desc0, b_desc0);
+          __syncwarp();
+          if (++stage == C::STAGES) stage = 0;
+        }
+      }
+      if (elect_one()) mma_commit(&tmem_full[0]);
       __syncwarp();
+    } else {
+      for (int k = 0; k * G < n_work; ++k) {
+        const int w = unit(k);
+        if (w < 0) continue;
+        const uint32_t as = it++ & 1;
+        int k0, k1;
+        krange(w, k0, k1);
+        const int na = n_acc(__ldg(&p.items[item_of(w)]).z);
+        named_bar_sync(kWgBarAcc + as, 64);  // warp 3 saw tmem_empty[as]
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * C::ACC_COLS;
+        for (int ks = k0; ks < k1; ++ks) {
+          named_bar_sync(kWgBarStage + stage, 64);  // warp 3 saw full[stage]
+          tc_fence_after();
+          if (elect_one()) mma_stage(stage, d, na, ks == k0, a_desc0, b_desc0);
+          __syncwarp();
+          if (++stage == C::STAGES) stage = 0;
+        }
+        if (elect_one()) mma_commit(&tmem_full[as]);
+        __syncwarp();
+      }
     }
   } else if (warp == 3) {
     // barrier waiter: mirrors the MMA warp's sequence
     uint32_t stage = 0, phase = 0, it = 0;
-    for (int k = 0; k * G < n_work; ++k) {
-      const int w = unit(k);
-      if (w < 0) continue;
-      const uint32_t as = it & 1, use = it >> 1;
-      ++it;
-      int k0, k1;
-      krange(w, k0, k1);
-      mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
-      named_bar_arrive(kWgBarAcc + as, 64);
-      for (int ks = k0; ks < k1; ++ks) {
-        mbar_wait(&full[stage], phase);
-        named_bar_arrive(kWgBarStage + stage, 64);
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+    if (sweep) {
+      int k0s[C::MAX_SWEEP], k1s[C::MAX_SWEEP];
+#pragma unroll
+      for (int j = 0; j < C::MAX_SWEEP; ++j) {
+        k0s[j] = k1s[j] = 0;
+        if (j < n_mine) krange(unit(j), k0s[j], k1s[j]);
+      }
+      for (int ks = sk0; ks < sk1; ++ks) {
+#pragma unroll
+        for (int j = 0; j < C::MAX_SWEEP; ++j) {
+          if (j >= n_mine || ks < k0s[j] || ks >= k1s[j]) continue;
+          mbar_wait(&full[stage], phase);
+          named_bar_arrive(kWgBarStage + stage, 64);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else {
+      for (int k = 0; k * G < n_work; ++k) {
+        const int w = unit(k);
+        if (w < 0) continue;
+        const uint32_t as = it & 1, use = it >> 1;
+        ++it;
+        int k0, k1;
+        krange(w, k0, k1);
+        mbar_wait(&tmem_empty[as], (use & 1) ^ 1);
+        named_bar_arrive(kWgBarAcc + as, 64);
+        for (int ks = k0; ks < k1; ++ks) {
+          mbar_wait(&full[stage], phase);
+          named_bar_arrive(kWgBarStage + stage, 64);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;
-    uint32_t it = 0;
-    for (int k = 0; k * G < n_work; ++k) {
-      const int w = unit(k);
-      if (w < 0) continue;
+    const int lrow = static_cast<int>(q * 32 + lane);  // 0..127
+    // TMEM -> global for work unit w whose accumulators start at TMEM column `col`
+    auto store_unit = [&](int w, uint32_t col) {
       const int4 itm = __ldg(&p.items[item_of(w)]);
       const bool tail = t_s > 1 && w >= t_base;
       const int sp = tail ? (w - t_base) % t_s : w % p.n_split;
@@ -262,53 +373,66 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
       const int64_t tslot0 = tail ? __ldg(&p.items[t_base]).y : 0;
       int k0, k1;
       krange(w, k0, k1);
-      const uint32_t as = it & 1, use = it >> 1;
-      ++it;
-      mbar_wait(&tmem_full[as], use & 1);
-      tc_fence_after();
-      const int lrow = static_cast<int>(q * 32 + lane);  // 0..127
       const int n = itm.z;
-      const int na = B == 64 ? (n + 1) / 2 : 1;
+      const int na = n_acc(n);
 #pragma unroll 1
       for (int acc = 0; acc < na; ++acc) {
-      // accumulator acc holds blocks 2 acc (rows 0..63) and 2 acc + 1 (rows 64..127) for b = 64
-      const int bi = B == 64 ? 2 * acc + (lrow >> 6) : 0;
-      const int slot = bi < n ? itm.y + bi : -1;
-      const int li = B == 64 ? (lrow & 63) : lrow;
-      const int r = slot >= 0 ? block_row(slot) : -1;
-      const uint32_t tbase = tmem_base + ((q * 32u) << 16) + as * C::ACC_COLS + acc * B;
+        // accumulator acc holds blocks 2 acc (rows 0..63) and 2 acc + 1 (rows 64..127), b = 64
+        const int bi = B == 64 ? 2 * acc + (lrow >> 6) : 0;
+        const int slot = bi < n ? itm.y + bi : -1;
+        const int li = B == 64 ? (lrow & 63) : lrow;
+        const int r = slot >= 0 ? block_row(slot) : -1;
+        const uint32_t tbase = tmem_base + ((q * 32u) << 16) + col + acc * B;
 #pragma unroll 1
-      for (int ch = 0; ch < B / 16; ++ch) {
-        float v[16];
-        tmem_ld16(tbase + ch * 16, v);
-        if (k1 <= k0) {
+        for (int ch = 0; ch < B / 16; ++ch) {
+          float v[16];
+          tmem_ld16(tbase + ch * 16, v);
+          if (k1 <= k0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-        }
-        if (slot < 0) continue;
-        if (tail) {  // fp32 partial of a tail item, reduced in split order afterwards
-          float* dst = p.tail_partial + ((sp * p.tail_cap + (slot - tslot0)) * B + li) * B + ch * 16;
-          store_chunk16<float>(dst, v, 16, true);
-        } else if (p.n_split > 1) {  // fp32 partial, reduced in split order afterwards
-          const int64_t flat = p.dense_out ? static_cast<int64_t>(itm.x) * p.gr + r : slot;
-          float* dst = p.partial + ((sp * p.n_slots + flat) * B + li) * B + ch * 16;
-          store_chunk16<float>(dst, v, 16, true);
-        } else if (p.dense_out) {
-          const int64_t row = static_cast<int64_t>(r) * B + li;
-          const int64_t col = static_cast<int64_t>(itm.x) * B + ch * 16;
-          if (row < p.rows) {
-            const int valid = static_cast<int>(p.cols - col);
-            store_chunk16<float>(p.dense_out + row * p.cols + col, v, valid, (p.cols % 4) == 0);
+            for (int i = 0; i < 16; ++i) v[i] = 0.0f;
           }
-        } else {
-          float* dst = p.out_blocks + (static_cast<int64_t>(slot) * B + li) * B + ch * 16;
-          store_chunk16<float>(dst, v, 16, true);
+          if (slot < 0) continue;
+          if (tail) {  // fp32 partial of a tail item, reduced in split order afterwards
+            float* dst = p.tail_partial + ((sp * p.tail_cap + (slot - tslot0)) * B + li) * B + ch * 16;
+            store_chunk16<float>(dst, v, 16, true);
+          } else if (p.n_split > 1) {  // fp32 partial, reduced in split order afterwards
+            const int64_t flat = p.dense_out ? static_cast<int64_t>(itm.x) * p.gr + r : slot;
+            float* dst = p.partial + ((sp * p.n_slots + flat) * B + li) * B + ch * 16;
+            store_chunk16<float>(dst, v, 16, true);
+          } else if (p.dense_out) {
+            const int64_t row = static_cast<int64_t>(r) * B + li;
+            const int64_t col = static_cast<int64_t>(itm.x) * B + ch * 16;
+            if (row < p.rows) {
+              const int valid = static_cast<int>(p.cols - col);
+              store_chunk16<float>(p.dense_out + row * p.cols + col, v, valid, (p.cols % 4) == 0);
+            }
+          } else {
+            float* dst = p.out_blocks + (static_cast<int64_t>(slot) * B + li) * B + ch * 16;
+            store_chunk16<float>(dst, v, 16, true);
+          }
         }
       }
+    };
+    if (sweep) {
+      if (n_mine > 0) {
+        mbar_wait(&tmem_full[0], 0);
+        tc_fence_after();
+        for (int j = 0; j < n_mine; ++j) store_unit(unit(j), j * C::ACC_COLS);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[as]);
+    } else {
+      uint32_t it = 0;
+      for (int k = 0; k * G < n_work; ++k) {
+        const int w = unit(k);
+        if (w < 0) continue;
+        const uint32_t as = it & 1, use = it >> 1;
+        ++it;
+        mbar_wait(&tmem_full[as], use & 1);
+        tc_fence_after();
+        store_unit(w, as * C::ACC_COLS);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_empty[as]);
+      }
     }
   }
   tc_fence_before();
@@ -548,6 +672,7 @@ static int block_wgrad_impl(const void* a, const void* d, int64_t m, int64_t row
   }
   if (nsel == 0) return BLAST_OK;
   WgradParams p{};
+  p.sweep_ok = wgrad_sweep_enabled() ? 1 : 0;
   p.m = static_cast<int32_t>(m);
   p.rows = rows;
   p.cols = cols;
