@@ -82,6 +82,14 @@ struct WgCfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE + 256 + 1024;
   static_assert(STAGES >= 3 && 2 * ACC_COLS <= 512, "wgrad stage / accumulator budget");
 };
+static bool wgrad_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BLAST_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 // BLAST_WG_SWEEP=0 disables the sweep mode (WgradParams::sweep_ok)
 static bool wgrad_sweep_enabled() {
   static int v = -1;
@@ -141,6 +149,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the setup above may overlap the previous kernel's tail (programmatic dependent launch)
+  griddep_wait();
 
   auto block_row = [&](int slot) -> int { return p.row_of ? p.row_of[slot] : slot; };
   // k-th work unit of this CTA: round robin over the column-ordered list (-1: past the end)
@@ -587,7 +597,19 @@ static int launch_wgrad_tc(const void* a, const void* d, const WgradParams& p, c
   if (p.n_items <= 0) return BLAST_OK;
   const int64_t work = static_cast<int64_t>(p.n_items) * p.n_split;
   const int grid = static_cast<int>(work < num_sms() ? work : num_sms());
-  kern<<<grid, 256, C::SMEM_BYTES, st>>>(ma, md, p);
+  // programmatic dependent launch: barrier init / TMEM allocation on SMs freed by the previous
+  // kernel's tail (the kernel waits for its completion before reading); BLAST_PDL=0 disables
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = wgrad_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, ma, md, p);
   int rc = check_launch("wgrad_tc");
   if (rc == BLAST_OK && p.tail_partial) {  // no-op on the device when no tail split happened
     const int64_t total = std::min<int64_t>(p.n_slots, p.tail_cap) * B * B;
