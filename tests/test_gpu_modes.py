@@ -95,3 +95,56 @@ def test_gate_up_layouts_bitwise_equal(b, sp, tmp_path):
         assert res.returncode == 0, res.stderr[-2000:]
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+SCRIPT_BWD = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import oracle
+import paper_2507_03117_b200 as bs
+rng = np.random.default_rng(11)
+mats = []
+for rows, cols in ((1024, 4096), (1024, 4096), (4096, 1024)):
+    w = oracle.random_bcsc(rows, cols, 64, 0.6, rng)
+    w = w._replace(values=(w.values / np.sqrt(rows)).astype(np.float32))
+    mats.append(bs.from_host(w, torch.bfloat16))
+net = bs.SparseMlp.from_caches(*mats)
+x = torch.from_numpy(rng.standard_normal(({m}, 1024)).astype(np.float32)).cuda().bfloat16()
+dy = torch.from_numpy(rng.standard_normal(({m}, 1024)).astype(np.float32)).cuda().bfloat16()
+y, acts = bs.mlp_forward(x, net, save_activations=True)
+g = bs.mlp_backward(dy, acts, net, grad_mode="active")
+torch.cuda.synchronize()
+np.savez({out!r}, y=y.float().cpu().numpy(), a=acts.gate_pre.float().cpu().numpy(),
+         dx=g[0].float().cpu().numpy(), dwg=g[1].cpu().numpy(), dwu=g[2].cpu().numpy(),
+         dwd=g[3].cpu().numpy())
+"""
+
+MODES_BWD = {
+    "default": {},
+    "narrow_gating_backward": {"BLAST_WIDE_BWD2": "0"},
+    "round_robin_training_forward": {"BLAST_LPT_SAVE": "0"},
+    "wgrad_unit_by_unit": {"BLAST_WG_SWEEP": "0"},
+    "no_pdl": {"BLAST_PDL": "0"},
+}
+
+
+@pytest.mark.parametrize("m", [640, 3000])
+def test_training_modes_bitwise_equal(m, tmp_path):
+    """Training forward + backward (mlp.py:102-143): the 256-token gating backward, the LPT
+    schedule of the G/a/b-writing gate+up, the weight-gradient sweep mode and programmatic
+    dependent launch change no bit of Y, the saved activations, dX or the stored-block dW."""
+    def run(env_extra, name):
+        out = str(tmp_path / f"bwd_{name}_{m}.npz")
+        env = dict(os.environ, **env_extra)
+        res = subprocess.run([sys.executable, "-c", SCRIPT_BWD.format(root=str(ROOT), m=m, out=out)],
+                             env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        return np.load(out)
+    ref = run(MODES_BWD["default"], "default")
+    for name, env in MODES_BWD.items():
+        if name == "default":
+            continue
+        got = run(env, name)
+        for k in ref.files:
+            assert np.array_equal(got[k], ref[k]), (name, k)
