@@ -9,6 +9,9 @@
 //   sequence: t-major, within a tile the lines in descending cost (ties by index);
 //   batch k = the next `grid` items of the sequence; its largest item goes to the CTA with
 //   the least accumulated cost, the second largest to the second least loaded, ...
+//   (the lines are sorted once with a bitonic sort; a batch's items are ranked from their
+//   sorted-run positions and two binary searches, its CTAs by counting; three barriers
+//   per batch)
 //
 // Batches are consecutive slices of the t-major sequence, so the CTAs still sweep the token
 // tiles together (the activation panels of the tiles in flight stay in L2), and CTA c's
@@ -64,17 +67,17 @@ lpt_schedule_kernel(const int32_t* step_ptr, const int32_t* flags, int seq_gu, i
                     int n_tiles, int grid, int pl, int pg, int32_t* out) {
   extern __shared__ unsigned long long sm[];
   unsigned long long* lkey = sm;         // [pl] lines by descending cost
-  unsigned long long* bkey = lkey + pl;  // [pg] batch items by descending cost
-  unsigned long long* ckey = bkey + pg;  // [pg] CTAs by ascending load
-  int* cost = reinterpret_cast<int*>(ckey + pg);  // [n_lines]
-  int* order = cost + n_lines;                    // [n_lines]
-  int* load = order + n_lines;                    // [grid]
+  unsigned long long* ckey = lkey + pl;  // [pg] CTAs by ascending load
+  int* order = reinterpret_cast<int*>(ckey + pg);  // [n_lines] line of sorted index i
+  int* scost = order + n_lines;                    // [n_lines] its cost (descending)
+  int* load = scost + n_lines;                     // [grid]
+  int* item_at = load + grid;                      // [grid] batch item of rank k
+  int* cta_at = item_at + grid;                    // [grid] CTA of rank k
   constexpr unsigned long long kMax = ~0ull;
 
   for (int j = threadIdx.x; j < pl; j += blockDim.x) {
     if (j < n_lines) {
       const int c = line_cost(step_ptr, flags, seq_gu, j);
-      cost[j] = c;
       lkey[j] = (static_cast<unsigned long long>(0x7fffffff - c) << 32) | static_cast<unsigned>(j);
     } else {
       lkey[j] = kMax;
@@ -83,37 +86,80 @@ lpt_schedule_kernel(const int32_t* step_ptr, const int32_t* flags, int seq_gu, i
   for (int c = threadIdx.x; c < grid; c += blockDim.x) load[c] = 0;
   __syncthreads();
   bitonic_sort(lkey, pl);
-  for (int j = threadIdx.x; j < n_lines; j += blockDim.x) order[j] = static_cast<int>(lkey[j] & 0xffffffffu);
+  for (int i = threadIdx.x; i < n_lines; i += blockDim.x) {
+    order[i] = static_cast<int>(lkey[i] & 0xffffffffu);
+    scost[i] = 0x7fffffff - static_cast<int>(lkey[i] >> 32);
+  }
   __syncthreads();
 
   const long long total = static_cast<long long>(n_tiles) * n_lines;
   const long long rows = (total + grid - 1) / grid;
+  const unsigned L = static_cast<unsigned>(n_lines);
   for (long long r = 0; r < rows; ++r) {
     const long long p0 = r * grid;
     const int n = static_cast<int>(min(static_cast<long long>(grid), total - p0));
-    for (int k = threadIdx.x; k < pg; k += blockDim.x) {
-      if (k < n) {
-        const long long pos = p0 + k;
-        const int j = order[pos % n_lines];
-        bkey[k] = (static_cast<unsigned long long>(0x7fffffff - cost[j]) << 32) | static_cast<unsigned>(k);
-      } else {
-        bkey[k] = kMax;
+    // the batch = sequence positions [p0, p0 + n): one run of sorted indices per token tile
+    // t_first .. t_last, the first starting at sorted index off0
+    const long long t_first = p0 / n_lines;
+    const unsigned off0 = static_cast<unsigned>(p0 - t_first * n_lines);
+    const unsigned t_span = (off0 + static_cast<unsigned>(n) - 1u) / L;  // t_last - t_first
+    // Rank of batch item k under the key (-cost, k): inside its own run the items ahead of it
+    // are exactly the ones before it (a run is sorted by descending cost, ties by line = by
+    // k); of an earlier run those with cost >= its cost, of a later run those with cost >.
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const unsigned q = off0 + static_cast<unsigned>(k);
+      const unsigned tr = q / L, i = q - tr * L;  // tile (relative) and sorted index
+      const int c = scost[i];
+      int lo = 0, hi = n_lines;  // gt = #sorted lines with cost > c
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (scost[mid] > c) lo = mid + 1; else hi = mid;
       }
-      ckey[k] = k < grid ? (static_cast<unsigned long long>(load[k]) << 32) | static_cast<unsigned>(k)
-                         : kMax;
+      const unsigned gt = static_cast<unsigned>(lo);
+      hi = n_lines;  // ge = #sorted lines with cost >= c
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (scost[mid] >= c) lo = mid + 1; else hi = mid;
+      }
+      const unsigned ge = static_cast<unsigned>(lo);
+      unsigned rank = i - (tr == 0 ? off0 : 0u);
+      for (unsigned u = 0; u <= t_span; ++u) {
+        if (u == tr) continue;
+        const unsigned a = u == 0 ? off0 : 0u;
+        const unsigned b = u == t_span ? off0 + static_cast<unsigned>(n) - u * L : L;
+        const unsigned lim = u < tr ? ge : gt;
+        rank += (lim < a ? a : lim > b ? b : lim) - a;
+      }
+      item_at[rank] = k;
+    }
+    for (int k = threadIdx.x; k < grid; k += blockDim.x)
+      ckey[k] = (static_cast<unsigned long long>(load[k]) << 32) | static_cast<unsigned>(k);
+    __syncthreads();
+    // rank of every CTA by ascending load: four lanes per CTA count the smaller keys over a
+    // quarter of the CTAs each (all keys distinct), summed with two shuffles
+    for (int t4 = threadIdx.x; t4 < 4 * ((grid + 7) & ~7); t4 += blockDim.x) {
+      const int c = t4 >> 2, part = t4 & 3;
+      const bool valid = c < grid;
+      const unsigned long long me = valid ? ckey[c] : 0ull;
+      int rank = 0;
+      if (valid) {
+#pragma unroll 4
+        for (int s2 = part; s2 < grid; s2 += 4) rank += ckey[s2] < me ? 1 : 0;
+      }
+      rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+      rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+      if (valid && part == 0) cta_at[rank] = c;
     }
     __syncthreads();
-    bitonic_sort(bkey, pg);
-    bitonic_sort(ckey, pg);
+    // the k-th largest item of the batch to the k-th least loaded CTA
     for (int k = threadIdx.x; k < grid; k += blockDim.x) {
-      const int cta = static_cast<int>(ckey[k] & 0xffffffffu);
+      const int cta = cta_at[k];
       int item = -1;
       if (k < n) {
-        const long long pos = p0 + static_cast<long long>(bkey[k] & 0xffffffffu);
-        const int t = static_cast<int>(pos / n_lines);
-        const int j = order[pos % n_lines];
-        item = t * n_lines + j;
-        load[cta] += cost[j];
+        const unsigned q = off0 + static_cast<unsigned>(item_at[k]);
+        const unsigned tr = q / L, i = q - tr * L;
+        item = static_cast<int>((t_first + tr) * n_lines + order[i]);
+        load[cta] += scost[i];
       }
       out[r * grid + cta] = item;
     }
@@ -135,7 +181,7 @@ static int launch_lpt_schedule(const int32_t* step_ptr, const int32_t* flags, in
     return BLAST_EINVAL;
   }
   const int pl = next_pow2(n_lines), pg = next_pow2(grid);
-  const size_t smem = sizeof(unsigned long long) * (pl + 2 * pg) + sizeof(int) * (2 * n_lines + grid);
+  const size_t smem = sizeof(unsigned long long) * (pl + pg) + sizeof(int) * (2 * n_lines + 3 * grid);
   static bool configured[64] = {};
   if (int rc = configure_smem(lpt_schedule_kernel, 160 * 1024, configured, "schedule smem attribute"))
     return rc;

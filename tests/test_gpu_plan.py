@@ -87,7 +87,8 @@ def lpt_reference(costs, n_tiles, grid):
 
 @pytest.mark.parametrize("gr,gc,density,n_tiles,grid,seq",
                          [(64, 64, 0.1, 32, 148, 0), (64, 224, 0.1, 32, 148, 1),
-                          (12, 48, 0.3, 5, 148, 0), (8, 8, 0.5, 3, 7, 1)])
+                          (12, 48, 0.3, 5, 148, 0), (8, 8, 0.5, 3, 7, 1),
+                          (4, 5, 0.5, 50, 37, 0), (64, 1000, 0.1, 3, 148, 1)])
 def test_balanced_schedule(gr, gc, density, n_tiles, grid, seq):
     from paper_2507_03117_b200 import _lib as L
     rng = np.random.default_rng(gr * gc + n_tiles)
