@@ -453,3 +453,48 @@ def save(w: BlockSparseMatrix, path) -> None:
 def load(path, dtype: torch.dtype = torch.float32) -> BlockSparseMatrix:
     with open(path, "rb") as fh:
         return deserialize(fh.read(), dtype)
+
+
+def write_dense_file(dense, path) -> None:
+    """Dense float32 matrix in the raw little-endian ``DNSE`` interchange format
+    (header magic, rows, cols, 0; then row-major f32), as bcsc.py:292-300."""
+    d = dense.detach().float().cpu().numpy() if isinstance(dense, torch.Tensor) else \
+        np.asarray(dense, dtype=np.float32)
+    if d.ndim != 2:
+        raise ValueError("expected a 2-D matrix")
+    rows, cols = d.shape
+    with open(path, "wb") as fh:
+        fh.write(_DENSE_HEADER.pack(DENSE_MAGIC, rows, cols, 0))
+        fh.write(np.ascontiguousarray(d).astype("<f4").tobytes())
+
+
+def read_dense_file(path) -> np.ndarray:
+    """Inverse of write_dense_file with the reference's checks (bcsc.py:303-314)."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if len(data) < _DENSE_HEADER.size:
+        raise FormatError("truncated stream: incomplete dense header")
+    magic, rows, cols, _ = _DENSE_HEADER.unpack_from(data)
+    if magic != DENSE_MAGIC:
+        raise FormatError(f"bad magic {magic!r}, expected {DENSE_MAGIC!r}")
+    need = _DENSE_HEADER.size + rows * cols * 4
+    if len(data) != need:
+        raise FormatError(f"dense payload size mismatch: expected {need} bytes, got {len(data)}")
+    return np.frombuffer(data, "<f4", rows * cols, _DENSE_HEADER.size).astype(np.float32).reshape(rows, cols)
+
+
+def convert(input_path, output_path, block_size: int = 64):
+    """The reference's ``convert`` command as a library call (cli.py:231-247): a ``DNSE``
+    dense file becomes a ``BCSC`` file (every block holding a nonzero stored, repacked on the
+    GPU), a ``BCSC`` file becomes a ``DNSE`` dense file. Returns the matrix written."""
+    with open(input_path, "rb") as fh:
+        magic = fh.read(4)
+    if magic == DENSE_MAGIC:
+        w = from_dense(read_dense_file(input_path), block_size)
+        save(w, output_path)
+        return w
+    if magic == MAGIC:
+        dense = to_dense(load(input_path))
+        write_dense_file(dense, output_path)
+        return dense
+    raise FormatError(f"{input_path}: unrecognized magic {magic!r} (expected DNSE or BCSC)")

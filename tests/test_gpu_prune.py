@@ -72,6 +72,18 @@ class TestGoldenFormat:
             w2 = bs.deserialize(d[f"c{i}_bytes"].tobytes())
             assert_cache_equal(w2, golden_bcsc(d, f"c{i}_mask"))
 
+    def test_convert_matches_reference_files(self, tmp_path):
+        # cli.py:231-247 (convert): DNSE -> BCSC bytes identical to the file the reference
+        # wrote for the same input (tests/golden/make_dense_files.py), and back to DNSE
+        from pathlib import Path
+        gdir = Path(__file__).resolve().parent / "golden"
+        d = self.d
+        w = bs.convert(gdir / "c1.dnse", tmp_path / "c1.bcsc", int(d["c1_b"]))
+        assert (tmp_path / "c1.bcsc").read_bytes() == (gdir / "c1.bcsc").read_bytes()
+        assert_cache_equal(w, golden_bcsc(d, "c1_auto"))
+        bs.convert(tmp_path / "c1.bcsc", tmp_path / "back.dnse")
+        assert (tmp_path / "back.dnse").read_bytes() == (gdir / "c1_back.dnse").read_bytes()
+
 
 class TestPruneS:
     def test_count_exactness(self):

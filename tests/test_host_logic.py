@@ -58,3 +58,35 @@ def test_train_config_rejects_unknown_fields():
         trainer.TrainConfig.from_dict({"schedule": {"bogus": 2}})
     with pytest.raises(ValueError, match="schedule"):
         trainer.TrainConfig.from_dict({"schedule": 3})
+
+
+GOLDEN_DIR = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+
+
+def test_dense_file_bytes_match_reference(tmp_path):
+    # bcsc.py:292-314: c1.dnse was written by the reference's write_dense_file
+    d = golden("format")
+    ref = (GOLDEN_DIR / "c1.dnse").read_bytes()
+    from paper_2507_03117_b200 import bcsc
+    out = tmp_path / "c1.dnse"
+    bcsc.write_dense_file(d["c1_dense"], out)
+    assert out.read_bytes() == ref
+    np.testing.assert_array_equal(bcsc.read_dense_file(GOLDEN_DIR / "c1.dnse"), d["c1_dense"])
+
+
+def test_dense_file_errors(tmp_path):
+    from paper_2507_03117_b200 import bcsc
+    with pytest.raises(ValueError, match="2-D"):
+        bcsc.write_dense_file(np.zeros(3, np.float32), tmp_path / "x")
+    good = (GOLDEN_DIR / "c1.dnse").read_bytes()
+    for name, data, msg in [("short", good[:8], "incomplete dense header"),
+                            ("magic", b"XXXX" + good[4:], "bad magic"),
+                            ("size", good + b"\0", "size mismatch")]:
+        f = tmp_path / name
+        f.write_bytes(data)
+        with pytest.raises(bcsc.FormatError, match=msg):
+            bcsc.read_dense_file(f)
+    f = tmp_path / "other"
+    f.write_bytes(b"ABCD" + good[4:])
+    with pytest.raises(bcsc.FormatError, match="unrecognized magic"):
+        bcsc.convert(f, tmp_path / "out", 4)
