@@ -272,3 +272,52 @@ def test_device_refresh_without_host_round_trips():
     assert_bits_equal(hd.values, hh.values)
     ref = oracle.apply_mask(w, oracle.generate_masks(w, g, b, s)[0], b)
     assert_cache_equal(cache_d, ref[1])
+
+
+def _fixed_order_norms(x: np.ndarray, b: int, vw: int) -> np.ndarray:
+    """The kernels' summation order in numpy: lane l of a block's warp adds the squares of the
+    16-byte vectors e = l, l + 32, ... (row-major, vw elements each, in order) in float64, then
+    the lanes combine by the xor-shuffle tree 16, 8, 4, 2, 1. A float32 / bfloat16 square is
+    exact in float64, so fma(x, x, acc) == acc + x * x here."""
+    rows, cols = x.shape
+    gr, gc = rows // b, cols // b
+    per_row = b // vw
+    out = np.empty((gr, gc))
+    for r in range(gr):
+        for c in range(gc):
+            blk = x[r * b:(r + 1) * b, c * b:(c + 1) * b].astype(np.float64).reshape(b * per_row, vw)
+            lanes = np.zeros(32)
+            for lane in range(32):
+                acc = 0.0
+                for v in blk[lane::32]:
+                    for e in v:
+                        acc = acc + e * e
+                lanes[lane] = acc
+            for o in (16, 8, 4, 2, 1):
+                lanes = lanes + lanes[np.arange(32) ^ o]
+            out[r, c] = np.sqrt(lanes[0])
+    return out
+
+
+@pytest.mark.parametrize("dtype,b,shape", [(torch.float32, 64, (128, 320)),
+                                           (torch.float32, 32, (64, 288)),
+                                           (torch.float32, 128, (256, 384)),
+                                           (torch.bfloat16, 64, (192, 448)),
+                                           (torch.bfloat16, 32, (96, 256))])
+def test_block_norms_fixed_order_bitwise(dtype, b, shape):
+    # the TMA-staged norms kernel (tiles of up to 256 columns, partial last tile) and the
+    # per-warp kernel share one summation order; check it bit for bit
+    rng = np.random.default_rng(b + shape[1])
+    x = torch.from_numpy(rng.standard_normal(shape).astype(np.float32) * 3).cuda().to(dtype)
+    g = (x * 0.5).contiguous()
+    from paper_2507_03117_b200 import _lib as L
+    gr, gc = shape[0] // b, shape[1] // b
+    nw = torch.empty(gr, gc, dtype=torch.float64, device="cuda")
+    ng = torch.empty_like(nw)
+    L.check(L.load().blast_block_norms(x.data_ptr(), g.data_ptr(), shape[0], shape[1], b,
+                                       L.dtype_code(dtype), nw.data_ptr(), ng.data_ptr(),
+                                       L.stream()), "norms")
+    vw = 4 if dtype == torch.float32 else 8
+    for t, n in ((x, nw), (g, ng)):
+        ref = _fixed_order_norms(t.float().cpu().numpy(), b, vw)
+        assert np.array_equal(n.cpu().numpy().view(np.uint64), ref.view(np.uint64))
