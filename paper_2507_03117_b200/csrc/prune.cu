@@ -11,6 +11,7 @@
 // norms are bitwise reproducible run to run.
 #include "activations.cuh"
 #include "host.hpp"
+#include "ptx.cuh"
 
 namespace blast {
 
@@ -277,11 +278,16 @@ __device__ __forceinline__ void topk_pick_bucket(const unsigned int* hist, unsig
 
 constexpr int kTopkSmemMax = 24576;
 
+// regrown / counts (optional, two grids): the fused set difference of pruner.py:142-156 —
+// launched as a cluster of the two CTAs, CTA 1 (grad_sel) waits for CTA 0's kept grid at the
+// cluster barrier and writes regrown = grad_sel & ~kept (regrown may alias keep1) and the
+// (kept, regrown) counts.
 __global__ void __launch_bounds__(1024) topk_smem_kernel(const double* __restrict__ norms0,
-                                                         uint8_t* __restrict__ keep0,
+                                                         uint8_t* keep0,
                                                          const double* __restrict__ norms1,
-                                                         uint8_t* __restrict__ keep1, int64_t gr,
-                                                         int64_t gc, int64_t k) {
+                                                         uint8_t* keep1, int64_t gr,
+                                                         int64_t gc, int64_t k, uint8_t* regrown,
+                                                         unsigned long long* counts) {
   extern __shared__ uint64_t keys[];
   __shared__ unsigned int hist[256];
   __shared__ unsigned int sel_bucket, sel_below;
@@ -401,6 +407,43 @@ __global__ void __launch_bounds__(1024) topk_smem_kernel(const double* __restric
       kp = static_cast<uint32_t>(c * gr + r) <= pre2;
     }
     keep[idx] = kp ? 1 : 0;
+  }
+  if (counts != nullptr) {
+    cluster_sync();  // release / acquire: CTA 0's kept grid is visible to CTA 1
+    if (blockIdx.x == 1) {
+      unsigned long long ck = 0, cr = 0;
+      for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+        const bool kp = keep0[idx] != 0;
+        const bool rg = keep1[idx] != 0 && !kp;
+        regrown[idx] = rg ? 1 : 0;
+        ck += kp;
+        cr += rg;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ck += __shfl_xor_sync(0xffffffffu, ck, o);
+        cr += __shfl_xor_sync(0xffffffffu, cr, o);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        red_and[threadIdx.x >> 5] = ck;
+        red_or[threadIdx.x >> 5] = cr;
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int nw = static_cast<int>(blockDim.x >> 5);
+        ck = threadIdx.x < nw ? red_and[threadIdx.x] : 0ull;
+        cr = threadIdx.x < nw ? red_or[threadIdx.x] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ck += __shfl_xor_sync(0xffffffffu, ck, o);
+          cr += __shfl_xor_sync(0xffffffffu, cr, o);
+        }
+        if (threadIdx.x == 0) {
+          counts[0] = ck;
+          counts[1] = cr;
+        }
+      }
+    }
   }
 }
 
@@ -527,6 +570,59 @@ __global__ void kmap_assign_kernel(const uint8_t* kept, const uint8_t* regrown,
     const unsigned bal = __ballot_sync(0xffffffffu, s);
     if (r < gr) kmap[idx] = s ? static_cast<int32_t>(out + __popc(bal & ((1u << lane) - 1u))) : -1;
     out += __popc(bal);
+  }
+}
+
+// count -> scan -> kmap in ONE single-CTA launch for grids of up to kRepackOneCta columns
+// (three launches otherwise): a warp per column counts with ballots into shared memory, warp 0
+// scans the counts, then the warps assign ranks exactly as kmap_assign_kernel does.
+constexpr int kRepackOneCta = 4096;
+__global__ void __launch_bounds__(1024) repack_index_one_cta_kernel(
+    const uint8_t* kept, const uint8_t* regrown, const uint8_t* store, int64_t gr, int64_t gc,
+    int64_t* col_ptr, int32_t* kmap) {
+  __shared__ int64_t cnt[kRepackOneCta + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  auto stored = [&](int64_t idx) {
+    return store ? store[idx] != 0 : ((kept && kept[idx]) || (regrown && regrown[idx]));
+  };
+  for (int64_t c = wid; c < gc; c += nw) {
+    int64_t n = 0;
+    for (int64_t base = 0; base < gr; base += 32) {
+      const int64_t r = base + lane;
+      n += __popc(__ballot_sync(0xffffffffu, r < gr && stored(r * gc + c)));
+    }
+    if (lane == 0) cnt[c + 1] = n;
+  }
+  if (threadIdx.x == 0) cnt[0] = 0;
+  __syncthreads();
+  if (wid == 0) {  // inclusive scan of cnt[1..gc]: 32 contiguous chunks, one per lane
+    const int64_t per = (gc + 31) / 32;
+    const int64_t lo = 1 + lane * per, hi = min(gc + 1, lo + per);
+    int64_t sum = 0;
+    for (int64_t i = lo; i < hi; ++i) sum += cnt[i];
+    int64_t pre = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
+    }
+    int64_t run = pre - sum;
+    for (int64_t i = lo; i < hi; ++i) {
+      run += cnt[i];
+      cnt[i] = run;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i <= gc; i += blockDim.x) col_ptr[i] = cnt[i];
+  for (int64_t c = wid; c < gc; c += nw) {
+    int64_t out = cnt[c];
+    for (int64_t base = 0; base < gr; base += 32) {
+      const int64_t r = base + lane;
+      const bool sd = r < gr && stored(r * gc + c);
+      const unsigned bal = __ballot_sync(0xffffffffu, sd);
+      if (r < gr)
+        kmap[r * gc + c] = sd ? static_cast<int32_t>(out + __popc(bal & ((1u << lane) - 1u))) : -1;
+      out += __popc(bal);
+    }
   }
 }
 
@@ -668,13 +764,32 @@ __global__ void sumsq_final_kernel(const double* partial, int n, double* out) {
 }
 
 static int topk_smem_launch(const double* n0, uint8_t* k0, const double* n1, uint8_t* k1,
-                            int64_t gr, int64_t gc, int64_t k, cudaStream_t st) {
+                            int64_t gr, int64_t gc, int64_t k, cudaStream_t st,
+                            uint8_t* regrown = nullptr, int64_t* counts = nullptr) {
   static bool configured[64] = {};
   const int smem = kTopkSmemMax * 8;
   if (int rc = configure_smem(topk_smem_kernel, smem, configured, "topk smem attribute")) return rc;
   const int n = static_cast<int>(gr * gc);
-  topk_smem_kernel<<<n1 ? 2 : 1, 1024, n * 8, st>>>(n0, k0, n1, k1, gr, gc, k);
-  return check_launch("topk_smem");
+  if (!(n1 && counts)) {
+    topk_smem_kernel<<<n1 ? 2 : 1, 1024, n * 8, st>>>(n0, k0, n1, k1, gr, gc, k, nullptr, nullptr);
+    return check_launch("topk_smem");
+  }
+  // both grids + the set difference: one cluster of two CTAs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = static_cast<size_t>(n) * 8;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, topk_smem_kernel, n0, k0, n1, k1, gr, gc, k, regrown,
+                     reinterpret_cast<unsigned long long*>(counts));
+  return check_launch("topk_smem (fused difference)");
 }
 
 static int grid_for(int64_t n, int threads, int per_sm = 16) {
@@ -802,10 +917,15 @@ extern "C" int blast_generate_masks(const void* w, int dtype_w, const void* g, i
   int r = norms_any(w, dtype_w, g, dtype_g, rows, cols, block, norms_w, norms_g, st);
   if (r) return r;
   const int64_t gr = cdiv(rows, block), gc = cdiv(cols, block);
-  // grad_sel goes into `regrown` and is turned into grad_sel & ~kept in place
-  r = blast_topk_mask2(norms_w, norms_g, gr, gc, k, kept, regrown, stream);
-  if (r) return r;
-  r = blast_mask_difference(kept, regrown, gr * gc, regrown, counts, stream);
+  // grad_sel goes into `regrown` and is turned into grad_sel & ~kept in place; for grids that
+  // fit one CTA's shared memory the difference and the counts run inside the top-k launch
+  const int64_t n = gr * gc;
+  if (n > 0 && k > 0 && k < n && n <= kTopkSmemMax) {
+    r = topk_smem_launch(norms_w, kept, norms_g, regrown, gr, gc, k, st, regrown, counts);
+  } else {
+    r = blast_topk_mask2(norms_w, norms_g, gr, gc, k, kept, regrown, stream);
+    if (!r) r = blast_mask_difference(kept, regrown, n, regrown, counts, stream);
+  }
   if (r) return r;
   if (counts_host) {
     cudaError_t e = cudaMemcpyAsync(counts_host, counts, 2 * sizeof(int64_t),
@@ -839,6 +959,10 @@ extern "C" int blast_repack_index(const uint8_t* kept, const uint8_t* regrown, c
     store = s.as<uint8_t>();
   }
   const int blocks = static_cast<int>(cdiv(gc * 32, 256));
+  if (gc <= kRepackOneCta) {
+    repack_index_one_cta_kernel<<<1, 1024, 0, st>>>(kept, regrown, store, gr, gc, col_ptr, kmap);
+    return check_launch("repack_index");
+  }
   col_count_kernel<<<blocks, 256, 0, st>>>(kept, regrown, store, gr, gc, col_ptr);
   scan_i64_kernel<<<1, 1024, 0, st>>>(col_ptr, gc);
   kmap_assign_kernel<<<blocks, 256, 0, st>>>(kept, regrown, store, gr, gc, col_ptr, kmap);
