@@ -403,6 +403,14 @@ __device__ __forceinline__ void bulk_wait_group() {
 // Blocks until the grid this one depends on (launched with programmatic stream serialization)
 // has completed and its memory is visible; a no-op for a normal launch.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef BLAST_EARLY_TRIGGER
+#define BLAST_EARLY_TRIGGER 1
+#endif
+// Lets the next PDL-launched kernel on the stream start its prologue on SMs this grid frees;
+// the dependent still waits (griddepcontrol.wait) for this grid's completion and memory flush.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // ---------------------------------------------------------------- misc
 // Shared-memory word read that the compiler cannot hoist above a preceding barrier wait

@@ -236,6 +236,7 @@ static int launch_tc(const EngineCall& c, const void* a0lo, const void* a1lo, cu
   const int64_t items = static_cast<int64_t>(p.n_tok_tiles) * p.n_lines;
   if (items <= 0) return BLAST_OK;
   const int grid = static_cast<int>(std::min<int64_t>(items, num_sms()));
+  p.early_trigger = items < 2 * static_cast<int64_t>(num_sms()) ? 1 : 0;
   // Persistent CTAs of single-matrix products take cost-balanced item lists (csrc/schedule.cu).
   // Same box, cfg3 (profiles/r02/cta_spans.txt): down 111.3 -> 108.0 us (CTA ends within 8.6
   // instead of 18.0 us); the gate+up kernel got slower (238.7 -> 243.0 us) although its CTAs
