@@ -45,28 +45,43 @@ def timed(fn, iters=10, warmup=3):
 
 
 def cfg3_sweep():
-    d, h, m = 4096, 14336, 8192
-    x = torch.randn(m, d, device="cuda").bfloat16()
-    wg = torch.randn(h, d, device="cuda", dtype=torch.bfloat16) * d ** -0.5
-    wu = torch.randn(h, d, device="cuda", dtype=torch.bfloat16) * d ** -0.5
-    wd = torch.randn(d, h, device="cuda", dtype=torch.bfloat16) * h ** -0.5
-    dense_ms = timed(lambda: F.linear(F.silu(F.linear(x, wg)) * F.linear(x, wu), wd))
-    del wg, wu, wd
+    """argv: cfg3 [blocks] [token counts] [sparsities], comma lists."""
+    d, h = 4096, 14336
     peak = bench.load_peaks()[1]
+    hbm = bench.load_peaks()[0]
     blocks = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else (16, 32, 64, 128)
-    for b in blocks:
-        for s in (0.5, 0.7, 0.8, 0.9, 0.95):
-            ws = bench.make_weights(d, h, b, s, 0)
-            net = bs.SparseMlp.from_caches(*[bs.from_host(w, torch.bfloat16) for w in ws])
-            ms = timed(lambda: bs.mlp_forward(x, net, save_activations=False))
-            fl = 2 * m * b * b * sum(w.cache.nnzb for w in net.matrices())
-            print(json.dumps({"config": "cfg3", "block": b, "sparsity": s, "tokens": m,
-                              "sparse_ms": ms, "dense_cublas_ms": dense_ms,
-                              "speedup_vs_dense": dense_ms / ms,
-                              "tokens_per_s": m / (ms * 1e-3),
-                              "tflops": fl / (ms * 1e-3) / 1e12,
-                              "frac_of_peak": fl / (ms * 1e-3) / 1e12 / peak}), flush=True)
-            del net
+    ms_list = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else (8192,)
+    sps = [float(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else (0.5, 0.7, 0.8, 0.9, 0.95)
+    for m in ms_list:
+        x = torch.randn(m, d, device="cuda").bfloat16()
+        wg = torch.randn(h, d, device="cuda", dtype=torch.bfloat16) * d ** -0.5
+        wu = torch.randn(h, d, device="cuda", dtype=torch.bfloat16) * d ** -0.5
+        wd = torch.randn(d, h, device="cuda", dtype=torch.bfloat16) * h ** -0.5
+        dense_ms = timed(lambda: F.linear(F.silu(F.linear(x, wg)) * F.linear(x, wu), wd))
+        del wg, wu, wd
+        for b in blocks:
+            for s in sps:
+                ws = bench.make_weights(d, h, b, s, 0)
+                net = bs.SparseMlp.from_caches(*[bs.from_host(w, torch.bfloat16) for w in ws])
+                ms = timed(lambda: bs.mlp_forward(x, net, save_activations=False))
+                nnzb = sum(w.cache.nnzb for w in net.matrices())
+                fl = 2 * m * b * b * nnzb
+                # roofline of the north star: the slower of nnz-block FLOPs at tensor peak and
+                # nonzero-weight + activation (X in, Y out) bytes at HBM bandwidth
+                byts = nnzb * b * b * 2 + 2 * m * d * 2
+                t_fl, t_by = fl / (peak * 1e12) * 1e3, byts / (hbm * 1e9) * 1e3
+                print(json.dumps({"config": "cfg3", "block": b, "sparsity": s, "tokens": m,
+                                  "sparse_ms": ms, "dense_cublas_ms": dense_ms,
+                                  "speedup_vs_dense": dense_ms / ms,
+                                  "tokens_per_s": m / (ms * 1e-3),
+                                  "tflops": fl / (ms * 1e-3) / 1e12,
+                                  "frac_of_peak": fl / (ms * 1e-3) / 1e12 / peak,
+                                  "bound": "tensor" if t_fl >= t_by else "hbm",
+                                  "roofline_ms": max(t_fl, t_by),
+                                  "frac_roofline": max(t_fl, t_by) / ms,
+                                  "hbm_gbs": byts / (ms * 1e-3) / 1e9}), flush=True)
+                del net
+        del x
 
 
 def cfg1_e2e():
