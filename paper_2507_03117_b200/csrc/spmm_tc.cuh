@@ -658,6 +658,41 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
     }
     return;
   }
+  if constexpr (EPI == EPI_GATED_FWD && OUT_SW > 0 && NCH <= 4 && ACC_W == B) {
+    // Staged gated forward (inference): both accumulators and the SiLU-mul of this thread's
+    // chunks (c = half, half + 2) before the output-staging wait, so they overlap the previous
+    // tile's TMA store still reading the staging buffer (as the gating backward above). Same
+    // arithmetic as epilogue_chunk; a / b outputs requested alongside take the general path.
+    if (!p.out1 && !p.out2) {
+      uint32_t r0[2][16], r1[2][16];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (half + 2 * k < NCH) {
+          tmem_ld16_nowait(tacc + (half + 2 * k) * 16, r0[k]);
+          tmem_ld16_nowait(tacc + ACC_W + (half + 2 * k) * 16, r1[k]);
+        }
+      tmem_wait_ld();
+      const bool a_init = (flags & 1) != 0, b_init = (flags & 2) != 0;
+      float g[2][16];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float a = a_init ? __uint_as_float(r0[k][i]) : 0.0f;
+          const float b = b_init ? __uint_as_float(r1[k][i]) : 0.0f;
+          if constexpr (sizeof(OutT) == 2)
+            g[k][i] = gated_fwd_fast(a, b);
+          else
+            g[k][i] = gated_fwd(a, b);
+        }
+      if (etid == 0) bulk_wait_group_read<NBUF - 1>();
+      named_bar_sync(1, kEpiWarpsT * 32);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (half + 2 * k < NCH) stage_chunk16<OutT, OUT_SW>(stg, trow, (half + 2 * k) * 16, g[k]);
+      return;
+    }
+  }
   if constexpr (OUT_SW > 0) {
     if (etid == 0) bulk_wait_group_read<NBUF - 1>();
     named_bar_sync(1, kEpiWarpsT * 32);
