@@ -573,25 +573,48 @@ __global__ void kmap_assign_kernel(const uint8_t* kept, const uint8_t* regrown,
   }
 }
 
-// count -> scan -> kmap in ONE single-CTA launch for grids of up to kRepackOneCta columns
-// (three launches otherwise): a warp per column counts with ballots into shared memory, warp 0
-// scans the counts, then the warps assign ranks exactly as kmap_assign_kernel does.
+// count -> scan -> kmap in ONE single-CTA launch for grids of up to kRepackOneCtaCells cells and
+// kRepackOneCta columns (three launches otherwise): the store flags are read once, coalesced,
+// into shared memory; a warp per column counts them with ballots, warp 0 scans the counts, and
+// the warps assign ranks exactly as kmap_assign_kernel does.
 constexpr int kRepackOneCta = 4096;
+constexpr int kRepackOneCtaCells = 98304;
 __global__ void __launch_bounds__(1024) repack_index_one_cta_kernel(
     const uint8_t* kept, const uint8_t* regrown, const uint8_t* store, int64_t gr, int64_t gc,
     int64_t* col_ptr, int32_t* kmap) {
   __shared__ int64_t cnt[kRepackOneCta + 1];
+  extern __shared__ __align__(16) uint8_t sflag[];  // [gr * gc] row-major store flags (nonzero)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  auto stored = [&](int64_t idx) {
-    return store ? store[idx] != 0 : ((kept && kept[idx]) || (regrown && regrown[idx]));
-  };
+  const int n = static_cast<int>(gr * gc);
+  // nonzero = stored; 16 flags per load when the grids allow it (one round trip for cfg3)
+  const bool vec = (n % 16) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(kept) | reinterpret_cast<uintptr_t>(regrown) |
+                     reinterpret_cast<uintptr_t>(store)) & 15u) == 0;
+  if (vec) {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < n / 16; i += blockDim.x) {
+      uint4 v;
+      if (store) {
+        v = reinterpret_cast<const uint4*>(store)[i];
+      } else {
+        const uint4 a = kept ? reinterpret_cast<const uint4*>(kept)[i] : z;
+        const uint4 b = regrown ? reinterpret_cast<const uint4*>(regrown)[i] : z;
+        v = make_uint4(a.x | b.x, a.y | b.y, a.z | b.z, a.w | b.w);
+      }
+      reinterpret_cast<uint4*>(sflag)[i] = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      sflag[i] = store ? (store[i] != 0) : ((kept && kept[i]) || (regrown && regrown[i]));
+  }
+  __syncthreads();
   for (int64_t c = wid; c < gc; c += nw) {
-    int64_t n = 0;
+    int64_t cn = 0;
     for (int64_t base = 0; base < gr; base += 32) {
       const int64_t r = base + lane;
-      n += __popc(__ballot_sync(0xffffffffu, r < gr && stored(r * gc + c)));
+      cn += __popc(__ballot_sync(0xffffffffu, r < gr && sflag[r * gc + c]));
     }
-    if (lane == 0) cnt[c + 1] = n;
+    if (lane == 0) cnt[c + 1] = cn;
   }
   if (threadIdx.x == 0) cnt[0] = 0;
   __syncthreads();
@@ -617,7 +640,7 @@ __global__ void __launch_bounds__(1024) repack_index_one_cta_kernel(
     int64_t out = cnt[c];
     for (int64_t base = 0; base < gr; base += 32) {
       const int64_t r = base + lane;
-      const bool sd = r < gr && stored(r * gc + c);
+      const bool sd = r < gr && sflag[r * gc + c];
       const unsigned bal = __ballot_sync(0xffffffffu, sd);
       if (r < gr)
         kmap[r * gc + c] = sd ? static_cast<int32_t>(out + __popc(bal & ((1u << lane) - 1u))) : -1;
@@ -959,9 +982,15 @@ extern "C" int blast_repack_index(const uint8_t* kept, const uint8_t* regrown, c
     store = s.as<uint8_t>();
   }
   const int blocks = static_cast<int>(cdiv(gc * 32, 256));
-  if (gc <= kRepackOneCta) {
-    repack_index_one_cta_kernel<<<1, 1024, 0, st>>>(kept, regrown, store, gr, gc, col_ptr, kmap);
-    return check_launch("repack_index");
+  if (gc <= kRepackOneCta && gr * gc <= kRepackOneCtaCells) {
+    static bool configured[64] = {};
+    if (configure_smem(repack_index_one_cta_kernel, kRepackOneCtaCells, configured,
+                       "repack smem attribute") == 0) {
+      repack_index_one_cta_kernel<<<1, 1024, static_cast<size_t>(gr * gc), st>>>(
+          kept, regrown, store, gr, gc, col_ptr, kmap);
+      return check_launch("repack_index");
+    }
+    cudaGetLastError();
   }
   col_count_kernel<<<blocks, 256, 0, st>>>(kept, regrown, store, gr, gc, col_ptr);
   scan_i64_kernel<<<1, 1024, 0, st>>>(col_ptr, gc);
