@@ -658,12 +658,15 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
     }
     return;
   }
-  if constexpr (EPI == EPI_GATED_FWD && OUT_SW > 0 && NCH <= 4 && ACC_W == B) {
-    // Staged gated forward (inference): both accumulators and the SiLU-mul of this thread's
-    // chunks (c = half, half + 2) before the output-staging wait, so they overlap the previous
-    // tile's TMA store still reading the staging buffer (as the gating backward above). Same
-    // arithmetic as epilogue_chunk; a / b outputs requested alongside take the general path.
-    if (!p.out1 && !p.out2) {
+  if constexpr ((EPI == EPI_GATED_FWD || EPI == EPI_GATED_FWD_SAVE) && OUT_SW > 0 && NCH <= 4 &&
+                ACC_W == B) {
+    // Staged gated forward: both accumulators and the SiLU-mul of this thread's chunks
+    // (c = half, half + 2) before the output-staging wait, so they overlap the previous tile's
+    // TMA store still reading the staging buffer (as the gating backward above). Same
+    // arithmetic as epilogue_chunk. The inference form with a / b requested as direct outputs
+    // takes the general path; the training form stages a and b next to G.
+    constexpr bool kSave = EPI == EPI_GATED_FWD_SAVE;
+    if (kSave || (!p.out1 && !p.out2)) {
       uint32_t r0[2][16], r1[2][16];
 #pragma unroll
       for (int k = 0; k < 2; ++k)
@@ -688,8 +691,21 @@ __device__ __forceinline__ void epi_tile_compute(const SpmmParams& p, uint32_t t
       if (etid == 0) bulk_wait_group_read<NBUF - 1>();
       named_bar_sync(1, kEpiWarpsT * 32);
 #pragma unroll
-      for (int k = 0; k < 2; ++k)
-        if (half + 2 * k < NCH) stage_chunk16<OutT, OUT_SW>(stg, trow, (half + 2 * k) * 16, g[k]);
+      for (int k = 0; k < 2; ++k) {
+        const int c = half + 2 * k;
+        if (c >= NCH) break;
+        stage_chunk16<OutT, OUT_SW>(stg, trow, c * 16, g[k]);
+        if constexpr (kSave) {
+          float a[16], b[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            a[i] = a_init ? __uint_as_float(r0[k][i]) : 0.0f;
+            b[i] = b_init ? __uint_as_float(r1[k][i]) : 0.0f;
+          }
+          stage_chunk16<OutT, OUT_SW>(stg + out1_off, trow, c * 16, a);
+          stage_chunk16<OutT, OUT_SW>(stg + 2 * out1_off, trow, c * 16, b);
+        }
+      }
       return;
     }
   }
